@@ -1,0 +1,234 @@
+"""Seeded synthetic inputs for the five BASELINE.json configs (shared by tests, bench, smoke).
+
+This module holds NONE of the method's arithmetic (no basis evaluation, no quadrature,
+no integrand, no assembly).  It only draws the numbers both the CUDA path and the CPU
+oracle are handed bit-identically: open knot vectors, control points / weights of the
+synthetic geometries, physics parameters, and the solution coefficient arrays U, Udot.
+
+Recipes (SURVEY.md §8(d) table and readings A-19..A-23):
+
+cfg 1  Poisson validation (SPEC demo): [0,1]^2, open uniform p=2 knots, N x N elements,
+       identity geometry as NURBS with Greville control points and unit weights (A-19);
+       LAPLACE kappa=1, sigma=0, f = 2 pi^2 sin(pi x) sin(pi y); U = 0; (a,b) = (0,1).
+cfg 2  NURBS quarter annulus r in [1,2], theta in [0,pi/2] (P:55-58 exact geometry),
+       cubic C^2, N x N; homogeneous control points are the exact blossoms of the
+       quadratic (angular) x linear (radial) numerators (A-20); LAPLACE kappa=sigma=1, f=0;
+       U ~ U[-1,1] i.i.d. seed 2; (a,b) = (0,1).
+cfg 3  Cahn-Hilliard, [0,1]^2 periodic C^1 quadratic (the library unclamps the open knot
+       vector with Alg. 1), parametric geometry; c = 0.63 + U[-0.05,0.05] seed 3,
+       cdot = 0; theta=1.5, alpha=3000; a = alpha_m = 5/6, b = alpha_f*gamma*dt = (4/9)*1e-6
+       (rho_inf = 0.5).
+cfg 4  Neo-Hookean, [0,1]^3 open C^1 quadratic, parametric, 3 dofs/node, E=1, nu=0.3
+       (lambda, mu by A-13); u = 0.05 sum_{m<8} a_m sin(pi k_m.X + phi_m) sampled at the
+       Greville abscissae (A-22, A-23); (a,b) = (0,1).
+cfg 5  RBVMS Navier-Stokes, [0,2pi]^3 periodic C^1 quadratic, 4 dofs/node (u,v,w,p);
+       Taylor-Green velocity + 0.01*U[-1,1] seed 5 and its pressure at Greville points;
+       Udot = 0; nu = 1/1600, dt = 1e-2, C_t = 4, C_I = 36; a = 5/6, b = (4/9)*1e-2.
+"""
+from __future__ import annotations
+
+import itertools
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+PHYS_LAPLACE, PHYS_CAHN_HILLIARD, PHYS_NEOHOOKE, PHYS_NS_VMS = 0, 1, 2, 3
+GEOM_PARAMETRIC, GEOM_NURBS = 0, 1
+
+# full-size element counts per axis (BASELINE.json configs[0..4])
+FULL_N = {1: 16, 2: 256, 3: 1024, 4: 64, 5: 128}
+NAMES = {1: "poisson2d_p2_16x16", 2: "annulus_lapmass_p3_256x256", 3: "cahn_hilliard2d_p2_1024x1024",
+         4: "neohooke3d_p2_64x64x64", 5: "ns_vms3d_p2_128x128x128"}
+
+
+@dataclass
+class Workload:
+    cid: int
+    name: str
+    dim: int
+    degree: list
+    knots: list            # open (clamped) knot vectors, one np.float64 array per axis
+    periodic: list
+    continuity: list       # C^k across the periodic seam (only read when periodic)
+    dof: int
+    quad: list
+    geometry: int
+    ctrl: np.ndarray | None      # [n0][n1][n2][dim] Euclidean control points, or None
+    weights: np.ndarray | None   # [n0][n1][n2] projective weights, or None (=> 1)
+    phys: int
+    params: list
+    a: float
+    b: float
+    U: np.ndarray          # [n0*n1*n2*dof] dof innermost, last axis fastest
+    Udot: np.ndarray
+    nel: list = field(default_factory=list)
+    nfun: list = field(default_factory=list)   # unique functions per axis
+
+    @property
+    def ndof(self) -> int:
+        return int(np.prod(self.nfun)) * self.dof
+
+    @property
+    def nqp(self) -> int:
+        return int(np.prod(self.nel)) * int(np.prod(self.quad))
+
+    @property
+    def nelem(self) -> int:
+        return int(np.prod(self.nel))
+
+
+def open_uniform_knots(p: int, n: int, a: float = 0.0, b: float = 1.0) -> np.ndarray:
+    """p+1 copies of a, a+(b-a)i/n for i=1..n-1, p+1 copies of b (SURVEY O-1)."""
+    inner = [a + (b - a) * i / n for i in range(1, n)]
+    return np.array([a] * (p + 1) + inner + [b] * (p + 1), dtype=np.float64)
+
+
+def _greville(U: np.ndarray, p: int) -> np.ndarray:
+    """Sample locations (Greville abscissae) of an OPEN knot vector: (t_{i+1}+..+t_{i+p})/p."""
+    n = len(U) - p - 1
+    return np.array([sum(U[i + 1:i + p + 1]) / p for i in range(n)], dtype=np.float64)
+
+
+def _periodic_greville(a: float, b: float, n: int, p: int) -> np.ndarray:
+    """Sample locations for the n unique functions of a uniform C^{p-1} periodic space on [a,b]:
+    function g is centred at a + (g + (1-p)/2) h (h=(b-a)/n), i.e. the Greville abscissa of the
+    uniformly extended knots.  Only used to place the synthetic field samples."""
+    h = (b - a) / n
+    return np.array([a + (g + 0.5 * (1 - p)) * h for g in range(n)], dtype=np.float64)
+
+
+def _blossom_quadratic_in_cubic(c0: float, c1: float, c2: float, t: np.ndarray) -> float:
+    """Blossom of f(x)=c0+c1 x+c2 x^2 viewed as a cubic, at knots t1,t2,t3 (A-20)."""
+    t1, t2, t3 = t
+    return c0 + c1 * (t1 + t2 + t3) / 3.0 + c2 * (t1 * t2 + t1 * t3 + t2 * t3) / 3.0
+
+
+def annulus_geometry(U0: np.ndarray, U1: np.ndarray, p: int = 3):
+    """Exact quarter-annulus NURBS in the cubic space (A-20): xi0 radial r = 1 + xi0, xi1 angular.
+
+    Homogeneous numerators of the quadratic arc (P0=(1,0),P1=(1,1),P2=(0,1), w=(1,1/sqrt2,1)):
+      wx(t) = (1-t)^2 + sqrt2 t(1-t),  wy(t) = sqrt2 t(1-t) + t^2,  w(t) = (1-t)^2 + sqrt2 t(1-t) + t^2
+    expanded in the monomial basis; each B-spline coefficient is the blossom at its p interior knots.
+    """
+    s2 = math.sqrt(2.0)
+    # monomial coefficients (c0, c1, c2)
+    wx = (1.0, -2.0 + s2, 1.0 - s2)
+    wy = (0.0, s2, 1.0 - s2)
+    ww = (1.0, -2.0 + s2, 2.0 - s2)
+    n0 = len(U0) - p - 1
+    n1 = len(U1) - p - 1
+    R = np.array([_blossom_quadratic_in_cubic(1.0, 1.0, 0.0, U0[i + 1:i + p + 1]) for i in range(n0)])
+    WX = np.array([_blossom_quadratic_in_cubic(*wx, U1[j + 1:j + p + 1]) for j in range(n1)])
+    WY = np.array([_blossom_quadratic_in_cubic(*wy, U1[j + 1:j + p + 1]) for j in range(n1)])
+    W = np.array([_blossom_quadratic_in_cubic(*ww, U1[j + 1:j + p + 1]) for j in range(n1)])
+    ctrl = np.zeros((n0, n1, 2))
+    ctrl[:, :, 0] = R[:, None] * (WX / W)[None, :]
+    ctrl[:, :, 1] = R[:, None] * (WY / W)[None, :]
+    weights = np.broadcast_to(W[None, :], (n0, n1)).copy()
+    return ctrl, weights
+
+
+def make(cid: int, n: int | None = None, seed: int | None = None) -> Workload:
+    """Build config `cid` (1..5) with n elements per axis (default: the full BASELINE size)."""
+    if n is None:
+        n = FULL_N[cid]
+    if seed is None:
+        seed = cid
+    rng = np.random.default_rng(seed)
+    if cid == 1:
+        p, d = 2, 2
+        U = [open_uniform_knots(p, n) for _ in range(d)]
+        g = [_greville(u, p) for u in U]
+        nf = [len(x) for x in g]
+        ctrl = np.zeros((nf[0], nf[1], 2))
+        ctrl[:, :, 0] = g[0][:, None]
+        ctrl[:, :, 1] = g[1][None, :]
+        w = Workload(1, NAMES[1], d, [p] * d, U, [0] * d, [p - 1] * d, 1, [p + 1] * d, GEOM_NURBS,
+                     ctrl, np.ones(nf), PHYS_LAPLACE, [1.0, 0.0, 1.0], 0.0, 1.0,
+                     np.zeros(nf[0] * nf[1]), np.zeros(nf[0] * nf[1]), [n] * d, nf)
+    elif cid == 2:
+        p, d = 3, 2
+        U = [open_uniform_knots(p, n) for _ in range(d)]
+        ctrl, weights = annulus_geometry(U[0], U[1], p)
+        nf = [ctrl.shape[0], ctrl.shape[1]]
+        nd = nf[0] * nf[1]
+        w = Workload(2, NAMES[2], d, [p] * d, U, [0] * d, [p - 1] * d, 1, [p + 1] * d, GEOM_NURBS,
+                     ctrl, weights, PHYS_LAPLACE, [1.0, 1.0, 0.0], 0.0, 1.0,
+                     rng.uniform(-1.0, 1.0, nd), np.zeros(nd), [n] * d, nf)
+    elif cid == 3:
+        p, d = 2, 2
+        U = [open_uniform_knots(p, n) for _ in range(d)]
+        nf = [n, n]
+        nd = n * n
+        c = 0.63 + rng.uniform(-0.05, 0.05, nd)
+        dt = 1e-6
+        w = Workload(3, NAMES[3], d, [p] * d, U, [1] * d, [p - 1] * d, 1, [p + 1] * d, GEOM_PARAMETRIC,
+                     None, None, PHYS_CAHN_HILLIARD, [1.5, 3000.0], 5.0 / 6.0, (4.0 / 9.0) * dt,
+                     c, np.zeros(nd), [n] * d, nf)
+    elif cid == 4:
+        p, d = 2, 3
+        U = [open_uniform_knots(p, n) for _ in range(d)]
+        g = [_greville(u, p) for u in U]
+        nf = [len(x) for x in g]
+        # A-22: idx, phi, amplitude drawn in this order from default_rng(4)
+        kvecs = [k for k in itertools.product((0, 1), repeat=3) if any(k)]
+        idx = rng.integers(0, 7, 8)
+        phi = rng.uniform(0.0, 2.0 * math.pi, 8)
+        amp = rng.uniform(-1.0, 1.0, (8, 3))
+        X = np.stack(np.meshgrid(g[0], g[1], g[2], indexing="ij"), axis=-1)   # [n0,n1,n2,3]
+        disp = np.zeros(X.shape)
+        for m in range(8):
+            kv = np.array(kvecs[idx[m]], dtype=np.float64)
+            s = np.sin(math.pi * (X @ kv) + phi[m])
+            disp += amp[m][None, None, None, :] * s[..., None]
+        disp *= 0.05
+        E, nu = 1.0, 0.3
+        lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+        mu = E / (2 * (1 + nu))
+        w = Workload(4, NAMES[4], d, [p] * d, U, [0] * d, [p - 1] * d, 3, [p + 1] * d, GEOM_PARAMETRIC,
+                     None, None, PHYS_NEOHOOKE, [lam, mu], 0.0, 1.0,
+                     disp.reshape(-1).copy(), np.zeros(disp.size), [n] * d, nf)
+    elif cid == 5:
+        p, d = 2, 3
+        L = 2.0 * math.pi
+        U = [open_uniform_knots(p, n, 0.0, L) for _ in range(d)]
+        g = _periodic_greville(0.0, L, n, p)
+        x, y, z = np.meshgrid(g, g, g, indexing="ij")
+        vel = np.stack([np.sin(x) * np.cos(y) * np.cos(z),
+                        -np.cos(x) * np.sin(y) * np.cos(z),
+                        np.zeros_like(x)], axis=-1)
+        vel = vel + 0.01 * rng.uniform(-1.0, 1.0, vel.shape)
+        pres = (np.cos(2 * x) + np.cos(2 * y)) * (np.cos(2 * z) + 2.0) / 16.0
+        Uarr = np.concatenate([vel, pres[..., None]], axis=-1).reshape(-1).copy()
+        dt = 1e-2
+        w = Workload(5, NAMES[5], d, [p] * d, U, [1] * d, [p - 1] * d, 4, [p + 1] * d, GEOM_PARAMETRIC,
+                     None, None, PHYS_NS_VMS, [1.0 / 1600.0, dt, 4.0, 36.0], 5.0 / 6.0, (4.0 / 9.0) * dt,
+                     Uarr, np.zeros(Uarr.size), [n] * d, [n] * d)
+    else:
+        raise ValueError(f"unknown config {cid}")
+    return w
+
+
+def probe_rows(w: Workload, nblocks_random: int = 4, block: int = 3, seed: int = 5) -> np.ndarray:
+    """Sorted global dof rows for probe-block parity at full size (SURVEY O-10, reduced):
+    block^d node boxes at the low corner / seam, the middle (a partition plane), the
+    quarter point, the high corner, plus `nblocks_random` seeded random boxes; all dofs."""
+    nf = w.nfun
+    d = w.dim
+    rng = np.random.default_rng(seed)
+    starts = []
+    for frac in (0.0, 0.5, 0.25):
+        starts.append([int(frac * f) for f in nf])
+    starts.append([f - block for f in nf])
+    for _ in range(nblocks_random):
+        starts.append([int(rng.integers(0, f - block + 1)) for f in nf])
+    rows = set()
+    for s in starts:
+        for off in itertools.product(range(block), repeat=d):
+            node = 0
+            for ax in range(d):
+                node = node * nf[ax] + min(max(s[ax] + off[ax], 0), nf[ax] - 1)
+            for c in range(w.dof):
+                rows.add(node * w.dof + c)
+    return np.array(sorted(rows), dtype=np.int64)
