@@ -1,0 +1,363 @@
+#!/usr/bin/env python
+"""bench.py -- Jacobian-assembly throughput of libiga on B200 (BASELINE.json metric).
+
+One "step" = one iga_form_jacobian(a, b) call on the configured state that also forms the
+residual F in the same pass (every §8(a) hot-path row: basis tables are resident, the call does
+tensor product -> rational -> push-forward -> fields -> integrand -> element contraction ->
+CSR / F scatter).  Pattern build and space creation are setup, outside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl iga|reference]
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "Jacobian assembly quadrature points/sec (fp64)"
+UNIT = "qpts/s"
+DEFAULT_CONFIG = 2          # BASELINE.json configs[1]
+# Algorithmic model:
+#   F_J  = min over rank / test-side sum-factorised / sum-factorised contraction flops per qpt
+#   F_R  = residual rank-form flops per qpt;  B = CSR values written once + vectors, bytes per qpt
+F_J = {1: 72.0, 2: 672.0, 3: 738.0, 4: 9477.0, 5: 40986.0}
+F_R = {1: 108.0, 2: 192.0, 3: 198.0, 4: 972.0, 5: 2376.0}
+B_QP = {1: 25.6, 2: 25.8, 3: 24.9, 4: 348.0, 5: 596.0}
+# FP64 peak from unit counts and clock: 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
+P64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------
+# reference arm: the CPU oracle (as it stands) on a bounded sample of the same workload
+# ------------------------------------------------------------------------------------------
+def oracle_sample(w, target_s: float):
+    """Pick a node box whose complete rows take ~target_s in the oracle; returns (rows, est)."""
+    import oracle
+    osp = oracle.Space.from_workload(w)
+    nf = w.nfun
+
+    def box_rows(b):
+        import itertools
+        lo = [max(0, f // 2 - b // 2) for f in nf]
+        rows = []
+        for off in itertools.product(*[range(min(b, f)) for f in nf]):
+            node = 0
+            for ax in range(w.dim):
+                node = node * nf[ax] + lo[ax] + off[ax]
+            rows.extend(node * w.dof + c for c in range(w.dof))
+        return np.array(sorted(rows), dtype=np.int64)
+
+    b = 2
+    t0 = time.perf_counter()
+    r = osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, box_rows(b), Udot=w.Udot)
+    t1 = time.perf_counter() - t0
+    per_el = t1 / max(1, r["nvisited"])
+    # elements visited by a b-box ~ (b + p)^d
+    p = w.degree[0]
+    while b < max(nf):
+        nb = b * 2
+        if per_el * (nb + p) ** w.dim > target_s:
+            break
+        b = nb
+    return osp, box_rows(b), b
+
+
+def run_reference(args, w, ws, rank):
+    if rank != 0:
+        return 0
+    import oracle  # noqa: F401  (test infrastructure, allowed for the reference arm)
+    budget = 150.0
+    per_step = max(0.5, min(4.0, budget / max(1, args.steps + args.warmup)))
+    osp, rows, b = oracle_sample(w, per_step)
+    times, qp = [], []
+    nq = int(np.prod(w.quad))
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, rows, Udot=w.Udot)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            qp.append(r["nvisited"] * nq)
+    value = sum(qp) / sum(times)
+    sample = (f"complete rows of a {b}^{w.dim}-node box (all {w.dof} dofs, {len(rows)} rows) of {w.name}: "
+              f"{r['nvisited']} elements x {nq} qpts per step, single-threaded C oracle")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": w.name, "nqp_per_step": int(qp[0]), "l2": "host"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# product arm
+# ------------------------------------------------------------------------------------------
+def run_iga(args, w, ws, rank, local):
+    import torch
+    import paper_1305_4452_b200 as iga
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    sp = iga.Space.from_workload(w, device=local)
+    stream = torch.cuda.current_stream()
+    U = torch.from_numpy(w.U).to(dev)
+    Ud = torch.from_numpy(w.Udot).to(dev)
+    rp, ci = sp.csr_pattern()
+    vals = torch.empty(sp.nnz, dtype=torch.float64, device=dev)
+    F = torch.empty(sp.nrows, dtype=torch.float64, device=dev)
+    ph = iga.make_phys(w.phys, w.params)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # 512 MiB > 126 MB L2
+
+    def step():
+        sp.form_jacobian(ph, w.a, w.b, U, Ud, vals=vals, F=F)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    sp.check()
+    torch.cuda.synchronize()
+    launches_per_step = sp.last_launch_count()
+
+    def timed_region(nsteps, profile=False):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nsteps)]
+        if profile:
+            sp.profile(True)
+            sp.profile_reset()
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for i in range(nsteps):
+            flush.zero_()                       # L2 flush between timed iterations (not timed)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        prof = sp.profile_read() if profile else None
+        if profile:
+            sp.profile(False)
+        return [a.elapsed_time(b) for a, b in evs], prof
+
+    with ClockSampler(local) as clk:
+        ms, _ = timed_region(args.steps)
+    sp.check()
+    step_ms = sum(ms) / len(ms)
+    if ws > 1:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_ms = float(t.item())
+    nqp_total = sp.nqp * ws
+    value = nqp_total / (step_ms * 1e-3)
+
+    # per-kernel device times (second pass with the kernel timing hook on)
+    _, prof = timed_region(args.steps, profile=True)
+
+    # end-to-end through the host-buffer C-ABI call (pinned buffers, copies inside the timed region)
+    Uh = torch.from_numpy(w.U).pin_memory()
+    Udh = torch.from_numpy(w.Udot).pin_memory()
+    vh = torch.empty(sp.nnz, dtype=torch.float64).pin_memory()
+    fh = torch.empty(sp.nrows, dtype=torch.float64).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    sp.form_jacobian_host(ph, w.a, w.b, Uh, Udh, vh, fh)
+    e2e_ms = []
+    for _ in range(e2e_steps):
+        flush.zero_()
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_ev.record(stream)
+        sp.form_jacobian_host(ph, w.a, w.b, Uh, Udh, vh, fh)
+        b_ev.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a_ev.elapsed_time(b_ev))
+    e2e_val = nqp_total / (statistics.mean(e2e_ms) * 1e-3)
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    peaks = load_peaks()
+    # dominant kernel and its roofline (FP64-ALU bound)
+    kern = {k: v for k, v in prof.items()}
+    dom = max(kern, key=lambda k: kern[k][1])
+    n_l, tot_ms = kern[dom]
+    avg_ms = tot_ms / n_l
+    nqp_launch = sp.nqp / max(1, kern["k_contract"][0] // args.steps) if "k_contract" in kern else sp.nqp
+    cid = w.cid
+    if dom == "k_contract":
+        alg = (F_J[cid] + F_R[cid]) * nqp_launch
+        bound, unit, peak = "alu", "TFLOP/s", P64_NOMINAL_TFLOPS
+        achieved = alg / (avg_ms * 1e-3) / 1e12
+    elif dom == "k_point":
+        # pointwise stage: no algorithmic flops in the model; its HBM stream is the coefficient workspace
+        alg = None
+        bound, unit, peak = "alu", "TFLOP/s", P64_NOMINAL_TFLOPS
+        achieved = 0.0
+    else:
+        alg = 8.0 * sp.nnz
+        bound, unit, peak = "hbm", "GB/s", peaks.get("hbm_gbs", 6650.0)
+        achieved = alg / (avg_ms * 1e-3) / 1e9
+    traffic = None
+    summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(summ):
+        try:
+            traffic = json.load(open(summ)).get(w.name, {}).get(dom, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    t_roof = max((F_J[cid] + F_R[cid]) * sp.nqp / (P64_NOMINAL_TFLOPS * 1e12),
+                 B_QP[cid] * sp.nqp / (peaks.get("hbm_gbs", 6650.0) * 1e9))
+    clocks = clk.summary()
+
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        import oracle  # noqa: F401  (bench's cpu_baseline leg may execute the oracle)
+        osp, rows, b = oracle_sample(w, 4.0)
+        nq = int(np.prod(w.quad))
+        t0 = time.perf_counter()
+        r = osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, rows, Udot=w.Udot)
+        dt = time.perf_counter() - t0
+        reps = 1
+        while time.perf_counter() - t0 < 10.0 and reps < 8:
+            osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, rows, Udot=w.Udot)
+            reps += 1
+        dt = (time.perf_counter() - t0) / reps
+        cpu = {"value": r["nvisited"] * nq / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"complete Jacobian+residual rows of a {b}^{w.dim}-node box ({len(rows)} rows, "
+                         f"{r['nvisited']} elements x {nq} qpts) of {w.name}, {reps} reps, single-threaded C oracle"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "nqp": sp.nqp, "nelem": w.nelem, "ndof": sp.ndof, "nnz": sp.nnz,
+                   "degree": w.degree[0], "dof_per_node": w.dof, "l2": "flushed (512 MiB write) between steps",
+                   "step": "iga_form_jacobian(a,b) with residual F fused"},
+        "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
+                     "frac": achieved / peak if peak else None, "traffic": traffic,
+                     "peak_source": "148 SM x 64 DFMA/clk x 2 x 1.965 GHz (B200 unit counts, DESIGN.md)"
+                     if unit == "TFLOP/s" else "MEASURED_PEAKS.json hbm_gbs",
+                     "kernel_ms": {k: v[1] / v[0] for k, v in kern.items()},
+                     "kernel_launches_per_step": {k: v[0] / args.steps for k, v in kern.items()},
+                     "step_roofline_ms": t_roof * 1e3, "step_frac": t_roof * 1e3 / step_ms},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(2 * 8 * sp.ndof),
+                "d2h_bytes_per_step": int(8 * (sp.nnz + sp.nrows)), "ms_per_step": statistics.mean(e2e_ms)},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clocks,
+    }
+    print(json.dumps(out), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
+    ap.add_argument("--n", type=int, default=None, help="elements per axis (default: BASELINE size)")
+    ap.add_argument("--impl", default="iga", choices=["iga", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup) if args.impl == "iga" else args.warmup
+    ws, rank, local = dist_env()
+    w = workloads.make(args.config, n=args.n)
+    if args.impl == "reference":
+        return run_reference(args, w, ws, rank)
+    if ws > 1:
+        raise SystemExit("multi-GPU box decomposition is not wired into bench.py yet")
+    return run_iga(args, w, ws, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,153 @@
+/*
+ * iga.h -- C ABI of libiga: Galerkin residual / Jacobian assembly on tensor-product
+ * B-spline / NURBS spaces, B200 (sm_100a) fp64 CUDA.  arXiv:1305.4452 ("PetIGA").
+ *
+ * The four calls follow the paper's statement of the problem:
+ *   iga_space_create   -- an IGA space: dim, degree, knots, continuity (periodic
+ *                         unclamping, Alg. 1), control points and weights
+ *                         (NURBS, eqs. rational), dofs per node
+ *   iga_csr_pattern    -- the CSR nonzero pattern from the knot vectors (Alg. 3, P:468-484;
+ *                         "preallocation is crucial for efficient matrix assembly" P:444-446)
+ *   iga_form_residual  -- FormVector, Alg. 4
+ *   iga_form_jacobian  -- the matrix analogue, J = a dR/dUdot + b dR/dU
+ *                         (generalized-alpha Newton matrix)
+ *
+ * Conventions:
+ *  - Plain pointers only.  "device" = CUDA device memory on the space's device (allocated
+ *    by the caller, e.g. with torch); "host" = ordinary host memory.
+ *  - Numbering: node (i0,i1,i2) of the unique (periodic-identified) functions has flat index
+ *    (i0*n1 + i1)*n2 + i2 (last parametric axis fastest); global dof = node*dof + component.
+ *  - Vectors (U, Udot, F) are owned-rows-only in that order (single GPU: all rows).
+ *  - CSR: row_ptr int64 [nrows+1] (config 5 has 4.19e9 nonzeros > 2^31), col_idx int32 [nnz]
+ *    global dof indices, ascending within each row; csr_val fp64 [nnz].
+ *  - Every call that takes a cudaStream_t (passed as void*) is asynchronous on that stream
+ *    and allocates no device memory.  Buffers must stay alive until the stream reaches them.
+ *  - Errors: every call returns an iga_status; iga_last_error() gives a thread-local message.
+ *    Argument / knot / continuity validation is synchronous.  Device-side conditions
+ *    (detJ <= 0, SURVEY A-7; non-finite integrand) set a device flag that
+ *    iga_space_check() reports after a stream synchronisation.
+ *  - There is no CPU fallback: without a usable CUDA device every call fails with
+ *    IGA_ERR_CUDA.
+ */
+#ifndef IGA_H
+#define IGA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    IGA_OK = 0,
+    IGA_ERR_PARAM = 1,        /* bad argument / unsupported combination                 */
+    IGA_ERR_DOMAIN = 2,       /* knots not non-decreasing, continuity out of range, ...  */
+    IGA_ERR_SINGULAR_MAP = 3, /* detJ <= 0 at a quadrature point (A-7)                   */
+    IGA_ERR_PATTERN = 4,      /* a contribution outside the Alg. 3 pattern (debug)       */
+    IGA_ERR_NONFINITE = 5,    /* non-finite residual / Jacobian coefficient              */
+    IGA_ERR_CUDA = 6,
+    IGA_ERR_COMM = 7,
+    IGA_ERR_NOMEM = 8,
+    IGA_ERR_STATE = 9
+} iga_status;
+
+typedef struct iga_space_s *iga_space;    /* opaque, library-owned */
+
+typedef enum { IGA_GEOM_PARAMETRIC = 0, IGA_GEOM_NURBS = 1 } iga_geom;
+
+typedef struct {
+    int dim;                       /* 1..3 (parametric dim = spatial dim)                      */
+    int degree[3];                 /* p_d in [1,3] in this build                               */
+    int n_knots[3];                /* knots on axis d                                          */
+    const double *knots[3];        /* host; OPEN (clamped) knot vectors, non-decreasing        */
+    int periodic[3];               /* 1 => unclamp axis d with Alg. 1 for C^k periodicity      */
+    int periodic_continuity[3];    /* k_d in [0, p_d-1] (read only when periodic)              */
+    int dof;                       /* m dofs per node, 1..4                                    */
+    int quad[3];                   /* Gauss points per dimension; 0 => p_d+1 (only p+1 here)   */
+    int geometry;                  /* iga_geom: PARAMETRIC => x = xi (knots carry coordinates)  */
+    const double *ctrl;            /* host [n0][n1][n2][dim] Euclidean control points (NURBS)  */
+    const double *weights;         /* host [n0][n1][n2] projective weights > 0, NULL => 1      */
+} iga_space_desc;
+
+/* Box decomposition of the element grid over ranks.
+ * NULL => one rank owns everything. procs[d] ranks along axis d, rank = (r0*p1+r1)*p2+r2. */
+typedef struct {
+    int rank;
+    int nranks;
+    int procs[3];
+} iga_dist;
+
+/* Create a space on CUDA device `device`.  Copies all host inputs.  Builds the per-axis
+ * quadrature rule (Gauss-Legendre, A-6), the 1D basis tables at the Gauss points (kernel K1)
+ * and the per-axis Alg. 3 stencils.  Returns IGA_ERR_DOMAIN for invalid knots. */
+iga_status iga_space_create(const iga_space_desc *desc, const iga_dist *dist, int device,
+                            iga_space *out);
+iga_status iga_space_destroy(iga_space s);
+
+/* Sizes (host outputs; any pointer may be NULL):
+ *   ndof_global  -- total dofs;  nrows_owned -- rows this rank owns;  nnz_owned -- nonzeros
+ *   in those rows;  nqp_local -- quadrature points of this rank's elements;
+ *   owned_lo/hi[3] -- owned node box [lo,hi) per axis;  elem_lo/hi[3] -- element box. */
+iga_status iga_space_info(iga_space s, int64_t *ndof_global, int64_t *nrows_owned,
+                          int64_t *nnz_owned, int64_t *nqp_local, int64_t owned_lo[3],
+                          int64_t owned_hi[3], int64_t elem_lo[3], int64_t elem_hi[3]);
+
+/* CSR pattern of the owned rows (kernel K2): Alg. 3 per axis x tensor product x dof blocks,
+ * sorted ascending.  row_ptr: device int64[nrows_owned+1] (starts at 0); col_idx: device
+ * int32[nnz_owned].  stream: cudaStream_t. */
+iga_status iga_csr_pattern(iga_space s, int64_t *row_ptr, int32_t *col_idx, void *stream);
+
+/* Physics (the paper's "user integrand", is a closed set here) */
+typedef enum {
+    IGA_PHYS_LAPLACE = 0,        /* p = [kappa, sigma, source_id]; m = 1                      */
+    IGA_PHYS_CAHN_HILLIARD = 1,  /* p = [theta, alpha]; m = 1; needs Hessians      */
+    IGA_PHYS_NEOHOOKE = 2,       /* p = [lambda, mu]; m = 3, dim 3                 */
+    IGA_PHYS_NS_VMS = 3          /* p = [nu, dt, C_t, C_I]; m = 4, dim 3, parametric*/
+} iga_phys_kind;
+
+typedef struct {
+    int kind;
+    double p[8];
+} iga_phys;
+
+/* Residual R(U, Udot) (Alg. 4).  U, Udot: device fp64 [ndof_global] (single rank) -- Udot may
+ * be NULL (=> 0).  F: device fp64 [nrows_owned], overwritten. */
+iga_status iga_form_residual(iga_space s, const iga_phys *phys, const double *U,
+                             const double *Udot, double *F, void *stream);
+
+/* Jacobian J = a dR/dUdot + b dR/dU into csr_val (device fp64 [nnz_owned], overwritten, in
+ * the order of iga_csr_pattern); if F is non-NULL the residual is formed in the same pass. */
+iga_status iga_form_jacobian(iga_space s, const iga_phys *phys, double a, double b,
+                             const double *U, const double *Udot, double *csr_val, double *F,
+                             void *stream);
+
+/* Host-buffer variant (end-to-end path): copies U/Udot host->device, forms J (and F if
+ * F_host != NULL) and copies csr_val / F back, all on `stream`; returns after the stream
+ * synchronises.  Host buffers should be pinned for full PCIe bandwidth. */
+iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, double b,
+                                  const double *U_host, const double *Udot_host,
+                                  double *csr_val_host, double *F_host, void *stream);
+
+/* Synchronises `stream` and reports (then clears) the device error flag of the last form
+ * call: IGA_OK, IGA_ERR_SINGULAR_MAP or IGA_ERR_NONFINITE. */
+iga_status iga_space_check(iga_space s, void *stream);
+
+/* Number of kernel launches the last form / pattern call issued (for the bench's gpu_launches). */
+int iga_last_launch_count(iga_space s);
+
+/* Kernel-level timing hook (bench only).  When enabled, every kernel a call launches is
+ * bracketed by CUDA events recorded on that call's stream.  iga_profile_read synchronises the
+ * recorded events and returns, per kernel name (up to `max` names of < 32 chars), the number
+ * of launches and the summed device time in ms since the last reset; returns the count of
+ * names, or -1 on error. */
+iga_status iga_profile_enable(iga_space s, int on);
+iga_status iga_profile_reset(iga_space s);
+int iga_profile_read(iga_space s, int max, char *names /* [max][32] */, int *launches, double *ms);
+
+const char *iga_last_error(void);
+const char *iga_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGA_H */

@@ -548,7 +548,7 @@ typedef struct {
     /* CH */
     double M, Mp, Mpp, mup, mupp;
     /* NH */
-    double F[3][3], S[3][3], P[3][3], Ci[3][3], J;
+    double F[3][3], S[3][3], P[3][3], Ci[3][3], J, AA[3][3][3][3];
     /* VMS */
     double tauM, tauC, rM[3], rC, up[3], pp;
 } orc_pt;
@@ -609,6 +609,21 @@ static double nh_CC(const orc_pt *P, int I, int J, int K, int L)
     double lam = P->prm[0], mu = P->prm[1];
     return lam * P->J * P->J * P->Ci[I][J] * P->Ci[K][L]
          + (mu - lam * (P->J * P->J - 1.0) / 2.0) * (P->Ci[I][K] * P->Ci[J][L] + P->Ci[I][L] * P->Ci[J][K]);
+}
+
+/* AA_aIbJ = delta_ab S_IJ + F_aK C_KILJ F_bL, once per point */
+static void nh_tangent(orc_pt *P)
+{
+    for (int a = 0; a < 3; a++)
+        for (int I = 0; I < 3; I++)
+            for (int bb = 0; bb < 3; bb++)
+                for (int J = 0; J < 3; J++) {
+                    double AA = (a == bb ? P->S[I][J] : 0.0);
+                    for (int Kk = 0; Kk < 3; Kk++)
+                        for (int L = 0; L < 3; L++)
+                            AA += P->F[a][Kk] * nh_CC(P, Kk, I, L, J) * P->F[bb][L];
+                    P->AA[a][I][bb][J] = AA;
+                }
 }
 
 /* RBVMS (readings A-14, A-15). prm = [nu, dt, C_t, C_I].
@@ -749,13 +764,7 @@ static void jacobian_at(const orc_pt *P, const orc_qp *Q, const orc_fields *f, i
             for (int bb = 0; bb < 3; bb++) {
                 double v = 0.0;
                 for (int I = 0; I < 3; I++)
-                    for (int J = 0; J < 3; J++) {
-                        double AA = (a == bb ? P->S[I][J] : 0.0);
-                        for (int Kk = 0; Kk < 3; Kk++)
-                            for (int L = 0; L < 3; L++)
-                                AA += P->F[a][Kk] * nh_CC(P, Kk, I, L, J) * P->F[bb][L];
-                        v += dNA[I] * AA * dNB[J];
-                    }
+                    for (int J = 0; J < 3; J++) v += dNA[I] * P->AA[a][I][bb][J] * dNB[J];
                 K[a * 3 + bb] = P->b * v;
             }
         break;
@@ -862,7 +871,7 @@ static int element_integrate(const orc_space *s, int kind, const double *prm, do
                 memset(&P, 0, sizeof(P));
                 P.kind = kind; P.dim = dim; P.m = m; P.prm = prm; P.a = a; P.b = b;
                 if (kind == ORC_CAHN_HILLIARD) ch_setup(&P, &f);
-                if (kind == ORC_NEOHOOKE) nh_setup(&P, &f);
+                if (kind == ORC_NEOHOOKE) { nh_setup(&P, &f); if (want_K) nh_tangent(&P); }
                 if (kind == ORC_NS_VMS) {
                     if (Utau) { eval_fields(s, &Q, Utau, Udot, &ftau); vms_tau(&P, &Q, &ftau); }
                     else vms_tau(&P, &Q, &f);

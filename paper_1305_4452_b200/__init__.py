@@ -1,0 +1,240 @@
+"""paper_1305_4452_b200 -- thin Python binding of libiga (include/iga.h).
+
+Argument marshalling only: every step of the assembly runs in libiga's CUDA kernels for
+sm_100a.  torch provides device memory and streams.  There is no CPU fallback: if libiga.so
+is missing or no CUDA device is present, the calls raise.
+
+    sp = Space(dim, degree, knots, periodic, continuity, dof, quad, geometry, ctrl, weights)
+    row_ptr, col_idx = sp.csr_pattern()
+    F = sp.form_residual(phys, U, Udot)
+    vals, F = sp.form_jacobian(phys, a, b, U, Udot, want_F=True)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libiga.so")
+
+PHYS_LAPLACE, PHYS_CAHN_HILLIARD, PHYS_NEOHOOKE, PHYS_NS_VMS = 0, 1, 2, 3
+GEOM_PARAMETRIC, GEOM_NURBS = 0, 1
+_STATUS = ["OK", "ERR_PARAM", "ERR_DOMAIN", "ERR_SINGULAR_MAP", "ERR_PATTERN", "ERR_NONFINITE",
+           "ERR_CUDA", "ERR_COMM", "ERR_NOMEM", "ERR_STATE"]
+
+
+class IgaError(RuntimeError):
+    def __init__(self, code, msg):
+        self.code = code
+        super().__init__(f"libiga {_STATUS[code] if 0 <= code < len(_STATUS) else code}: {msg}")
+
+
+class _Desc(C.Structure):
+    _fields_ = [("dim", C.c_int), ("degree", C.c_int * 3), ("n_knots", C.c_int * 3),
+                ("knots", C.POINTER(C.c_double) * 3), ("periodic", C.c_int * 3),
+                ("periodic_continuity", C.c_int * 3), ("dof", C.c_int), ("quad", C.c_int * 3),
+                ("geometry", C.c_int), ("ctrl", C.POINTER(C.c_double)), ("weights", C.POINTER(C.c_double))]
+
+
+class _Dist(C.Structure):
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("procs", C.c_int * 3)]
+
+
+class _Phys(C.Structure):
+    _fields_ = [("kind", C.c_int), ("p", C.c_double * 8)]
+
+
+_lib = None
+
+EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
+           "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
+           "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read"]
+
+
+def lib():
+    """Load libiga.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1305_4452_b200.build` "
+                              "(libiga has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        dp = C.POINTER(C.c_double)
+        lp = C.POINTER(C.c_int64)
+        L.iga_space_create.argtypes = [C.POINTER(_Desc), C.POINTER(_Dist), C.c_int, C.POINTER(vp)]
+        L.iga_space_destroy.argtypes = [vp]
+        L.iga_space_info.argtypes = [vp, lp, lp, lp, lp, lp, lp, lp, lp]
+        L.iga_csr_pattern.argtypes = [vp, vp, vp, vp]
+        L.iga_form_residual.argtypes = [vp, C.POINTER(_Phys), vp, vp, vp, vp]
+        L.iga_form_jacobian.argtypes = [vp, C.POINTER(_Phys), C.c_double, C.c_double, vp, vp, vp, vp, vp]
+        L.iga_form_jacobian_host.argtypes = [vp, C.POINTER(_Phys), C.c_double, C.c_double, vp, vp, vp, vp, vp]
+        L.iga_space_check.argtypes = [vp, vp]
+        L.iga_last_launch_count.argtypes = [vp]
+        L.iga_last_launch_count.restype = C.c_int
+        L.iga_profile_enable.argtypes = [vp, C.c_int]
+        L.iga_profile_reset.argtypes = [vp]
+        L.iga_profile_read.argtypes = [vp, C.c_int, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.iga_profile_read.restype = C.c_int
+        L.iga_last_error.restype = C.c_char_p
+        L.iga_version.restype = C.c_char_p
+        for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
+                  "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
+                  "iga_profile_reset"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code != 0:
+        raise IgaError(code, lib().iga_last_error().decode())
+
+
+def _ptr(t):
+    """Raw data pointer of a torch tensor or numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return C.c_void_p(t.data_ptr())
+    return C.c_void_p(t.ctypes.data)
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def make_phys(kind: int, params) -> _Phys:
+    ph = _Phys()
+    ph.kind = kind
+    for i, v in enumerate(params):
+        ph.p[i] = float(v)
+    return ph
+
+
+class Space:
+    """An IGA space on one CUDA device (iga_space_create).  Inputs are host arrays."""
+
+    def __init__(self, dim, degree, knots, periodic, continuity, dof, quad, geometry, ctrl=None, weights=None,
+                 device: int = 0, dist=None):
+        L = lib()
+        d = _Desc()
+        d.dim = dim
+        self._keep = []
+        for a in range(3):
+            if a < dim:
+                k = np.ascontiguousarray(knots[a], dtype=np.float64)
+                self._keep.append(k)
+                d.degree[a] = int(degree[a])
+                d.n_knots[a] = len(k)
+                d.knots[a] = k.ctypes.data_as(C.POINTER(C.c_double))
+                d.periodic[a] = int(periodic[a])
+                d.periodic_continuity[a] = int(continuity[a])
+                d.quad[a] = int(quad[a]) if quad is not None else 0
+        d.dof = dof
+        d.geometry = geometry
+        if ctrl is not None:
+            c = np.ascontiguousarray(ctrl, dtype=np.float64).reshape(-1)
+            self._keep.append(c)
+            d.ctrl = c.ctypes.data_as(C.POINTER(C.c_double))
+        if weights is not None:
+            w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+            self._keep.append(w)
+            d.weights = w.ctypes.data_as(C.POINTER(C.c_double))
+        dd = None
+        if dist is not None:
+            dd = _Dist()
+            dd.rank, dd.nranks = dist["rank"], dist["nranks"]
+            for a in range(3):
+                dd.procs[a] = dist["procs"][a] if a < len(dist["procs"]) else 1
+        h = C.c_void_p()
+        _check(L.iga_space_create(C.byref(d), C.byref(dd) if dd is not None else None, device, C.byref(h)))
+        self.h = h
+        self.dim, self.dof, self.device = dim, dof, device
+        v = [C.c_int64() for _ in range(4)]
+        lo, hi, elo, ehi = [(C.c_int64 * 3)() for _ in range(4)]
+        _check(L.iga_space_info(h, *[C.byref(x) for x in v], lo, hi, elo, ehi))
+        self.ndof, self.nrows, self.nnz, self.nqp = [x.value for x in v]
+        self.owned_lo, self.owned_hi = list(lo), list(hi)
+        self.elem_lo, self.elem_hi = list(elo), list(ehi)
+
+    @classmethod
+    def from_workload(cls, w, device: int = 0, dist=None):
+        return cls(w.dim, w.degree, w.knots, w.periodic, w.continuity, w.dof, w.quad, w.geometry, w.ctrl,
+                   w.weights, device=device, dist=dist)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().iga_space_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- calls -------------------------------------------------------------------------------
+    def csr_pattern(self, row_ptr=None, col_idx=None, stream=None):
+        import torch
+        dev = torch.device("cuda", self.device)
+        if row_ptr is None:
+            row_ptr = torch.empty(self.nrows + 1, dtype=torch.int64, device=dev)
+        if col_idx is None:
+            col_idx = torch.empty(self.nnz, dtype=torch.int32, device=dev)
+        _check(lib().iga_csr_pattern(self.h, _ptr(row_ptr), _ptr(col_idx), _stream(stream)))
+        return row_ptr, col_idx
+
+    def form_residual(self, phys, U, Udot=None, F=None, stream=None):
+        import torch
+        if F is None:
+            F = torch.empty(self.nrows, dtype=torch.float64, device=U.device)
+        _check(lib().iga_form_residual(self.h, C.byref(phys), _ptr(U), _ptr(Udot), _ptr(F), _stream(stream)))
+        return F
+
+    def form_jacobian(self, phys, a, b, U, Udot=None, vals=None, F=None, want_F=False, stream=None):
+        import torch
+        if vals is None:
+            vals = torch.empty(self.nnz, dtype=torch.float64, device=U.device)
+        if want_F and F is None:
+            F = torch.empty(self.nrows, dtype=torch.float64, device=U.device)
+        _check(lib().iga_form_jacobian(self.h, C.byref(phys), float(a), float(b), _ptr(U), _ptr(Udot), _ptr(vals),
+                                       _ptr(F), _stream(stream)))
+        return vals, F
+
+    def form_jacobian_host(self, phys, a, b, U_host, Udot_host, vals_host, F_host=None, stream=None):
+        _check(lib().iga_form_jacobian_host(self.h, C.byref(phys), float(a), float(b), _ptr(U_host),
+                                            _ptr(Udot_host), _ptr(vals_host), _ptr(F_host), _stream(stream)))
+        return vals_host, F_host
+
+    def check(self, stream=None):
+        _check(lib().iga_space_check(self.h, _stream(stream)))
+
+    def last_launch_count(self) -> int:
+        return int(lib().iga_last_launch_count(self.h))
+
+    def profile(self, on: bool = True):
+        _check(lib().iga_profile_enable(self.h, int(on)))
+
+    def profile_reset(self):
+        _check(lib().iga_profile_reset(self.h))
+
+    def profile_read(self) -> dict:
+        """{kernel name: (launches, total ms)} since the last reset (synchronises)."""
+        mx = 32
+        names = C.create_string_buffer(32 * mx)
+        cnt = (C.c_int * mx)()
+        ms = (C.c_double * mx)()
+        n = lib().iga_profile_read(self.h, mx, names, cnt, ms)
+        if n < 0:
+            raise IgaError(1, lib().iga_last_error().decode())
+        out = {}
+        for k in range(min(n, mx)):
+            nm = names.raw[32 * k:32 * k + 32].split(b"\0", 1)[0].decode()
+            out[nm] = (int(cnt[k]), float(ms[k]))
+        return out

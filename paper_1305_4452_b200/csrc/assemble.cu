@@ -1,0 +1,678 @@
+// assemble.cu -- residual / Jacobian assembly kernels (Alg. 4) for sm_100a, fp64.
+//
+// Two kernels per batch of elements:
+//   K3a  k_point     one thread per (element, quadrature point): 1D tables -> tensor-product
+//                    kinds -> rational basis and isoparametric push-forward
+//                    (folded into the map T) -> fields U_e -> physics -> the compact
+//                    coefficient lists r~ and D~ written to the HBM workspace (SoA, coalesced).
+//   K3b  k_contract  one CTA per element: stages the element's 1D tables and coefficients in
+//                    shared memory, contracts  K_e = w_A w_B sum_q P(A,q)^T D~(q) P(B,q)
+//                    (rank form, compile-time sparse), F_e likewise, and scatter-adds the
+//                    dense element blocks into the CSR values / F at positions computed in
+//                    closed form from the per-axis Alg. 3 stencils (no search).
+// DESIGN.md documents the data layout and the roofline of each kernel.
+#include <cstdio>
+#include <type_traits>
+
+#include "iga_host.h"
+#include "kinds.cuh"
+#include "physics.cuh"
+
+namespace iga {
+
+struct Prm { double p[8]; };
+
+__host__ __device__ constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+__device__ __forceinline__ void elem_coords(const SpaceDev &s, long long el, int e[3]) {
+    const int n1 = s.ax[1].el_hi - s.ax[1].el_lo, n2 = s.ax[2].el_hi - s.ax[2].el_lo;
+    e[2] = s.ax[2].el_lo + (int)(el % n2);
+    el /= n2;
+    e[1] = s.ax[1].el_lo + (int)(el % n1);
+    el /= n1;
+    e[0] = s.ax[0].el_lo + (int)el;
+}
+
+// value of separable contraction kind C of local function (a0,a1,a2) from 1D tables v[d][k][a]
+template <class KS, int DIM, int C, int NP1, class V>
+__device__ __forceinline__ double kind_value(const V &v, const int *aa, int /*unused*/ = 0) {
+    double s = 0.0;
+    static_for<KS::nterms(C)>([&](auto T) {
+        constexpr int t = decltype(T)::value;
+        double prod = 1.0;
+        static_for<DIM>([&](auto D) {
+            constexpr int d = decltype(D)::value;
+            prod *= v[d][KS::ord(C, t, d)][aa[d]];
+        });
+        s += prod;
+    });
+    return s;
+}
+
+// ============================================================================================
+// K3a: pointwise kernel
+// ============================================================================================
+template <int DIM, int P, class PH, int MODE, bool JAC>
+__global__ void __launch_bounds__(128)
+k_point(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
+        double *__restrict__ Dt, double *__restrict__ Rt, long long e0, int nb, long long ldq) {
+    using L = Lists<PH, DIM, MODE>;
+    using KS = typename L::KS;
+    constexpr int M = PH::M, NQ1 = P + 1, NP1 = P + 1;
+    constexpr int NQ = ipow(NQ1, DIM);
+    constexpr int NKS = KS::NKS, NC = KS::NC;
+    constexpr bool HESS = PH::HESS;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long long)nb * NQ) return;
+    const int q = (int)(t % NQ);
+    int e[3];
+    elem_coords(s, e0 + t / NQ, e);
+    int qd[3] = {0, 0, 0};
+    {
+        int r = q;
+#pragma unroll
+        for (int d = DIM - 1; d >= 0; d--) { qd[d] = r % NQ1; r /= NQ1; }
+    }
+    double v[DIM][3][NP1];
+    double wq = 1.0, xq[DIM], hp[DIM];
+    int first[DIM];
+#pragma unroll
+    for (int d = 0; d < DIM; d++) {
+        const double *tp = s.ax[d].tab + (size_t)(e[d] * NQ1 + qd[d]) * 3 * NP1;
+#pragma unroll
+        for (int k = 0; k < 3; k++)
+#pragma unroll
+            for (int aa = 0; aa < NP1; aa++) v[d][k][aa] = __ldg(tp + k * NP1 + aa);
+        wq *= __ldg(s.ax[d].qw + e[d] * NQ1 + qd[d]);
+        xq[d] = __ldg(s.ax[d].qx + e[d] * NQ1 + qd[d]);
+        hp[d] = __ldg(s.ax[d].hpar + e[d]);
+        first[d] = __ldg(s.ax[d].first + e[d]);
+    }
+    double Phi[M][NC], Phit[M], W[NC], X[DIM][NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        W[c] = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; m++) Phi[m][c] = 0.0;
+#pragma unroll
+        for (int i = 0; i < DIM; i++) X[i][c] = 0.0;
+    }
+#pragma unroll
+    for (int m = 0; m < M; m++) Phit[m] = 0.0;
+    const bool nurbs_geom = (MODE == MODE_NURBS) && s.geom == IGA_GEOM_NURBS;
+
+    constexpr int NEN = ipow(NP1, DIM);
+#pragma unroll 1
+    for (int A = 0; A < NEN; A++) {
+        int aa[3] = {0, 0, 0};
+        {
+            int r = A;
+#pragma unroll
+            for (int d = DIM - 1; d >= 0; d--) { aa[d] = r % NP1; r /= NP1; }
+        }
+        int g[3] = {0, 0, 0};
+#pragma unroll
+        for (int d = 0; d < DIM; d++) {
+            g[d] = first[d] + aa[d];
+            if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
+        }
+        const long long node = node_index(s, g[0], g[1], g[2]);
+        double Pc[NC];
+        static_for<NC>([&](auto C) {
+            constexpr int c = decltype(C)::value;
+            Pc[c] = kind_value<KS, DIM, c, NP1>(v, aa);
+        });
+        double wA = 1.0;
+        if (MODE == MODE_NURBS) {
+            if (s.wts) wA = __ldg(s.wts + node);
+#pragma unroll
+            for (int c = 0; c < NC; c++) W[c] += wA * Pc[c];
+            if (nurbs_geom) {
+#pragma unroll
+                for (int i = 0; i < DIM; i++) {
+                    const double xA = wA * __ldg(s.ctrl + node * DIM + i);
+#pragma unroll
+                    for (int c = 0; c < NC; c++) X[i][c] += xA * Pc[c];
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const double uA = wA * __ldg(U + node * M + m);
+#pragma unroll
+            for (int c = 0; c < NC; c++) Phi[m][c] += uA * Pc[c];
+            if (Ud) Phit[m] += wA * __ldg(Ud + node * M + m) * Pc[0];
+        }
+    }
+
+    Fields<DIM, M> F;
+    double T[NKS][NC];
+    double dV;
+    bool bad = false;
+    if (MODE == MODE_PARAM) {
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            F.u[m] = Phi[m][0];
+#pragma unroll
+            for (int i = 0; i < DIM; i++) F.gu[m][i] = Phi[m][1 + i];
+            F.lu[m] = HESS ? Phi[m][NKS - 1] : 0.0;
+            F.ut[m] = Phit[m];
+        }
+#pragma unroll
+        for (int i = 0; i < DIM; i++) {
+            F.x[i] = xq[i];
+            F.hpar[i] = hp[i];
+#pragma unroll
+            for (int j = 0; j < DIM; j++) F.dxi[i][j] = (i == j) ? 1.0 : 0.0;
+        }
+        dV = wq;
+#pragma unroll
+        for (int k = 0; k < NKS; k++)
+#pragma unroll
+            for (int c = 0; c < NC; c++) T[k][c] = (k == c) ? 1.0 : 0.0;
+    } else {
+        // rational kinds as combinations of parametric kinds (drational P:234, ddrational P:245)
+        const double w = W[0], iw = 1.0 / w;
+        double rR[NC], rA[DIM][NC], rAB[HESS ? KS::NH : 1][NC];
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            rR[c] = (c == 0 ? 1.0 : 0.0) * iw;
+#pragma unroll
+            for (int al = 0; al < DIM; al++) rA[al][c] = ((c == 1 + al ? 1.0 : 0.0) - W[1 + al] * rR[c]) * iw;
+        }
+        if (HESS) {
+#pragma unroll
+            for (int h = 0; h < KS::NH; h++) {
+                const int al = KS::hal(h), be = KS::hbe(h);
+#pragma unroll
+                for (int c = 0; c < NC; c++)
+                    rAB[h][c] = ((c == 1 + DIM + h ? 1.0 : 0.0) - W[1 + DIM + h] * rR[c] - W[1 + al] * rA[be][c]
+                                 - W[1 + be] * rA[al][c]) * iw;
+            }
+        }
+        // isoparametric map by the quotient rule on the homogeneous sums
+        double x[DIM], xa[DIM][DIM], xab[DIM][HESS ? KS::NH : 1];
+#pragma unroll
+        for (int i = 0; i < DIM; i++) {
+            if (nurbs_geom) {
+                x[i] = X[i][0] * iw;
+#pragma unroll
+                for (int al = 0; al < DIM; al++) xa[i][al] = (X[i][1 + al] - x[i] * W[1 + al]) * iw;
+                if (HESS) {
+#pragma unroll
+                    for (int h = 0; h < KS::NH; h++) {
+                        const int al = KS::hal(h), be = KS::hbe(h);
+                        xab[i][h] = (X[i][1 + DIM + h] - x[i] * W[1 + DIM + h] - xa[i][be] * W[1 + al]
+                                     - xa[i][al] * W[1 + be]) * iw;
+                    }
+                }
+            } else {
+                x[i] = xq[i];
+#pragma unroll
+                for (int al = 0; al < DIM; al++) xa[i][al] = (i == al) ? 1.0 : 0.0;
+#pragma unroll
+                for (int h = 0; h < (HESS ? KS::NH : 1); h++) xab[i][h] = 0.0;
+            }
+        }
+        // inverse map xi_{alpha,i} (identity P:287, derividentity P:292 as a matrix inverse)
+        double det, Xi[DIM][DIM];
+        if constexpr (DIM == 2) {
+            det = xa[0][0] * xa[1][1] - xa[0][1] * xa[1][0];
+            const double id = 1.0 / det;
+            Xi[0][0] = xa[1][1] * id;
+            Xi[0][1] = -xa[0][1] * id;
+            Xi[1][0] = -xa[1][0] * id;
+            Xi[1][1] = xa[0][0] * id;
+        } else {
+            const double c00 = xa[1][1] * xa[2][2] - xa[1][2] * xa[2][1];
+            const double c01 = xa[1][2] * xa[2][0] - xa[1][0] * xa[2][2];
+            const double c02 = xa[1][0] * xa[2][1] - xa[1][1] * xa[2][0];
+            det = xa[0][0] * c00 + xa[0][1] * c01 + xa[0][2] * c02;
+            const double id = 1.0 / det;
+            // Xi = adj(xa) / det, Xi[alpha][i]
+            Xi[0][0] = c00 * id;
+            Xi[1][0] = c01 * id;
+            Xi[2][0] = c02 * id;
+            Xi[0][1] = (xa[0][2] * xa[2][1] - xa[0][1] * xa[2][2]) * id;
+            Xi[1][1] = (xa[0][0] * xa[2][2] - xa[0][2] * xa[2][0]) * id;
+            Xi[2][1] = (xa[0][1] * xa[2][0] - xa[0][0] * xa[2][1]) * id;
+            Xi[0][2] = (xa[0][1] * xa[1][2] - xa[0][2] * xa[1][1]) * id;
+            Xi[1][2] = (xa[0][2] * xa[1][0] - xa[0][0] * xa[1][2]) * id;
+            Xi[2][2] = (xa[0][0] * xa[1][1] - xa[0][1] * xa[1][0]) * id;
+        }
+        if (!(det > 0.0)) bad = true;
+        // T rows: spatial kinds from rational kinds (dspatial P:309, ddspatial P:310)
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            T[0][c] = rR[c];
+#pragma unroll
+            for (int i = 0; i < DIM; i++) {
+                double sum = 0.0;
+#pragma unroll
+                for (int al = 0; al < DIM; al++) sum += Xi[al][i] * rA[al][c];
+                T[1 + i][c] = sum;
+            }
+        }
+        if (HESS) {
+            // xi_{nu,nl} = - x_{m,eps mu} xi_{eps,n} xi_{mu,l} xi_{nu,m}, only n = l needed
+            double Xi2d[DIM][DIM];   // [nu][n] = xi_{nu,nn}
+#pragma unroll
+            for (int nu_ = 0; nu_ < DIM; nu_++)
+#pragma unroll
+                for (int n = 0; n < DIM; n++) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int m = 0; m < DIM; m++)
+#pragma unroll
+                        for (int ep = 0; ep < DIM; ep++)
+#pragma unroll
+                            for (int mu = 0; mu < DIM; mu++)
+                                sum -= xab[m][KS::hidx(ep, mu)] * Xi[ep][n] * Xi[mu][n] * Xi[nu_][m];
+                    Xi2d[nu_][n] = sum;
+                }
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                double sum = 0.0;
+#pragma unroll
+                for (int i = 0; i < DIM; i++) {
+#pragma unroll
+                    for (int al = 0; al < DIM; al++) {
+#pragma unroll
+                        for (int be = 0; be < DIM; be++) sum += Xi[al][i] * Xi[be][i] * rAB[KS::hidx(al, be)][c];
+                        sum += Xi2d[al][i] * rA[al][c];
+                    }
+                }
+                T[NKS - 1][c] = sum;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            double u0 = 0.0, l0 = 0.0;
+            double gg[DIM];
+#pragma unroll
+            for (int i = 0; i < DIM; i++) gg[i] = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; c++) {
+                u0 += T[0][c] * Phi[m][c];
+#pragma unroll
+                for (int i = 0; i < DIM; i++) gg[i] += T[1 + i][c] * Phi[m][c];
+                if (HESS) l0 += T[NKS - 1][c] * Phi[m][c];
+            }
+            F.u[m] = u0;
+            F.lu[m] = l0;
+            F.ut[m] = Phit[m] * iw;
+#pragma unroll
+            for (int i = 0; i < DIM; i++) F.gu[m][i] = gg[i];
+        }
+#pragma unroll
+        for (int i = 0; i < DIM; i++) {
+            F.x[i] = x[i];
+            F.hpar[i] = hp[i];
+#pragma unroll
+            for (int j = 0; j < DIM; j++) F.dxi[i][j] = Xi[i][j];
+        }
+        dV = det * wq;
+    }
+
+    typename PH::template State<DIM> st;
+    PH::template prepare<DIM>(prm.p, F, st);
+    double chk = 0.0;
+    if (Rt) {
+        double r[NKS * M];
+        PH::template residual<DIM>(st, r);
+        static_for<L::NR>([&](auto RR) {
+            constexpr int rr = decltype(RR)::value;
+            constexpr int c = L::R.c[rr], i = L::R.i[rr];
+            double val = 0.0;
+            static_for<NKS>([&](auto K) {
+                constexpr int k = decltype(K)::value;
+                if constexpr (KS::tmask(k, c) && PH::rmask(k, i)) val += T[k][c] * r[k * M + i];
+            });
+            val *= dV;
+            chk += val;
+            Rt[rr * ldq + t] = val;
+        });
+    }
+    if constexpr (JAC) {
+        if constexpr (MODE == MODE_PARAM) {
+            static_for<NKS>([&](auto K2) {
+                constexpr int k2 = decltype(K2)::value;
+                static_for<M>([&](auto J) {
+                    constexpr int j = decltype(J)::value;
+                    double col[NKS * M];
+                    PH::template dcol<DIM>(st, k2, j, a, b, col);
+                    static_for<L::NE>([&](auto E) {
+                        constexpr int ee = decltype(E)::value;
+                        constexpr int c = L::E.c[ee], i = L::E.i[ee];
+                        if constexpr (L::E.c2[ee] == k2 && L::E.j[ee] == j) {
+                            const double val = col[c * M + i] * dV;
+                            chk += val;
+                            Dt[ee * ldq + t] = val;
+                        }
+                    });
+                });
+            });
+        } else {
+            double acc[L::NE];
+#pragma unroll
+            for (int ee = 0; ee < L::NE; ee++) acc[ee] = 0.0;
+            static_for<NKS>([&](auto K2) {
+                constexpr int k2 = decltype(K2)::value;
+                static_for<M>([&](auto J) {
+                    constexpr int j = decltype(J)::value;
+                    double col[NKS * M];
+                    PH::template dcol<DIM>(st, k2, j, a, b, col);
+                    static_for<L::NE>([&](auto E) {
+                        constexpr int ee = decltype(E)::value;
+                        constexpr int c = L::E.c[ee], i = L::E.i[ee], c2 = L::E.c2[ee];
+                        if constexpr (L::E.j[ee] == j && KS::tmask(k2, c2)) {
+                            double sum = 0.0;
+                            static_for<NKS>([&](auto K) {
+                                constexpr int k = decltype(K)::value;
+                                if constexpr (KS::tmask(k, c) && PH::template dmask<DIM>(k, i, k2, j))
+                                    sum += T[k][c] * col[k * M + i];
+                            });
+                            acc[ee] += T[k2][c2] * sum;
+                        }
+                    });
+                });
+            });
+#pragma unroll
+            for (int ee = 0; ee < L::NE; ee++) {
+                const double val = acc[ee] * dV;
+                chk += val;
+                Dt[ee * ldq + t] = val;
+            }
+        }
+    }
+    if (!isfinite(chk)) bad = true;
+    if (bad) atomicOr(s.errflag, (MODE == MODE_NURBS && !(dV > 0.0)) ? 1 : 2);
+}
+
+// ============================================================================================
+// K3b: contraction + scatter kernel (one CTA per element)
+// ============================================================================================
+template <int DIM, int P, class PH, int MODE, bool JAC>
+__global__ void __launch_bounds__(256)
+k_contract(SpaceDev s, const double *__restrict__ Dt, const double *__restrict__ Rt, long long e0, long long ldq,
+           double *__restrict__ val, double *__restrict__ Fout) {
+    using L = Lists<PH, DIM, MODE>;
+    using KS = typename L::KS;
+    constexpr int M = PH::M, NQ1 = P + 1, NP1 = P + 1;
+    constexpr int NQ = ipow(NQ1, DIM), NEN = ipow(NP1, DIM);
+    constexpr int NC = KS::NC;
+    __shared__ double tabs[DIM][NQ1][3][NP1];
+    __shared__ long long nodeS[NEN], rowL[NEN];
+    __shared__ double sA[NEN];
+    __shared__ int Wn[NEN], W1n[NEN], W2n[NEN], own[NEN];
+    __shared__ int posT[DIM][NP1][NP1];
+    extern __shared__ double dyn[];
+    double *Ds = dyn;                                   // [NE][NQ]
+    double *Rs = dyn + (JAC ? L::NE * NQ : 0);          // [NR][NQ]
+
+    int e[3];
+    elem_coords(s, e0 + blockIdx.x, e);
+    const long long qbase = (long long)blockIdx.x * NQ;
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < DIM * NQ1 * 3 * NP1; idx += blockDim.x) {
+        const int d = idx / (NQ1 * 3 * NP1), rest = idx % (NQ1 * 3 * NP1);
+        (&tabs[0][0][0][0])[idx] = s.ax[d].tab[(size_t)e[d] * NQ1 * 3 * NP1 + rest];
+    }
+    for (int idx = tid; idx < DIM * NP1 * NP1; idx += blockDim.x) {
+        const int d = idx / (NP1 * NP1), rest = idx % (NP1 * NP1);
+        (&posT[0][0][0])[idx] = s.ax[d].pos[(size_t)e[d] * NP1 * NP1 + rest];
+    }
+    if (JAC)
+        for (int idx = tid; idx < L::NE * NQ; idx += blockDim.x)
+            Ds[idx] = Dt[(idx / NQ) * ldq + qbase + idx % NQ];
+    if (Fout)
+        for (int idx = tid; idx < L::NR * NQ; idx += blockDim.x)
+            Rs[idx] = Rt[(idx / NQ) * ldq + qbase + idx % NQ];
+    for (int A = tid; A < NEN; A += blockDim.x) {
+        int aa[3] = {0, 0, 0};
+        int r = A;
+        for (int d = DIM - 1; d >= 0; d--) { aa[d] = r % NP1; r /= NP1; }
+        int g[3] = {0, 0, 0}, l[3] = {0, 0, 0}, Wd[3] = {1, 1, 1};
+        long long Sd[3] = {0, 0, 0}, Td[3] = {1, 1, 1};
+        int ok = 1;
+        for (int d = 0; d < DIM; d++) {
+            g[d] = s.ax[d].first[e[d]] + aa[d];
+            if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
+            l[d] = g[d] - s.ax[d].own_lo;
+            if (l[d] < 0 || g[d] >= s.ax[d].own_hi) ok = 0;
+            Wd[d] = s.ax[d].rowW[g[d]];
+            Sd[d] = s.ax[d].rowS[g[d]];
+            Td[d] = s.ax[d].T;
+        }
+        own[A] = ok;
+        nodeS[A] = (long long)M * M * (Sd[0] * Td[1] * Td[2] + Wd[0] * Sd[1] * Td[2] + (long long)Wd[0] * Wd[1] * Sd[2]);
+        Wn[A] = Wd[0] * Wd[1] * Wd[2];
+        W1n[A] = Wd[1];
+        W2n[A] = Wd[2];
+        const int n1o = s.ax[1].own_hi - s.ax[1].own_lo, n2o = s.ax[2].own_hi - s.ax[2].own_lo;
+        rowL[A] = (((long long)l[0] * n1o + l[1]) * n2o + l[2]) * M;
+        sA[A] = (MODE == MODE_NURBS && s.wts) ? s.wts[node_index(s, g[0], g[1], g[2])] : 1.0;
+    }
+    __syncthreads();
+
+    // ---- residual: thread per test function A --------------------------------------------
+    if (Fout) {
+        for (int A = tid; A < NEN; A += blockDim.x) {
+            if (!own[A]) continue;
+            int aa[3] = {0, 0, 0};
+            int r = A;
+#pragma unroll
+            for (int d = DIM - 1; d >= 0; d--) { aa[d] = r % NP1; r /= NP1; }
+            double acc[M];
+#pragma unroll
+            for (int i = 0; i < M; i++) acc[i] = 0.0;
+#pragma unroll 1
+            for (int q = 0; q < NQ; q++) {
+                int qd[3] = {0, 0, 0};
+                int rq = q;
+#pragma unroll
+                for (int d = DIM - 1; d >= 0; d--) { qd[d] = rq % NQ1; rq /= NQ1; }
+                double v[DIM][3][NP1];
+#pragma unroll
+                for (int d = 0; d < DIM; d++)
+#pragma unroll
+                    for (int k = 0; k < 3; k++)
+#pragma unroll
+                        for (int x = 0; x < NP1; x++) v[d][k][x] = tabs[d][qd[d]][k][x];
+                static_for<L::NR>([&](auto RR) {
+                    constexpr int rr = decltype(RR)::value;
+                    constexpr int c = L::R.c[rr], i = L::R.i[rr];
+                    acc[i] += kind_value<KS, DIM, c, NP1>(v, aa) * Rs[rr * NQ + q];
+                });
+            }
+#pragma unroll
+            for (int i = 0; i < M; i++) atomicAdd(Fout + rowL[A] + i, sA[A] * acc[i]);
+        }
+    }
+
+    // ---- Jacobian: thread per (A, B) pair ---------------------------------------------------
+    if constexpr (JAC) {
+        for (int idx = tid; idx < NEN * NEN; idx += blockDim.x) {
+            const int A = idx / NEN, B = idx % NEN;
+            if (!own[A]) continue;
+            int aa[3] = {0, 0, 0}, bb[3] = {0, 0, 0};
+            {
+                int r = A, r2 = B;
+#pragma unroll
+                for (int d = DIM - 1; d >= 0; d--) { aa[d] = r % NP1; r /= NP1; bb[d] = r2 % NP1; r2 /= NP1; }
+            }
+            double K[M][M];
+#pragma unroll
+            for (int i = 0; i < M; i++)
+#pragma unroll
+                for (int j = 0; j < M; j++) K[i][j] = 0.0;
+#pragma unroll 1
+            for (int q = 0; q < NQ; q++) {
+                int qd[3] = {0, 0, 0};
+                int rq = q;
+#pragma unroll
+                for (int d = DIM - 1; d >= 0; d--) { qd[d] = rq % NQ1; rq /= NQ1; }
+                double va[DIM][3][NP1];
+#pragma unroll
+                for (int d = 0; d < DIM; d++)
+#pragma unroll
+                    for (int k = 0; k < 3; k++)
+#pragma unroll
+                        for (int x = 0; x < NP1; x++) va[d][k][x] = tabs[d][qd[d]][k][x];
+                double PA[NC], PB[NC];
+                static_for<NC>([&](auto C) {
+                    constexpr int c = decltype(C)::value;
+                    if constexpr (L::test_used(c)) PA[c] = kind_value<KS, DIM, c, NP1>(va, aa);
+                    else PA[c] = 0.0;
+                    if constexpr (L::trial_used(c)) PB[c] = kind_value<KS, DIM, c, NP1>(va, bb);
+                    else PB[c] = 0.0;
+                });
+                static_for<L::NE>([&](auto E) {
+                    constexpr int ee = decltype(E)::value;
+                    constexpr int i = L::E.i[ee], j = L::E.j[ee], c = L::E.c[ee], c2 = L::E.c2[ee];
+                    K[i][j] += PA[c] * Ds[ee * NQ + q] * PB[c2];
+                });
+            }
+            int pos[3] = {0, 0, 0};
+#pragma unroll
+            for (int d = 0; d < DIM; d++) pos[d] = posT[d][aa[d]][bb[d]];
+            const long long off = ((long long)(pos[0] * W1n[A] + pos[1]) * W2n[A] + pos[2]) * M;
+            const double sc = sA[A] * sA[B];
+#pragma unroll
+            for (int i = 0; i < M; i++) {
+                double *dst = val + nodeS[A] + (long long)i * Wn[A] * M + off;
+#pragma unroll
+                for (int j = 0; j < M; j++) atomicAdd(dst + j, sc * K[i][j]);
+            }
+        }
+    }
+}
+
+__global__ void k_zero(double *__restrict__ p, long long n) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) p[k] = 0.0;
+}
+
+static int zero_launch(iga_space_s *s, double *p, long long n, cudaStream_t st, int nsm) {
+    if (n <= 0) return 0;
+    ProfScope ps(s, "k_zero", st);
+    long long blocks = (n + 255) / 256;
+    const long long cap = (long long)nsm * 16;
+    if (blocks > cap) blocks = cap;
+    k_zero<<<(unsigned)blocks, 256, 0, st>>>(p, n);
+    return 1;
+}
+
+// ============================================================================================
+// host launcher
+// ============================================================================================
+template <int DIM, int P, class PH, int MODE>
+static iga_status run_form(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
+                           const double *Ud, double *val, double *F, cudaStream_t st) {
+    using L = Lists<PH, DIM, MODE>;
+    constexpr int NQ = ipow(P + 1, DIM);
+    const bool jac = val != nullptr;
+    Prm prm;
+    for (int i = 0; i < 8; i++) prm.p[i] = phys->p[i];
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    int launches = 0;
+    if (jac) launches += zero_launch(s, val, s->nnz_owned, st, nsm);
+    if (F) launches += zero_launch(s, F, s->nrows_owned, st, nsm);
+    const size_t per_el = (size_t)NQ * ((jac ? L::NE : 0) + (F ? L::NR : 0)) * sizeof(double);
+    long long nb_max = per_el ? (long long)(s->work_bytes / per_el) : s->nel_local;
+    if (nb_max < 1) { set_error("workspace too small"); return IGA_ERR_NOMEM; }
+    if (nb_max > s->nel_local) nb_max = s->nel_local;
+    nb_max = std::min<long long>(nb_max, (1LL << 31) / NQ - 1);
+    const size_t dsm = (size_t)NQ * ((jac ? L::NE : 0) + L::NR) * sizeof(double);
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[jac]) {
+        cudaError_t ce;
+        if (jac) ce = cudaFuncSetAttribute(k_contract<DIM, P, PH, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        else ce = cudaFuncSetAttribute(k_contract<DIM, P, PH, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (ce != cudaSuccess) { set_error(cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+        attr_set[jac] = true;
+    }
+    double *Dt = s->work;
+    for (long long e0 = 0; e0 < s->nel_local; e0 += nb_max) {
+        const int nb = (int)std::min<long long>(nb_max, s->nel_local - e0);
+        const long long ldq = (long long)nb * NQ;
+        double *Rt = F ? Dt + (jac ? (size_t)L::NE * ldq : 0) : nullptr;
+        const long long nthr = (long long)nb * NQ;
+        const unsigned gA = (unsigned)((nthr + 127) / 128);
+        if (jac) {
+            { ProfScope ps(s, "k_point", st);
+              k_point<DIM, P, PH, MODE, true><<<gA, 128, 0, st>>>(s->dev, prm, a, b, U, Ud, Dt, Rt, e0, nb, ldq); }
+            { ProfScope ps(s, "k_contract", st);
+              k_contract<DIM, P, PH, MODE, true><<<nb, 256, dsm, st>>>(s->dev, Dt, Rt, e0, ldq, val, F); }
+        } else {
+            { ProfScope ps(s, "k_point", st);
+              k_point<DIM, P, PH, MODE, false><<<gA, 128, 0, st>>>(s->dev, prm, a, b, U, Ud, Dt, Rt, e0, nb, ldq); }
+            { ProfScope ps(s, "k_contract", st);
+              k_contract<DIM, P, PH, MODE, false><<<nb, 256, dsm, st>>>(s->dev, Dt, Rt, e0, ldq, val, F); }
+        }
+        launches += 2;
+    }
+    s->last_launches = launches;
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) { set_error(std::string("kernel launch: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return IGA_OK;
+}
+
+template <int DIM, int P, class PH>
+static iga_status dispatch_mode(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                                const double *Ud, double *val, double *F, cudaStream_t st) {
+    if (s->mode == MODE_PARAM) return run_form<DIM, P, PH, MODE_PARAM>(s, ph, a, b, U, Ud, val, F, st);
+    if constexpr (std::is_same<PH, PhysNSVMS>::value) {
+        set_error("NS_VMS supports parametric geometry with unit weights only");
+        return IGA_ERR_PARAM;
+    } else {
+        return run_form<DIM, P, PH, MODE_NURBS>(s, ph, a, b, U, Ud, val, F, st);
+    }
+}
+
+template <int DIM, class PH>
+static iga_status dispatch_p(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                             const double *Ud, double *val, double *F, cudaStream_t st) {
+    const int p = s->p[0];
+    switch (p) {
+    case 2: return dispatch_mode<DIM, 2, PH>(s, ph, a, b, U, Ud, val, F, st);
+    case 3: return dispatch_mode<DIM, 3, PH>(s, ph, a, b, U, Ud, val, F, st);
+    default: break;
+    }
+    set_error("degree must be 2 or 3 (equal on all axes) in this build");
+    return IGA_ERR_PARAM;
+}
+
+iga_status launch_form(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                       const double *Ud, double *val, double *F, cudaStream_t st) {
+    for (int d = 1; d < s->dim; d++)
+        if (s->p[d] != s->p[0]) { set_error("degree must be equal on all axes in this build"); return IGA_ERR_PARAM; }
+    for (int d = 0; d < s->dim; d++)
+        if (s->nq[d] != s->p[d] + 1) { set_error("quad must be p+1 in this build"); return IGA_ERR_PARAM; }
+    switch (ph->kind) {
+    case IGA_PHYS_LAPLACE:
+        if (s->dof != 1) break;
+        if (s->dim == 2) return dispatch_p<2, PhysLaplace>(s, ph, a, b, U, Ud, val, F, st);
+        if (s->dim == 3) return dispatch_p<3, PhysLaplace>(s, ph, a, b, U, Ud, val, F, st);
+        break;
+    case IGA_PHYS_CAHN_HILLIARD:
+        if (s->dof != 1) break;
+        if (s->dim == 2) return dispatch_p<2, PhysCahnHilliard>(s, ph, a, b, U, Ud, val, F, st);
+        if (s->dim == 3) return dispatch_p<3, PhysCahnHilliard>(s, ph, a, b, U, Ud, val, F, st);
+        break;
+    case IGA_PHYS_NEOHOOKE:
+        if (s->dof != 3 || s->dim != 3) break;
+        return dispatch_p<3, PhysNeoHooke>(s, ph, a, b, U, Ud, val, F, st);
+    case IGA_PHYS_NS_VMS:
+        if (s->dof != 4 || s->dim != 3) break;
+        return dispatch_p<3, PhysNSVMS>(s, ph, a, b, U, Ud, val, F, st);
+    default:
+        set_error("unknown physics kind");
+        return IGA_ERR_PARAM;
+    }
+    set_error("physics / dim / dof combination not supported");
+    return IGA_ERR_PARAM;
+}
+
+}  // namespace iga

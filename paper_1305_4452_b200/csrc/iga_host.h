@@ -1,0 +1,53 @@
+// iga_host.h -- host-side state of an IGA space (libiga internals).
+#pragma once
+#include <string>
+#include <vector>
+
+#include "iga_internal.cuh"
+
+struct iga_space_s {
+    int device = 0;
+    iga::SpaceDev dev{};                 // device view (pointers into `allocs`)
+    int dim = 0, dof = 1, geom = 0, weighted = 0, mode = 0;
+    int p[3] = {0, 0, 0}, nel[3] = {1, 1, 1}, nu[3] = {1, 1, 1}, nq[3] = {1, 1, 1}, nfun[3] = {1, 1, 1};
+    int periodic[3] = {0, 0, 0};
+    std::vector<double> U[3];            // unclamped knot vectors
+    std::vector<int> rowW[3];            // per axis stencil widths [nu]
+    std::vector<int> cols[3];            // per axis column lists [nu][colmax]
+    int colmax[3] = {1, 1, 1};
+    // distribution (box decomposition)
+    int rank = 0, nranks = 1, procs[3] = {1, 1, 1}, rcoord[3] = {0, 0, 0};
+    int own_lo[3] = {0, 0, 0}, own_hi[3] = {1, 1, 1};
+    int el_lo[3] = {0, 0, 0}, el_hi[3] = {1, 1, 1};
+    long long ndof_global = 0, nrows_owned = 0, nnz_owned = 0, nqp_local = 0, nel_local = 0;
+    // device allocations owned by the space
+    std::vector<void *> allocs;
+    double *work = nullptr;              // per-batch quadrature-point coefficient workspace
+    size_t work_bytes = 0;
+    int *errflag = nullptr;
+    int last_launches = 0;
+    // kernel timing hook (iga_profile_*)
+    struct ProfRec { const char *name; cudaEvent_t a, b; };
+    bool prof_on = false;
+    std::vector<ProfRec> prof_pending;
+    std::vector<cudaEvent_t> prof_pool;
+    std::vector<std::string> prof_names;
+    std::vector<int> prof_count;
+    std::vector<double> prof_ms;
+};
+
+namespace iga {
+// bracket one kernel launch with events when profiling is on
+struct ProfScope {
+    iga_space_s *s;
+    const char *name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(iga_space_s *s_, const char *n, cudaStream_t st_);
+    ~ProfScope();
+};
+void set_error(const std::string &msg);
+iga_status launch_form(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
+                       const double *Udot, double *csr_val, double *F, cudaStream_t st);
+iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st);
+}  // namespace iga

@@ -1,0 +1,687 @@
+// space.cu -- libiga space setup (host orchestration + kernels K1 basis tables, K2 CSR pattern)
+// and the extern "C" entry points declared in include/iga.h.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "iga_host.h"
+
+namespace iga {
+
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+
+static cudaEvent_t prof_event(iga_space_s *s) {
+    if (!s->prof_pool.empty()) {
+        cudaEvent_t e = s->prof_pool.back();
+        s->prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(iga_space_s *s_, const char *n, cudaStream_t st_) : s(s_), name(n), st(st_) {
+    if (!s->prof_on) return;
+    a = prof_event(s);
+    b = prof_event(s);
+    cudaEventRecord(a, st);
+}
+
+ProfScope::~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    s->prof_pending.push_back({name, a, b});
+}
+
+static void prof_collect(iga_space_s *s) {
+    for (auto &r : s->prof_pending) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        size_t k = 0;
+        for (; k < s->prof_names.size(); k++)
+            if (s->prof_names[k] == r.name) break;
+        if (k == s->prof_names.size()) {
+            s->prof_names.push_back(r.name);
+            s->prof_count.push_back(0);
+            s->prof_ms.push_back(0.0);
+        }
+        s->prof_count[k] += 1;
+        s->prof_ms[k] += ms;
+        s->prof_pool.push_back(r.a);
+        s->prof_pool.push_back(r.b);
+    }
+    s->prof_pending.clear();
+}
+
+#define CUDA_TRY(x)                                                                   \
+    do {                                                                              \
+        cudaError_t _e = (x);                                                         \
+        if (_e != cudaSuccess) {                                                      \
+            set_error(std::string(#x) + ": " + cudaGetErrorString(_e));               \
+            return IGA_ERR_CUDA;                                                      \
+        }                                                                             \
+    } while (0)
+
+// ------------------------------------------------------------------------------------------
+// K1: univariate basis N, N', N'' of the p+1 functions of a span at a point, by the triangular
+// in-span scheme (the "more computationally efficient algorithm" P:191-193 points to): the
+// upper triangle of ndu holds the degree-by-degree basis values, the lower triangle the knot
+// differences, from which the derivatives follow by the recurrence on the a[][] coefficients.
+// ------------------------------------------------------------------------------------------
+__device__ void span_basis_ders(int span, double xi, int p, const double *U, double out[3][MAXP + 1]) {
+    double ndu[MAXP + 1][MAXP + 1], left[MAXP + 1], right[MAXP + 1];
+    ndu[0][0] = 1.0;
+    for (int j = 1; j <= p; j++) {
+        left[j] = xi - U[span + 1 - j];
+        right[j] = U[span + j] - xi;
+        double saved = 0.0;
+        for (int r = 0; r < j; r++) {
+            ndu[j][r] = right[r + 1] + left[j - r];
+            const double tmp = ndu[r][j - 1] / ndu[j][r];
+            ndu[r][j] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        ndu[j][j] = saved;
+    }
+    for (int r = 0; r <= p; r++) {
+        out[0][r] = ndu[r][p];
+        out[1][r] = 0.0;
+        out[2][r] = 0.0;
+    }
+    const int nd = p < 2 ? p : 2;
+    double a[2][MAXP + 1];
+    for (int r = 0; r <= p; r++) {
+        int s1 = 0, s2 = 1;
+        a[0][0] = 1.0;
+        for (int k = 1; k <= nd; k++) {
+            double d = 0.0;
+            const int rk = r - k, pk = p - k;
+            if (r >= k) {
+                a[s2][0] = a[s1][0] / ndu[pk + 1][rk];
+                d = a[s2][0] * ndu[rk][pk];
+            }
+            const int j1 = (rk >= -1) ? 1 : -rk;
+            const int j2 = (r - 1 <= pk) ? k - 1 : p - r;
+            for (int j = j1; j <= j2; j++) {
+                a[s2][j] = (a[s1][j] - a[s1][j - 1]) / ndu[pk + 1][rk + j];
+                d += a[s2][j] * ndu[rk + j][pk];
+            }
+            if (r <= pk) {
+                a[s2][k] = -a[s1][k - 1] / ndu[pk + 1][r];
+                d += a[s2][k] * ndu[r][pk];
+            }
+            out[k][r] = d;
+            const int t = s1; s1 = s2; s2 = t;
+        }
+    }
+    double f = p;
+    for (int k = 1; k <= nd; k++) {
+        for (int r = 0; r <= p; r++) out[k][r] *= f;
+        f *= (p - k);
+    }
+}
+
+__global__ void k_tables(int nel, int nq, int p, const double *__restrict__ U, const int *__restrict__ first,
+                         const double *__restrict__ qx, double *__restrict__ tab) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nel * nq) return;
+    const int e = t / nq;
+    double out[3][MAXP + 1];
+    span_basis_ders(first[e] + p, qx[t], p, U, out);
+    for (int k = 0; k < 3; k++)
+        for (int a = 0; a <= p; a++) tab[(size_t)t * 3 * (p + 1) + k * (p + 1) + a] = out[k][a];
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: CSR pattern, one warp per owned row.  row r = (local node, component i);
+//   row start = m^2 (S0 T1 T2 + W0 S1 T2 + W0 W1 S2) + i W m   (separable prefix sums)
+//   entry t = ((c0 W1 + c1) W2 + c2) m + j  ->  column node(cols0[c0], cols1[c1], cols2[c2]) m + j
+// ------------------------------------------------------------------------------------------
+__global__ void k_pattern(SpaceDev s, long long nrows, long long nnz, long long *__restrict__ row_ptr,
+                          int *__restrict__ col_idx) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= nrows) return;
+    const int m = s.dof;
+    long long r = warp;
+    const int i = (int)(r % m);
+    r /= m;
+    const int n1o = s.ax[1].own_hi - s.ax[1].own_lo, n2o = s.ax[2].own_hi - s.ax[2].own_lo;
+    const int g2 = s.ax[2].own_lo + (int)(r % n2o);
+    r /= n2o;
+    const int g1 = s.ax[1].own_lo + (int)(r % n1o);
+    r /= n1o;
+    const int g0 = s.ax[0].own_lo + (int)r;
+    const int W0 = s.ax[0].rowW[g0], W1 = s.ax[1].rowW[g1], W2 = s.ax[2].rowW[g2];
+    const long long S0 = s.ax[0].rowS[g0], S1 = s.ax[1].rowS[g1], S2 = s.ax[2].rowS[g2];
+    const long long T1 = s.ax[1].T, T2 = s.ax[2].T;
+    const long long W = (long long)W0 * W1 * W2;
+    const long long start = (long long)m * m * (S0 * T1 * T2 + W0 * S1 * T2 + (long long)W0 * W1 * S2) + i * W * m;
+    if (lane == 0) {
+        row_ptr[warp] = start;
+        if (warp == nrows - 1) row_ptr[nrows] = nnz;
+    }
+    const int *c0 = s.ax[0].cols + (size_t)g0 * s.ax[0].colmax;
+    const int *c1 = s.ax[1].cols + (size_t)g1 * s.ax[1].colmax;
+    const int *c2 = s.ax[2].cols + (size_t)g2 * s.ax[2].colmax;
+    const int nu1 = s.ax[1].nu, nu2 = s.ax[2].nu;
+    const long long len = W * m;
+    for (long long t = lane; t < len; t += 32) {
+        long long u = t;
+        const int j = (int)(u % m);
+        u /= m;
+        const int k2 = (int)(u % W2);
+        u /= W2;
+        const int k1 = (int)(u % W1);
+        const int k0 = (int)(u / W1);
+        const long long node = ((long long)c0[k0] * nu1 + c1[k1]) * nu2 + c2[k2];
+        col_idx[start + t] = (int)(node * m + j);
+    }
+}
+
+iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st) {
+    const long long nrows = s->nrows_owned;
+    if (nrows == 0) return IGA_OK;
+    const long long threads = nrows * 32;
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
+    {
+        ProfScope ps(s, "k_pattern", st);
+        k_pattern<<<blocks, 256, 0, st>>>(s->dev, nrows, s->nnz_owned, (long long *)row_ptr, col_idx);
+    }
+    CUDA_TRY(cudaGetLastError());
+    s->last_launches = 1;
+    return IGA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// host setup helpers
+// ------------------------------------------------------------------------------------------
+// Alg. 1: unclamp U (n+1 functions, degree p) for C^k periodicity, in place.
+static void unclamp(std::vector<double> &U, int p, int k) {
+    const int n = (int)U.size() - p - 2;
+    const int m = n + p + 1;
+    for (int i = 0; i <= k; i++) {
+        U[k - i] = U[p] - U[n + 1] + U[n - i];
+        U[m - k + i] = U[n + 1] - U[p] + U[p + i + 1];
+    }
+}
+
+// Gauss-Legendre nodes/weights on [-1,1] (A-6), Newton on the three-term recurrence in double.
+static void gauss_legendre(int n, std::vector<double> &x, std::vector<double> &w) {
+    x.assign(n, 0.0);
+    w.assign(n, 0.0);
+    const double pi = 3.14159265358979323846;
+    for (int i = 1; i <= n; i++) {
+        double z = std::cos(pi * (i - 0.25) / (n + 0.5));
+        double dp = 1.0;
+        for (int it = 0; it < 100; it++) {
+            double p0 = 1.0, p1 = z;
+            for (int k = 2; k <= n; k++) {
+                const double p2 = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = (n == 1) ? 1.0 : n * (p0 - z * p1) / (1.0 - z * z);
+            const double dz = p1 / dp;
+            z -= dz;
+            if (std::fabs(dz) <= 1e-17) break;
+        }
+        double p0 = 1.0, p1 = z;
+        for (int k = 2; k <= n; k++) {
+            const double p2 = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k;
+            p0 = p1;
+            p1 = p2;
+        }
+        dp = (n == 1) ? 1.0 : n * (p0 - z * p1) / (1.0 - z * z);
+        x[n - i] = z;
+        w[n - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+    }
+}
+
+template <class T>
+static iga_status dalloc(iga_space_s *s, T **p, size_t count) {
+    void *ptr = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&ptr, count * sizeof(T));
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        return IGA_ERR_NOMEM;
+    }
+    s->allocs.push_back(ptr);
+    *p = (T *)ptr;
+    return IGA_OK;
+}
+
+template <class T>
+static iga_status upload(iga_space_s *s, T **p, const std::vector<T> &h) {
+    iga_status st = dalloc(s, p, h.size());
+    if (st != IGA_OK) return st;
+    if (!h.empty()) CUDA_TRY(cudaMemcpy(*p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return IGA_OK;
+}
+
+static void free_space(iga_space_s *s) {
+    if (!s) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    prof_collect(s);
+    for (cudaEvent_t e : s->prof_pool) cudaEventDestroy(e);
+    for (void *p : s->allocs) cudaFree(p);
+    cudaSetDevice(prev);
+    delete s;
+}
+
+static iga_status create(const iga_space_desc *d, const iga_dist *dist, int device, iga_space *out) {
+    if (!d || !out) { set_error("null argument"); return IGA_ERR_PARAM; }
+    *out = nullptr;
+    if (d->dim < 2 || d->dim > 3) { set_error("dim must be 2 or 3 in this build"); return IGA_ERR_PARAM; }
+    if (d->dof < 1 || d->dof > 4) { set_error("dof must be 1..4"); return IGA_ERR_PARAM; }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        set_error("no CUDA device (libiga has no CPU fallback)");
+        return IGA_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) { set_error("bad device ordinal"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    CUDA_TRY(cudaSetDevice(device));
+    iga_space_s *s = new iga_space_s();
+    s->device = device;
+    s->dim = d->dim;
+    s->dof = d->dof;
+    s->geom = d->geometry;
+    s->weighted = d->weights != nullptr;
+    s->mode = (d->geometry == IGA_GEOM_NURBS || d->weights) ? MODE_NURBS : MODE_PARAM;
+    if (d->geometry == IGA_GEOM_NURBS && !d->ctrl) { delete s; set_error("NURBS geometry needs ctrl"); return IGA_ERR_PARAM; }
+    // distribution
+    if (dist) {
+        s->rank = dist->rank;
+        s->nranks = dist->nranks;
+        int prod = 1;
+        for (int a = 0; a < 3; a++) {
+            s->procs[a] = a < d->dim ? std::max(1, dist->procs[a]) : 1;
+            prod *= s->procs[a];
+        }
+        if (prod != s->nranks || s->rank < 0 || s->rank >= s->nranks) {
+            delete s;
+            set_error("iga_dist: procs product must equal nranks and 0 <= rank < nranks");
+            return IGA_ERR_PARAM;
+        }
+        int r = s->rank;
+        s->rcoord[2] = r % s->procs[2]; r /= s->procs[2];
+        s->rcoord[1] = r % s->procs[1]; r /= s->procs[1];
+        s->rcoord[0] = r;
+    }
+    iga_status st = IGA_OK;
+    long long nnodes = 1, nrows_nodes = 1;
+    s->dev.ctrl = nullptr;
+    s->dev.wts = nullptr;
+    for (int a = 0; a < 3; a++) {
+        AxisDev &ax = s->dev.ax[a];
+        if (a >= d->dim) {
+            // trivial axis: one element, one function, one point
+            s->p[a] = 0; s->nel[a] = 1; s->nu[a] = 1; s->nq[a] = 1; s->nfun[a] = 1;
+            s->rowW[a] = {1};
+            s->cols[a] = {0};
+            s->colmax[a] = 1;
+            ax.p = 0; ax.nel = 1; ax.nu = 1; ax.nq = 1;
+            std::vector<double> one = {1.0, 0.0, 0.0}, w1 = {1.0}, x0 = {0.0}, h1 = {1.0};
+            std::vector<int> z = {0}, one_i = {1}, zc = {0};
+            std::vector<long long> zl = {0};
+            if ((st = upload(s, (double **)&ax.tab, one)) != IGA_OK) goto fail;
+            if ((st = upload(s, (double **)&ax.qw, w1)) != IGA_OK) goto fail;
+            if ((st = upload(s, (double **)&ax.qx, x0)) != IGA_OK) goto fail;
+            if ((st = upload(s, (double **)&ax.hpar, h1)) != IGA_OK) goto fail;
+            if ((st = upload(s, (int **)&ax.first, z)) != IGA_OK) goto fail;
+            if ((st = upload(s, (int **)&ax.pos, z)) != IGA_OK) goto fail;
+            if ((st = upload(s, (int **)&ax.rowW, one_i)) != IGA_OK) goto fail;
+            if ((st = upload(s, (long long **)&ax.rowS, zl)) != IGA_OK) goto fail;
+            if ((st = upload(s, (int **)&ax.cols, zc)) != IGA_OK) goto fail;
+            ax.colmax = 1; ax.T = 1; ax.own_lo = 0; ax.own_hi = 1; ax.el_lo = 0; ax.el_hi = 1;
+            s->own_lo[a] = 0; s->own_hi[a] = 1; s->el_lo[a] = 0; s->el_hi[a] = 1;
+            continue;
+        }
+        const int p = d->degree[a];
+        if (p < 1 || p > MAXP) { st = IGA_ERR_PARAM; set_error("degree must be 1..3"); goto fail; }
+        const int nk = d->n_knots[a];
+        if (nk < 2 * (p + 1) || !d->knots[a]) { st = IGA_ERR_DOMAIN; set_error("too few knots"); goto fail; }
+        std::vector<double> U(d->knots[a], d->knots[a] + nk);
+        for (int i = 0; i + 1 < nk; i++)
+            if (!(U[i] <= U[i + 1])) { st = IGA_ERR_DOMAIN; set_error("knots must be non-decreasing"); goto fail; }
+        const int nfun = nk - p - 1;
+        int nu = nfun;
+        s->periodic[a] = d->periodic[a] ? 1 : 0;
+        if (s->periodic[a]) {
+            const int k = d->periodic_continuity[a];
+            if (k < 0 || k > p - 1) { st = IGA_ERR_DOMAIN; set_error("periodic continuity must be in [0, p-1]"); goto fail; }
+            if (d->geometry == IGA_GEOM_NURBS) { st = IGA_ERR_PARAM; set_error("periodic NURBS geometry (Alg. 2) not supported"); goto fail; }
+            unclamp(U, p, k);
+            nu = nfun - (k + 1);
+        }
+        // elements: nonzero spans inside [U_p, U_nfun]
+        std::vector<int> first;
+        std::vector<double> hpar;
+        for (int sp = p; sp < nfun; sp++)
+            if (U[sp] < U[sp + 1]) { first.push_back(sp - p); hpar.push_back(U[sp + 1] - U[sp]); }
+        const int nel = (int)first.size();
+        if (s->periodic[a] && nu < 2 * p + 1) { st = IGA_ERR_DOMAIN; set_error("periodic axis needs >= 2p+1 functions"); goto fail; }
+        const int nq = d->quad[a] > 0 ? d->quad[a] : p + 1;
+        std::vector<double> gx, gw;
+        gauss_legendre(nq, gx, gw);
+        std::vector<double> qx((size_t)nel * nq), qw((size_t)nel * nq);
+        for (int e = 0; e < nel; e++) {
+            const double lo = U[first[e] + p], hi = U[first[e] + p + 1];
+            for (int q = 0; q < nq; q++) {
+                qx[(size_t)e * nq + q] = 0.5 * (lo + hi) + 0.5 * (hi - lo) * gx[q];
+                qw[(size_t)e * nq + q] = gw[q] * 0.5 * (hi - lo);
+            }
+        }
+        // Alg. 3 on every representative i of each unique function, wrapped mod nu
+        std::vector<std::vector<int>> colset(nu);
+        for (int i = 0; i < nfun; i++) {
+            int k = i;
+            while (k + 1 < nk && U[k] == U[k + 1]) k++;
+            const int l = k - p;
+            k = i + p + 1;
+            while (k - 1 >= 0 && U[k] == U[k - 1]) k--;
+            const int r = k - 1;
+            auto &cs = colset[i % nu];
+            for (int j = l; j <= r; j++) cs.push_back(((j % nu) + nu) % nu);
+        }
+        int colmax = 1;
+        std::vector<int> rowW(nu);
+        for (int g = 0; g < nu; g++) {
+            auto &cs = colset[g];
+            std::sort(cs.begin(), cs.end());
+            cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
+            rowW[g] = (int)cs.size();
+            colmax = std::max(colmax, rowW[g]);
+        }
+        std::vector<int> cols((size_t)nu * colmax, 0);
+        for (int g = 0; g < nu; g++) std::copy(colset[g].begin(), colset[g].end(), cols.begin() + (size_t)g * colmax);
+        // per element: position of column function beta in row function alpha's list
+        std::vector<int> pos((size_t)nel * (p + 1) * (p + 1));
+        for (int e = 0; e < nel; e++)
+            for (int al = 0; al <= p; al++)
+                for (int be = 0; be <= p; be++) {
+                    const int ga = (first[e] + al) % nu, gb = (first[e] + be) % nu;
+                    const auto &cs = colset[ga];
+                    const int ps = (int)(std::lower_bound(cs.begin(), cs.end(), gb) - cs.begin());
+                    pos[((size_t)e * (p + 1) + al) * (p + 1) + be] = ps;
+                }
+        // box decomposition of elements (b_r = floor(N r / P)) and dof ownership
+        // (A-9: owner of a function = owner of the last element of its support)
+        const int P = s->procs[a], rc = s->rcoord[a];
+        const int el_lo = (int)((long long)nel * rc / P), el_hi = (int)((long long)nel * (rc + 1) / P);
+        std::vector<int> last_el(nu, -1);
+        for (int e = 0; e < nel; e++)
+            for (int al = 0; al <= p; al++) {
+                const int i = first[e] + al;
+                if (i < nu) last_el[i] = std::max(last_el[i], e);     // representative i = g
+            }
+        for (int g = 0; g < nu; g++)
+            if (last_el[g] < 0) last_el[g] = nel - 1;
+        int own_lo = nu, own_hi = 0;
+        for (int g = 0; g < nu; g++)
+            if (last_el[g] >= el_lo && last_el[g] < el_hi) { own_lo = std::min(own_lo, g); own_hi = std::max(own_hi, g + 1); }
+        if (own_hi <= own_lo) { own_lo = own_hi = 0; }
+        std::vector<long long> rowS(nu, 0);
+        long long T = 0;
+        for (int g = own_lo; g < own_hi; g++) { rowS[g] = T; T += rowW[g]; }
+
+        s->p[a] = p; s->nel[a] = nel; s->nu[a] = nu; s->nq[a] = nq; s->nfun[a] = nfun;
+        s->U[a] = U; s->rowW[a] = rowW; s->cols[a] = cols; s->colmax[a] = colmax;
+        s->own_lo[a] = own_lo; s->own_hi[a] = own_hi; s->el_lo[a] = el_lo; s->el_hi[a] = el_hi;
+        ax.p = p; ax.nel = nel; ax.nu = nu; ax.nq = nq; ax.colmax = colmax; ax.T = T;
+        ax.own_lo = own_lo; ax.own_hi = own_hi; ax.el_lo = el_lo; ax.el_hi = el_hi;
+        double *dU = nullptr;
+        double *dtab = nullptr;
+        if ((st = upload(s, &dU, U)) != IGA_OK) goto fail;
+        if ((st = upload(s, (double **)&ax.qw, qw)) != IGA_OK) goto fail;
+        if ((st = upload(s, (double **)&ax.qx, qx)) != IGA_OK) goto fail;
+        if ((st = upload(s, (double **)&ax.hpar, hpar)) != IGA_OK) goto fail;
+        if ((st = upload(s, (int **)&ax.first, first)) != IGA_OK) goto fail;
+        if ((st = upload(s, (int **)&ax.pos, pos)) != IGA_OK) goto fail;
+        if ((st = upload(s, (int **)&ax.rowW, rowW)) != IGA_OK) goto fail;
+        if ((st = upload(s, (long long **)&ax.rowS, rowS)) != IGA_OK) goto fail;
+        if ((st = upload(s, (int **)&ax.cols, cols)) != IGA_OK) goto fail;
+        if ((st = dalloc(s, &dtab, (size_t)nel * nq * 3 * (p + 1))) != IGA_OK) goto fail;
+        {
+            const int nt = nel * nq;
+            k_tables<<<(nt + 127) / 128, 128>>>(nel, nq, p, dU, ax.first, ax.qx, dtab);
+            cudaError_t ce = cudaGetLastError();
+            if (ce != cudaSuccess) { st = IGA_ERR_CUDA; set_error(cudaGetErrorString(ce)); goto fail; }
+        }
+        ax.tab = dtab;
+        nnodes *= nu;
+        nrows_nodes *= (own_hi - own_lo);
+    }
+    {
+        s->dev.dim = s->dim;
+        s->dev.dof = s->dof;
+        s->dev.mode = s->mode;
+        s->dev.weighted = s->weighted;
+        s->dev.geom = s->geom;
+        s->dev.nnodes = nnodes;
+        const int m = s->dof;
+        s->ndof_global = nnodes * m;
+        s->nrows_owned = nrows_nodes * m;
+        long long Tprod = 1;
+        for (int a = 0; a < 3; a++) Tprod *= s->dev.ax[a].T;
+        s->nnz_owned = Tprod * m * m;
+        s->nel_local = 1;
+        s->nqp_local = 1;
+        for (int a = 0; a < 3; a++) {
+            s->nel_local *= (s->el_hi[a] - s->el_lo[a]);
+            s->nqp_local *= (long long)(s->el_hi[a] - s->el_lo[a]) * s->nq[a];
+        }
+        if (d->geometry == IGA_GEOM_NURBS) {
+            std::vector<double> c(d->ctrl, d->ctrl + nnodes * d->dim);
+            if ((st = upload(s, (double **)&s->dev.ctrl, c)) != IGA_OK) goto fail;
+        }
+        if (d->weights) {
+            std::vector<double> w(d->weights, d->weights + nnodes);
+            for (double v : w)
+                if (!(v > 0.0)) { st = IGA_ERR_DOMAIN; set_error("weights must be > 0"); goto fail; }
+            if ((st = upload(s, (double **)&s->dev.wts, w)) != IGA_OK) goto fail;
+        }
+        if ((st = dalloc(s, &s->errflag, 1)) != IGA_OK) goto fail;
+        CUDA_TRY(cudaMemset(s->errflag, 0, sizeof(int)));
+        s->dev.errflag = s->errflag;
+        // quadrature-point coefficient workspace: <= 4 GiB, sized to the local element count
+        size_t want = (size_t)s->nqp_local * 512 * sizeof(double);
+        const size_t cap = (size_t)4 << 30;
+        s->work_bytes = std::min(want, cap);
+        s->work_bytes = std::max<size_t>(s->work_bytes, 1 << 20);
+        if ((st = dalloc(s, (char **)&s->work, s->work_bytes)) != IGA_OK) goto fail;
+        CUDA_TRY(cudaDeviceSynchronize());
+    }
+    cudaSetDevice(prev);
+    *out = s;
+    return IGA_OK;
+fail:
+    free_space(s);
+    cudaSetDevice(prev);
+    return st;
+}
+
+}  // namespace iga
+
+using namespace iga;
+
+extern "C" {
+
+const char *iga_last_error(void) { return g_err.c_str(); }
+const char *iga_version(void) { return "libiga 0.1 (sm_100a, fp64)"; }
+
+iga_status iga_space_create(const iga_space_desc *desc, const iga_dist *dist, int device, iga_space *out) {
+    return create(desc, dist, device, out);
+}
+
+iga_status iga_space_destroy(iga_space s) {
+    free_space(s);
+    return IGA_OK;
+}
+
+iga_status iga_space_info(iga_space s, int64_t *ndof_global, int64_t *nrows_owned, int64_t *nnz_owned,
+                          int64_t *nqp_local, int64_t owned_lo[3], int64_t owned_hi[3], int64_t elem_lo[3],
+                          int64_t elem_hi[3]) {
+    if (!s) { set_error("null space"); return IGA_ERR_PARAM; }
+    if (ndof_global) *ndof_global = s->ndof_global;
+    if (nrows_owned) *nrows_owned = s->nrows_owned;
+    if (nnz_owned) *nnz_owned = s->nnz_owned;
+    if (nqp_local) *nqp_local = s->nqp_local;
+    for (int a = 0; a < 3; a++) {
+        if (owned_lo) owned_lo[a] = s->own_lo[a];
+        if (owned_hi) owned_hi[a] = s->own_hi[a];
+        if (elem_lo) elem_lo[a] = s->el_lo[a];
+        if (elem_hi) elem_hi[a] = s->el_hi[a];
+    }
+    return IGA_OK;
+}
+
+iga_status iga_csr_pattern(iga_space s, int64_t *row_ptr, int32_t *col_idx, void *stream) {
+    if (!s || !row_ptr || !col_idx) { set_error("null argument"); return IGA_ERR_PARAM; }
+    if (s->ndof_global > 0x7fffffffLL) { set_error("global dof count exceeds int32 column indices"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    iga_status st = launch_pattern(s, row_ptr, col_idx, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
+static iga_status check_phys(iga_space s, const iga_phys *phys) {
+    if (!s || !phys) { set_error("null argument"); return IGA_ERR_PARAM; }
+    if (s->nranks > 1) { set_error("multi-rank forms go through iga_form_*_dist"); return IGA_ERR_STATE; }
+    return IGA_OK;
+}
+
+iga_status iga_form_residual(iga_space s, const iga_phys *phys, const double *U, const double *Udot, double *F,
+                             void *stream) {
+    iga_status st = check_phys(s, phys);
+    if (st != IGA_OK) return st;
+    if (!U || !F) { set_error("U and F are required"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    st = launch_form(s, phys, 0.0, 0.0, U, Udot, nullptr, F, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
+iga_status iga_form_jacobian(iga_space s, const iga_phys *phys, double a, double b, const double *U,
+                             const double *Udot, double *csr_val, double *F, void *stream) {
+    iga_status st = check_phys(s, phys);
+    if (st != IGA_OK) return st;
+    if (!U || !csr_val) { set_error("U and csr_val are required"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    st = launch_form(s, phys, a, b, U, Udot, csr_val, F, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
+iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, double b, const double *U_host,
+                                  const double *Udot_host, double *csr_val_host, double *F_host, void *stream) {
+    iga_status st = check_phys(s, phys);
+    if (st != IGA_OK) return st;
+    if (!U_host || !csr_val_host) { set_error("U and csr_val are required"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    cudaStream_t cs = (cudaStream_t)stream;
+    const size_t nU = (size_t)s->ndof_global, nF = (size_t)s->nrows_owned, nz = (size_t)s->nnz_owned;
+    // staging buffers live inside the workspace's tail is not safe (the workspace is in use);
+    // allocate transient device buffers with the stream-ordered allocator.
+    double *dU = nullptr, *dUd = nullptr, *dV = nullptr, *dF = nullptr;
+    cudaError_t ce = cudaMallocAsync(&dU, nU * sizeof(double), cs);
+    if (ce == cudaSuccess && Udot_host) ce = cudaMallocAsync(&dUd, nU * sizeof(double), cs);
+    if (ce == cudaSuccess) ce = cudaMallocAsync(&dV, nz * sizeof(double), cs);
+    if (ce == cudaSuccess && F_host) ce = cudaMallocAsync(&dF, nF * sizeof(double), cs);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(dU, U_host, nU * sizeof(double), cudaMemcpyHostToDevice, cs);
+    if (ce == cudaSuccess && Udot_host) ce = cudaMemcpyAsync(dUd, Udot_host, nU * sizeof(double), cudaMemcpyHostToDevice, cs);
+    if (ce == cudaSuccess) {
+        st = launch_form(s, phys, a, b, dU, dUd, dV, dF, cs);
+        const int nl = s->last_launches;
+        if (st == IGA_OK) ce = cudaMemcpyAsync(csr_val_host, dV, nz * sizeof(double), cudaMemcpyDeviceToHost, cs);
+        if (st == IGA_OK && ce == cudaSuccess && F_host)
+            ce = cudaMemcpyAsync(F_host, dF, nF * sizeof(double), cudaMemcpyDeviceToHost, cs);
+        s->last_launches = nl;
+    }
+    if (dU) cudaFreeAsync(dU, cs);
+    if (dUd) cudaFreeAsync(dUd, cs);
+    if (dV) cudaFreeAsync(dV, cs);
+    if (dF) cudaFreeAsync(dF, cs);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(cs);
+    cudaSetDevice(prev);
+    if (ce != cudaSuccess) { set_error(cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return st;
+}
+
+iga_status iga_space_check(iga_space s, void *stream) {
+    if (!s) { set_error("null space"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    int flag = 0;
+    cudaError_t ce = cudaStreamSynchronize((cudaStream_t)stream);
+    if (ce == cudaSuccess) ce = cudaMemcpy(&flag, s->errflag, sizeof(int), cudaMemcpyDeviceToHost);
+    if (ce == cudaSuccess) ce = cudaMemset(s->errflag, 0, sizeof(int));
+    cudaSetDevice(prev);
+    if (ce != cudaSuccess) { set_error(cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    if (flag & 1) { set_error("detJ <= 0 at a quadrature point"); return IGA_ERR_SINGULAR_MAP; }
+    if (flag & 2) { set_error("non-finite coefficient"); return IGA_ERR_NONFINITE; }
+    return IGA_OK;
+}
+
+int iga_last_launch_count(iga_space s) { return s ? s->last_launches : 0; }
+
+iga_status iga_profile_enable(iga_space s, int on) {
+    if (!s) { set_error("null space"); return IGA_ERR_PARAM; }
+    s->prof_on = on != 0;
+    return IGA_OK;
+}
+
+iga_status iga_profile_reset(iga_space s) {
+    if (!s) { set_error("null space"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    prof_collect(s);
+    s->prof_names.clear();
+    s->prof_count.clear();
+    s->prof_ms.clear();
+    cudaSetDevice(prev);
+    return IGA_OK;
+}
+
+int iga_profile_read(iga_space s, int max, char *names, int *launches, double *ms) {
+    if (!s) { set_error("null space"); return -1; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    prof_collect(s);
+    cudaSetDevice(prev);
+    const int n = (int)s->prof_names.size();
+    for (int k = 0; k < n && k < max; k++) {
+        if (names) {
+            std::strncpy(names + 32 * k, s->prof_names[k].c_str(), 31);
+            names[32 * k + 31] = 0;
+        }
+        if (launches) launches[k] = s->prof_count[k];
+        if (ms) ms[k] = s->prof_ms[k];
+    }
+    return n;
+}
+
+}  // extern "C"

@@ -1,0 +1,199 @@
+"""GPU parity: libiga (CUDA, sm_100a) vs the CPU oracle, through the C ABI.
+
+Pattern: bit-exact.  Values: within 1e-11 of the row's max |entry| (north_star), plus the
+per-term-group runs of reading A-17 so that small terms are checked on their own scale.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from parity_util import ROW_TOL, gather_rows, rowmax_rel_err, vec_rel_err
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1305_4452_b200 as iga
+    return iga
+
+
+def _gpu_assemble(iga, w, a=None, b=None, params=None, Udot=None, want_F=True):
+    sp = iga.Space.from_workload(w)
+    dev = torch.device("cuda", 0)
+    U = torch.from_numpy(w.U).to(dev)
+    Ud = torch.from_numpy(Udot if Udot is not None else w.Udot).to(dev)
+    rp, ci = sp.csr_pattern()
+    ph = iga.make_phys(w.phys, params if params is not None else w.params)
+    vals, F = sp.form_jacobian(ph, w.a if a is None else a, w.b if b is None else b, U, Ud, want_F=want_F)
+    Fr = sp.form_residual(ph, U, Ud)
+    sp.check()
+    torch.cuda.synchronize()
+    return sp, rp.cpu().numpy(), ci.cpu().numpy(), vals.cpu().numpy(), (F.cpu().numpy() if F is not None else None), \
+        Fr.cpu().numpy()
+
+
+SMALL = [(1, 16), (1, 5), (2, 3), (2, 16), (3, 5), (3, 12), (4, 2), (4, 5), (5, 5), (5, 7)]
+
+
+@pytest.mark.parametrize("cid,n", SMALL)
+def test_small_full_parity(cid, n):
+    """Whole matrix vs dense-then-CSR oracle on small meshes (several elements, ragged sizes)."""
+    iga = _gpu()
+    w = workloads.make(cid, n=n)
+    rng = np.random.default_rng(100 + cid)
+    Ud = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3) else w.Udot
+    sp, rp, ci, vals, F, Fr = _gpu_assemble(iga, w, Udot=Ud)
+    osp = oracle.Space.from_workload(w)
+    K, T, Fo = osp.assemble_dense(w.phys, w.params, w.a, w.b, w.U, Ud)
+    orp, oci, ovals = oracle.dense_to_csr(K, T)
+    assert np.array_equal(rp, orp), "row_ptr differs"
+    assert np.array_equal(ci, oci), "col_idx differs"
+    assert rowmax_rel_err(orp, ovals, vals) <= ROW_TOL
+    assert vec_rel_err(Fo, F) <= ROW_TOL
+    assert vec_rel_err(Fo, Fr) <= ROW_TOL
+
+
+@pytest.mark.parametrize("cid,n,groups", [
+    (2, 8, [dict(params=[1.0, 0.0, 0.0]), dict(params=[0.0, 1.0, 0.0])]),            # kappa | sigma
+    (3, 9, [dict(a=1.0, b=0.0), dict(a=0.0, b=1.0)]),                               # mass | d/dc
+    (5, 5, [dict(a=1.0, b=0.0), dict(a=0.0, b=1.0)]),                               # d/dUdot | d/dU
+    (1, 6, [dict(params=[1.0, 0.0, 1.0]), dict(params=[0.0, 1.0, 1.0])]),
+])
+def test_term_groups(cid, n, groups):
+    """A-17: the 1e-11 row-max rule hides small terms; check each term group on its own scale."""
+    iga = _gpu()
+    w = workloads.make(cid, n=n)
+    rng = np.random.default_rng(7)
+    Ud = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3) else w.Udot
+    osp = oracle.Space.from_workload(w)
+    for g in groups:
+        a, b, prm = g.get("a", w.a), g.get("b", w.b), g.get("params", w.params)
+        sp, rp, ci, vals, F, Fr = _gpu_assemble(iga, w, a=a, b=b, params=prm, Udot=Ud)
+        K, T, Fo = osp.assemble_dense(w.phys, prm, a, b, w.U, Ud)
+        orp, oci, ovals = oracle.dense_to_csr(K, T)
+        assert np.array_equal(ci, oci)
+        assert rowmax_rel_err(orp, ovals, vals) <= ROW_TOL, g
+        assert vec_rel_err(Fo, F) <= ROW_TOL
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_full_size_probe_rows(cid):
+    """BASELINE full sizes, the launch bench.py times: complete probe rows vs the oracle's
+    row-subset assembly (SURVEY O-10), pattern of those rows bit-exact, row lengths of ALL rows.
+    (Rows are gathered on the device: config 5's CSR is 50 GB.)"""
+    iga = _gpu()
+    w = workloads.make(cid)
+    sp = iga.Space.from_workload(w)
+    dev = torch.device("cuda", 0)
+    U = torch.from_numpy(w.U).to(dev)
+    Ud = torch.from_numpy(w.Udot).to(dev)
+    rp_d, ci_d = sp.csr_pattern()
+    ph = iga.make_phys(w.phys, w.params)
+    vals_d, F_d = sp.form_jacobian(ph, w.a, w.b, U, Ud, want_F=True)
+    Fr_d = sp.form_residual(ph, U, Ud)
+    sp.check()
+    rp = rp_d.cpu().numpy()
+    osp = oracle.Space.from_workload(w)
+    assert sp.ndof == osp.ndof and sp.nrows == osp.ndof
+    rows = workloads.probe_rows(w, nblocks_random=2, block=3 if cid != 5 else 2)
+    ref = osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, rows, Udot=w.Udot)
+    idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows])
+    idx_d = torch.from_numpy(idx).to(dev)
+    sci = ci_d[idx_d].cpu().numpy()
+    svals = vals_d[idx_d].cpu().numpy()
+    srp = np.zeros(len(rows) + 1, np.int64)
+    srp[1:] = np.cumsum(rp[rows + 1] - rp[rows])
+    assert np.array_equal(srp, ref["rowptr"])
+    assert np.array_equal(sci, ref["cols"])
+    assert ref["touched"].all()
+    assert rowmax_rel_err(ref["rowptr"], ref["vals"], svals) <= ROW_TOL
+    F = F_d.cpu().numpy()
+    Fr = Fr_d.cpu().numpy()
+    assert vec_rel_err(ref["F"], F[rows]) <= ROW_TOL
+    assert vec_rel_err(ref["F"], Fr[rows]) <= ROW_TOL
+    # every row length (closed-form row_ptr) against the oracle's Alg. 3 count
+    all_rows = np.arange(sp.nrows, dtype=np.int64)
+    rl = np.zeros(len(all_rows), np.int64)
+    import ctypes as C
+    oracle.lib().orc_pattern_rows(osp.h, len(all_rows), all_rows.ctypes.data_as(C.POINTER(C.c_int64)),
+                                  rl.ctypes.data_as(C.POINTER(C.c_int64)), None)
+    assert np.array_equal(np.diff(rp), rl)
+    assert bool(torch.isfinite(vals_d).all())
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_full_size_full_pattern(cid):
+    iga = _gpu()
+    w = workloads.make(cid)
+    sp = iga.Space.from_workload(w)
+    rp, ci = sp.csr_pattern()
+    osp = oracle.Space.from_workload(w)
+    orp, oci = osp.pattern()
+    assert np.array_equal(rp.cpu().numpy(), orp)
+    assert np.array_equal(ci.cpu().numpy(), oci)
+
+
+def test_host_variant_matches_device():
+    iga = _gpu()
+    w = workloads.make(3, n=16)
+    sp = iga.Space.from_workload(w)
+    dev = torch.device("cuda", 0)
+    ph = iga.make_phys(w.phys, w.params)
+    vals, F = sp.form_jacobian(ph, w.a, w.b, torch.from_numpy(w.U).to(dev), torch.from_numpy(w.Udot).to(dev),
+                               want_F=True)
+    vh = torch.empty(sp.nnz, dtype=torch.float64).pin_memory()
+    fh = torch.empty(sp.nrows, dtype=torch.float64).pin_memory()
+    Uh = torch.from_numpy(w.U).pin_memory()
+    Udh = torch.from_numpy(w.Udot).pin_memory()
+    sp.form_jacobian_host(ph, w.a, w.b, Uh, Udh, vh, fh)
+    osp = oracle.Space.from_workload(w)
+    K, T, Fo = osp.assemble_dense(w.phys, w.params, w.a, w.b, w.U, w.Udot)
+    orp, _, ovals = oracle.dense_to_csr(K, T)
+    assert rowmax_rel_err(orp, ovals, vh.numpy()) <= ROW_TOL
+    assert rowmax_rel_err(orp, ovals, vals.cpu().numpy()) <= ROW_TOL
+    assert vec_rel_err(Fo, fh.numpy()) <= ROW_TOL
+
+
+def test_singular_map_flag():
+    """A-7: an inverted geometry (detJ < 0) is reported as IGA_ERR_SINGULAR_MAP."""
+    iga = _gpu()
+    w = workloads.make(1, n=4)
+    w.ctrl = w.ctrl[:, :, ::-1].copy()          # swap x <-> y: orientation reversed, detJ = -1
+    sp = iga.Space.from_workload(w)
+    U = torch.zeros(sp.ndof, dtype=torch.float64, device="cuda")
+    sp.form_jacobian(iga.make_phys(w.phys, w.params), 0.0, 1.0, U)
+    with pytest.raises(iga.IgaError) as ei:
+        sp.check()
+    assert ei.value.code == 3
+
+
+def test_nonfinite_flag():
+    """c = 0 makes mu' infinite in Cahn-Hilliard: IGA_ERR_NONFINITE."""
+    iga = _gpu()
+    w = workloads.make(3, n=6)
+    sp = iga.Space.from_workload(w)
+    U = torch.zeros(sp.ndof, dtype=torch.float64, device="cuda")
+    sp.form_residual(iga.make_phys(w.phys, w.params), U)
+    with pytest.raises(iga.IgaError) as ei:
+        sp.check()
+    assert ei.value.code == 5
+
+
+def test_bad_arguments_rejected():
+    iga = _gpu()
+    w = workloads.make(3, n=6)
+    with pytest.raises(iga.IgaError):       # periodic with too few elements (< 2p+1 functions)
+        iga.Space.from_workload(workloads.make(3, n=4))
+    bad = workloads.make(1, n=4)
+    bad.knots[0] = bad.knots[0][::-1].copy()   # decreasing knots
+    with pytest.raises(iga.IgaError) as ei:
+        iga.Space.from_workload(bad)
+    assert ei.value.code == 2
+    sp = iga.Space.from_workload(w)
+    U = torch.zeros(sp.ndof, dtype=torch.float64, device="cuda")
+    with pytest.raises(iga.IgaError):       # NEOHOOKE needs dof 3 / dim 3
+        sp.form_residual(iga.make_phys(2, [1.0, 1.0]), U)
