@@ -132,6 +132,11 @@ iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, d
  * call: IGA_OK, IGA_ERR_SINGULAR_MAP or IGA_ERR_NONFINITE. */
 iga_status iga_space_check(iga_space s, void *stream);
 
+/* Tuning / testing options: "split" = 1 forces the generic two-kernel path (pointwise kernel +
+ * contraction kernel through an HBM workspace) instead of the fused kernels; 0 restores the
+ * default.  Returns IGA_ERR_PARAM for an unknown key. */
+iga_status iga_space_set_option(iga_space s, const char *key, long long value);
+
 /* Number of kernel launches the last form / pattern call issued (for the bench's gpu_launches). */
 int iga_last_launch_count(iga_space s);
 
@@ -143,6 +148,12 @@ int iga_last_launch_count(iga_space s);
 iga_status iga_profile_enable(iga_space s, int on);
 iga_status iga_profile_reset(iga_space s);
 int iga_profile_read(iga_space s, int max, char *names /* [max][32] */, int *launches, double *ms);
+
+/* Diagnostics (K8): measured ceilings on this device.  which: 0 DFMA flop/s, 1 DMMA
+ * (mma.sync m8n8k4 f64) flop/s, 2 DFMA+DMMA mixed flop/s, 3/4/5 fp64 red.add per second with
+ * 32/4/1 lanes per contiguous group into a `param`-double (default 26 MB) array, 6 store
+ * bytes/s, 7 shared-memory fp64 atomics/s.  Returns < 0 on error. */
+double iga_microbench(int device, int which, long long param);
 
 const char *iga_last_error(void);
 const char *iga_version(void);

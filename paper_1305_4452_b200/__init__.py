@@ -50,7 +50,8 @@ _lib = None
 
 EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
-           "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read"]
+           "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
+           "iga_microbench", "iga_space_set_option"]
 
 
 def lib():
@@ -78,6 +79,10 @@ def lib():
         L.iga_profile_reset.argtypes = [vp]
         L.iga_profile_read.argtypes = [vp, C.c_int, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.iga_profile_read.restype = C.c_int
+        L.iga_space_set_option.argtypes = [vp, C.c_char_p, C.c_longlong]
+        L.iga_space_set_option.restype = C.c_int
+        L.iga_microbench.argtypes = [C.c_int, C.c_int, C.c_longlong]
+        L.iga_microbench.restype = C.c_double
         L.iga_last_error.restype = C.c_char_p
         L.iga_version.restype = C.c_char_p
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
@@ -115,6 +120,20 @@ def make_phys(kind: int, params) -> _Phys:
     for i, v in enumerate(params):
         ph.p[i] = float(v)
     return ph
+
+
+MICROBENCH = {0: "dfma_flops", 1: "dmma_flops", 2: "dfma_dmma_mixed_flops", 3: "red_f64_warp_contig_per_s",
+              4: "red_f64_sector_per_s", 5: "red_f64_scattered_per_s", 6: "store_bytes_per_s",
+              7: "smem_atomic_f64_per_s", 8: "bulkred_96B_ops_per_s", 9: "red_f64_c5pattern_per_s",
+              10: "bulkred_384B_ops_per_s"}
+
+
+def microbench(device: int = 0, which=None, param: int = 0) -> dict:
+    """K8 ceilings measured on `device` (see iga.h)."""
+    out = {}
+    for k in (MICROBENCH if which is None else [which]):
+        out[MICROBENCH[k]] = float(lib().iga_microbench(device, k, param))
+    return out
 
 
 class Space:
@@ -217,6 +236,9 @@ class Space:
 
     def last_launch_count(self) -> int:
         return int(lib().iga_last_launch_count(self.h))
+
+    def set_option(self, key: str, value: int):
+        _check(lib().iga_space_set_option(self.h, key.encode(), int(value)))
 
     def profile(self, on: bool = True):
         _check(lib().iga_profile_enable(self.h, int(on)))

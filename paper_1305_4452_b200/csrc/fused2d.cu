@@ -1,0 +1,430 @@
+// fused2d.cu -- K4/K3 for 2D scalar spaces (configs 1-3): one fused kernel per call.
+//
+// A CTA owns a tile of TE0 x TE1 elements (persistent over tiles).  Per element, a group of
+// NEN lanes (16 for p=3, 9 for p=2) runs Alg. 4 for all its quadrature points at once:
+//   lane q  -> pointwise_qp (tables -> kinds -> rational/geometry -> fields -> physics), the
+//              compact coefficients D~ / r~ for its point go to a per-group shared scratch;
+//   lane B  -> test-side sum factorisation of column B of the element matrix
+//              K_e[A,B] = w_A w_B sum_q P(A,q)^T D~(q) P(B,q): H(q) = D~(q) P(B,q), then the
+//              contraction over q1 (per q0) and over q0, using the 1D tables only;
+//   lane A  -> F_e[A].
+// Element blocks are added into a shared-memory copy of the tile's CSR rows (one slot per
+// stencil offset delta in [-p,p]^2) with shared-memory atomics.  At the end of the tile, rows
+// whose whole support lies in the tile are written once with plain coalesced stores; the
+// others (tile boundary) are added with red.global.add.f64 into rows pre-zeroed by
+// k_zero_rows2d.  The CSR position of (row g, delta) comes from the per-axis Alg. 3 tables.
+#include <cstdio>
+
+#include "iga_host.h"
+#include "pointwise.cuh"
+
+namespace iga {
+
+template <int P> struct Tile2 {
+    static constexpr int TE0 = P == 3 ? 8 : 16;
+    static constexpr int TE1 = 16;
+    static constexpr int NB0 = TE0 + P, NB1 = TE1 + P;      // touched node box (uniform knots)
+    static constexpr int NSL = (2 * P + 1) * (2 * P + 1);   // stencil slots per row
+};
+
+// per axis: is function g (unique) complete in tile T of width TE (all support elements inside)
+__device__ __forceinline__ bool complete_axis(const AxisDev &ax, int g, int T, int TE) {
+    const int lo = ax.suplo[g], c = ax.supcnt[g];
+    const int hi = lo + c - 1;
+    return hi < ax.nel && lo >= T * TE && hi < (T + 1) * TE;
+}
+
+struct SmemNodes2 {
+    const double *pu, *pud, *pw, *px0, *px1;
+    int idx[16];
+    bool hud;
+    __device__ double u(int A, int) const { return pu[idx[A]]; }
+    __device__ double ud(int A, int) const { return pud[idx[A]]; }
+    __device__ bool has_ud() const { return hud; }
+    __device__ double w(int A) const { return pw ? pw[idx[A]] : 1.0; }
+    __device__ double x(int A, int i) const { return i == 0 ? px0[idx[A]] : px1[idx[A]]; }
+};
+
+// test-side sum factorisation of one column (trial function (b0,b1)) in 2D
+template <class L, class KS, int P>
+__device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], const double *__restrict__ Dg,
+                                              const double *__restrict__ tb0, const double *__restrict__ tb1,
+                                              int b0, int b1) {
+    constexpr int NP1 = P + 1, NQ1 = P + 1, NQ = NQ1 * NQ1, NC = KS::NC;
+    // tb_d layout: [q][k][a]
+#pragma unroll
+    for (int A = 0; A < NP1 * NP1; A++) Kc[A] = 0.0;
+#pragma unroll
+    for (int q0 = 0; q0 < NQ1; q0++) {
+        double S[3][NP1];
+#pragma unroll
+        for (int o = 0; o < 3; o++)
+#pragma unroll
+            for (int a = 0; a < NP1; a++) S[o][a] = 0.0;
+        double vb0[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) vb0[k] = tb0[(q0 * 3 + k) * NP1 + b0];
+#pragma unroll
+        for (int q1 = 0; q1 < NQ1; q1++) {
+            const int q = q0 * NQ1 + q1;
+            double vb1[3];
+#pragma unroll
+            for (int k = 0; k < 3; k++) vb1[k] = tb1[(q1 * 3 + k) * NP1 + b1];
+            double Pb[NC], H[NC];
+            static_for<NC>([&](auto C) {
+                constexpr int c = decltype(C)::value;
+                H[c] = 0.0;
+                Pb[c] = 0.0;
+                if constexpr (L::trial_used(c)) {
+                    static_for<KS::nterms(c)>([&](auto T) {
+                        constexpr int t = decltype(T)::value;
+                        Pb[c] += vb0[KS::ord(c, t, 0)] * vb1[KS::ord(c, t, 1)];
+                    });
+                }
+            });
+            static_for<L::NE>([&](auto E) {
+                constexpr int e = decltype(E)::value;
+                constexpr int c = L::E.c[e], c2 = L::E.c2[e];
+                H[c] += Dg[e * NQ + q] * Pb[c2];
+            });
+            // stage 1: contract q1 into tracks keyed by the axis-0 derivative order
+            static_for<NC>([&](auto C) {
+                constexpr int c = decltype(C)::value;
+                if constexpr (L::test_used(c)) {
+                    static_for<KS::nterms(c)>([&](auto T) {
+                        constexpr int t = decltype(T)::value;
+                        constexpr int o0 = KS::ord(c, t, 0), o1 = KS::ord(c, t, 1);
+#pragma unroll
+                        for (int a1 = 0; a1 < NP1; a1++) S[o0][a1] += H[c] * tb1[(q1 * 3 + o1) * NP1 + a1];
+                    });
+                }
+            });
+        }
+        // stage 2: contract q0
+#pragma unroll
+        for (int o0 = 0; o0 < 3; o0++) {
+            bool used = false;
+            static_for<NC>([&](auto C) {
+                constexpr int c = decltype(C)::value;
+                if constexpr (L::test_used(c)) {
+                    static_for<KS::nterms(c)>([&](auto T) {
+                        constexpr int t = decltype(T)::value;
+                        if (KS::ord(c, t, 0) == o0) used = true;
+                    });
+                }
+            });
+            if (!used) continue;
+#pragma unroll
+            for (int a0 = 0; a0 < NP1; a0++) {
+                const double n0 = tb0[(q0 * 3 + o0) * NP1 + a0];
+#pragma unroll
+                for (int a1 = 0; a1 < NP1; a1++) Kc[a0 * NP1 + a1] += n0 * S[o0][a1];
+            }
+        }
+    }
+}
+
+template <int P, class PH, int MODE, bool JAC>
+__global__ void __launch_bounds__(256, 1)
+k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
+          double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1) {
+    using L = Lists<PH, 2, MODE>;
+    using KS = typename L::KS;
+    using TL = Tile2<P>;
+    constexpr int NP1 = P + 1, NQ1 = P + 1, NQ = NQ1 * NQ1, NEN = NP1 * NP1;
+    constexpr int G = NEN;                  // lanes per element group
+    constexpr int GPW = 32 / G;             // groups per warp
+    constexpr int NWARP = 8, NGRP = NWARP * GPW;
+    constexpr int NB0 = TL::NB0, NB1 = TL::NB1, NBN = NB0 * NB1, NSL = TL::NSL, W2 = 2 * P + 1;
+    constexpr int NE = L::NE, NR = L::NR;
+    constexpr int SCR = (JAC ? NE : 0) + NR;
+
+    extern __shared__ __align__(16) double sm[];
+    double *rows = sm;                                  // [NBN][NSL]
+    double *Fb = rows + (JAC ? NBN * NSL : 0);          // [NBN]
+    double *nU = Fb + NBN, *nUd = nU + NBN, *nw = nUd + NBN, *nx0 = nw + NBN, *nx1 = nx0 + NBN;
+    double *tb = nx1 + NBN;                             // [2][TE][NQ1][3][NP1]
+    double *qwb = tb + 2 * TL::TE1 * NQ1 * 3 * NP1;      // [2][TE][NQ1]  weights
+    double *qxb = qwb + 2 * TL::TE1 * NQ1;              // [2][TE][NQ1]  coordinates
+    double *hpb = qxb + 2 * TL::TE1 * NQ1;              // [2][TE]
+    double *scr = hpb + 2 * TL::TE1;                    // [NGRP][SCR][NQ]
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int grp_in_warp = lane / G, t = lane % G;
+    const bool lane_ok = grp_in_warp < GPW;
+    const int grp = warp * GPW + (lane_ok ? grp_in_warp : 0);
+    double *gs = scr + (size_t)grp * SCR * NQ;
+    const AxisDev &A0 = s.ax[0], &A1 = s.ax[1];
+    const int TEd[2] = {TL::TE0, TL::TE1};
+    int errbits = 0;
+
+    for (int tile = blockIdx.x; tile < ntile0 * ntile1; tile += gridDim.x) {
+        const int T0 = tile / ntile1, T1 = tile % ntile1;
+        const int e0lo = T0 * TL::TE0, e1lo = T1 * TL::TE1;
+        const int ne0 = min(TL::TE0, A0.nel - e0lo), ne1 = min(TL::TE1, A1.nel - e1lo);
+        const int F00 = A0.first[e0lo], F01 = A1.first[e1lo];
+        const int nb0 = ne0 + P, nb1 = ne1 + P;
+        // ---- stage the tile: zero rows/F, node data, tables ----
+        if (JAC)
+            for (int i = tid; i < NBN * NSL; i += blockDim.x) rows[i] = 0.0;
+        for (int i = tid; i < NBN; i += blockDim.x) {
+            Fb[i] = 0.0;
+            const int l0 = i / NB1, l1 = i % NB1;
+            if (l0 < nb0 && l1 < nb1) {
+                int g0 = F00 + l0, g1 = F01 + l1;
+                if (g0 >= A0.nu) g0 -= A0.nu;
+                if (g1 >= A1.nu) g1 -= A1.nu;
+                const long long node = (long long)g0 * A1.nu + g1;
+                nU[i] = U[node];
+                nUd[i] = Ud ? Ud[node] : 0.0;
+                nw[i] = s.wts ? s.wts[node] : 1.0;
+                if (s.geom == IGA_GEOM_NURBS) {
+                    nx0[i] = s.ctrl[node * 2];
+                    nx1[i] = s.ctrl[node * 2 + 1];
+                }
+            }
+        }
+        for (int i = tid; i < 2 * TL::TE1 * NQ1 * 3 * NP1; i += blockDim.x) {
+            const int d = i / (TL::TE1 * NQ1 * 3 * NP1), r = i % (TL::TE1 * NQ1 * 3 * NP1);
+            const int el = r / (NQ1 * 3 * NP1);
+            const int elo = d == 0 ? e0lo : e1lo, ne = d == 0 ? ne0 : ne1;
+            if (el < ne) tb[i] = s.ax[d].tab[(size_t)(elo + el) * NQ1 * 3 * NP1 + r % (NQ1 * 3 * NP1)];
+        }
+        for (int i = tid; i < 2 * TL::TE1 * NQ1; i += blockDim.x) {
+            const int d = i / (TL::TE1 * NQ1), r = i % (TL::TE1 * NQ1);
+            const int el = r / NQ1;
+            const int elo = d == 0 ? e0lo : e1lo, ne = d == 0 ? ne0 : ne1;
+            if (el < ne) {
+                qwb[i] = s.ax[d].qw[(size_t)(elo + el) * NQ1 + r % NQ1];
+                qxb[i] = s.ax[d].qx[(size_t)(elo + el) * NQ1 + r % NQ1];
+            }
+        }
+        for (int i = tid; i < 2 * TL::TE1; i += blockDim.x) {
+            const int d = i / TL::TE1, el = i % TL::TE1;
+            const int elo = d == 0 ? e0lo : e1lo, ne = d == 0 ? ne0 : ne1;
+            if (el < ne) hpb[i] = s.ax[d].hpar[elo + el];
+        }
+        __syncthreads();
+
+        // ---- element loop: one group of G lanes per element ----
+        const int nel_tile = ne0 * ne1;
+        for (int base = 0; base < nel_tile; base += NGRP) {
+            const int el = base + grp;
+            const bool act = lane_ok && el < nel_tile;
+            const int le0 = act ? el / ne1 : 0, le1 = act ? el % ne1 : 0;
+            // local node offsets of the element's functions within the tile box
+            const int fo0 = A0.first[e0lo + le0] - F00, fo1 = A1.first[e1lo + le1] - F01;
+            const double *tb0 = tb + (size_t)(0 * TL::TE1 + le0) * NQ1 * 3 * NP1;
+            const double *tb1 = tb + (size_t)(1 * TL::TE1 + le1) * NQ1 * 3 * NP1;
+            if (act) {
+                // (1) pointwise at quadrature point q = t
+                const int q0 = t / NQ1, q1 = t % NQ1;
+                double v[2][3][NP1];
+#pragma unroll
+                for (int k = 0; k < 3; k++)
+#pragma unroll
+                    for (int x = 0; x < NP1; x++) {
+                        v[0][k][x] = tb0[(q0 * 3 + k) * NP1 + x];
+                        v[1][k][x] = tb1[(q1 * 3 + k) * NP1 + x];
+                    }
+                const double wq = qwb[le0 * NQ1 + q0] * qwb[TL::TE1 * NQ1 + le1 * NQ1 + q1];
+                const double xq[2] = {qxb[le0 * NQ1 + q0], qxb[TL::TE1 * NQ1 + le1 * NQ1 + q1]};
+                const double hp[2] = {hpb[le0], hpb[TL::TE1 + le1]};
+                SmemNodes2 nodes;
+                nodes.pu = nU; nodes.pud = nUd; nodes.pw = s.wts ? nw : nullptr; nodes.px0 = nx0; nodes.px1 = nx1;
+                nodes.hud = Ud != nullptr;
+#pragma unroll
+                for (int A = 0; A < NEN; A++) nodes.idx[A] = (fo0 + A / NP1) * NB1 + fo1 + A % NP1;
+                errbits |= pointwise_qp<2, P, PH, MODE, JAC>(s, prm, a, b, v, wq, xq, hp, nodes,
+                                                             JAC ? gs + t : nullptr, NQ,
+                                                             Fout ? gs + (JAC ? NE * NQ : 0) + t : nullptr, NQ);
+            }
+            __syncwarp();
+            if (act) {
+                const int c0 = t / NP1, c1 = t % NP1;          // this lane's local function (A or B)
+                const int nidx = (fo0 + c0) * NB1 + fo1 + c1;
+                const double sw = s.wts ? nw[nidx] : 1.0;
+                // (2) residual F_e[A], A = t
+                if (Fout) {
+                    const double *Rg = gs + (JAC ? NE * NQ : 0);
+                    double acc = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NQ; q++) {
+                        double vv[2][3][NP1];
+#pragma unroll
+                        for (int k = 0; k < 3; k++)
+#pragma unroll
+                            for (int x = 0; x < NP1; x++) {
+                                vv[0][k][x] = tb0[((q / NQ1) * 3 + k) * NP1 + x];
+                                vv[1][k][x] = tb1[((q % NQ1) * 3 + k) * NP1 + x];
+                            }
+                        const int aa[3] = {c0, c1, 0};
+                        static_for<NR>([&](auto RR) {
+                            constexpr int rr = decltype(RR)::value;
+                            constexpr int c = L::R.c[rr];
+                            acc += kind_value<KS, 2, c, NP1>(vv, aa) * Rg[rr * NQ + q];
+                        });
+                    }
+                    atomicAdd(Fb + nidx, sw * acc);
+                }
+                // (3) Jacobian column B = t
+                if constexpr (JAC) {
+                    double Kc[NEN];
+                    tsf_column_2d<L, KS, P>(Kc, gs, tb0, tb1, c0, c1);
+#pragma unroll
+                    for (int A = 0; A < NEN; A++) {
+                        const int a0 = A / NP1, a1 = A % NP1;
+                        const int ridx = (fo0 + a0) * NB1 + fo1 + a1;
+                        const double sa = s.wts ? nw[ridx] : 1.0;
+                        const int slot = (c0 - a0 + P) * W2 + (c1 - a1 + P);
+                        atomicAdd(rows + ridx * NSL + slot, sa * sw * Kc[A]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+
+        // ---- write-out: complete rows with plain stores, boundary rows with red.add ----
+        const long long T1s = A1.T;
+        if (JAC) {
+            for (int i = tid; i < NBN * NSL; i += blockDim.x) {
+                const int node = i / NSL, slot = i % NSL;
+                const int l0 = node / NB1, l1 = node % NB1;
+                if (l0 >= nb0 || l1 >= nb1) continue;
+                int g0 = F00 + l0, g1 = F01 + l1;
+                if (g0 >= A0.nu) g0 -= A0.nu;
+                if (g1 >= A1.nu) g1 -= A1.nu;
+                const int d0 = slot / W2 - P, d1 = slot % W2 - P;
+                const int p0 = A0.posd[g0 * W2 + d0 + P], p1 = A1.posd[g1 * W2 + d1 + P];
+                if (p0 < 0 || p1 < 0) continue;
+                const bool uniq = (l0 < A0.nu && l0 + A0.nu >= nb0) && (l1 < A1.nu && l1 + A1.nu >= nb1);
+                const bool comp = uniq && complete_axis(A0, g0, T0, TEd[0]) && complete_axis(A1, g1, T1, TEd[1]);
+                const long long addr = A0.rowS[g0] * T1s + (long long)A0.rowW[g0] * A1.rowS[g1]
+                                       + (long long)p0 * A1.rowW[g1] + p1;
+                const double vv = rows[i];
+                if (comp) val[addr] = vv;
+                else if (vv != 0.0) atomicAdd(val + addr, vv);
+            }
+        }
+        if (Fout) {
+            for (int i = tid; i < NBN; i += blockDim.x) {
+                const int l0 = i / NB1, l1 = i % NB1;
+                if (l0 >= nb0 || l1 >= nb1) continue;
+                int g0 = F00 + l0, g1 = F01 + l1;
+                if (g0 >= A0.nu) g0 -= A0.nu;
+                if (g1 >= A1.nu) g1 -= A1.nu;
+                if (Fb[i] != 0.0) atomicAdd(Fout + (long long)g0 * A1.nu + g1, Fb[i]);
+            }
+        }
+        __syncthreads();
+    }
+    if (errbits) atomicOr(s.errflag, errbits);
+}
+
+// zero the CSR rows that are NOT complete inside their owner tile (they receive red.add)
+template <int P>
+__global__ void k_zero_rows2d(SpaceDev s, double *__restrict__ val) {
+    using TL = Tile2<P>;
+    const AxisDev &A0 = s.ax[0], &A1 = s.ax[1];
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long nrows = (long long)A0.nu * A1.nu;
+    if (warp >= nrows) return;
+    const int g0 = (int)(warp / A1.nu), g1 = (int)(warp % A1.nu);
+    const int T0 = A0.suplo[g0] / TL::TE0, T1 = A1.suplo[g1] / TL::TE1;
+    // same test as the fused kernel's write-out, including the unique-copy condition
+    const int l0 = ((g0 - A0.first[T0 * TL::TE0]) % A0.nu + A0.nu) % A0.nu;
+    const int l1 = ((g1 - A1.first[T1 * TL::TE1]) % A1.nu + A1.nu) % A1.nu;
+    const int nb0 = min(TL::TE0, A0.nel - T0 * TL::TE0) + P, nb1 = min(TL::TE1, A1.nel - T1 * TL::TE1) + P;
+    const bool uniq = (l0 + A0.nu >= nb0) && (l1 + A1.nu >= nb1);
+    const bool comp = uniq && complete_axis(A0, g0, T0, TL::TE0) && complete_axis(A1, g1, T1, TL::TE1);
+    if (comp) return;
+    const long long start = A0.rowS[g0] * A1.T + (long long)A0.rowW[g0] * A1.rowS[g1];
+    const int len = A0.rowW[g0] * A1.rowW[g1];
+    for (int k = lane; k < len; k += 32) val[start + k] = 0.0;
+}
+
+template <int P, class PH, int MODE>
+static size_t fused2d_smem(bool jac) {
+    using L = Lists<PH, 2, MODE>;
+    using TL = Tile2<P>;
+    constexpr int NQ1 = P + 1, NP1 = P + 1, NQ = NQ1 * NQ1;
+    constexpr int NGRP = 8 * (32 / (NP1 * NP1));
+    const int NBN = TL::NB0 * TL::NB1;
+    size_t n = (jac ? (size_t)NBN * TL::NSL : 0) + 6 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
+               + 2 * TL::TE1 + (size_t)NGRP * ((jac ? L::NE : 0) + L::NR) * NQ;
+    return n * sizeof(double);
+}
+
+template <int P, class PH, int MODE>
+iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U, const double *Ud,
+                       double *val, double *F, cudaStream_t st, int nsm) {
+    using TL = Tile2<P>;
+    Prm prm;
+    for (int i = 0; i < 8; i++) prm.p[i] = phys->p[i];
+    const bool jac = val != nullptr;
+    const int nt0 = (s->nel[0] + TL::TE0 - 1) / TL::TE0, nt1 = (s->nel[1] + TL::TE1 - 1) / TL::TE1;
+    const size_t smem = fused2d_smem<P, PH, MODE>(jac);
+    static bool attr[2] = {false, false};
+    if (!attr[jac]) {
+        cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused2d<P, PH, MODE, true>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(k_fused2d<P, PH, MODE, false>,
+                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (ce != cudaSuccess) { set_error(std::string("fused2d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+        attr[jac] = true;
+    }
+    int occ = 1;
+    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, true>, 256, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, false>, 256, smem);
+    occ = std::max(occ, 1);
+    const int grid = std::min(nt0 * nt1, nsm * occ);
+    int launches = 0;
+    if (F) {
+        ProfScope ps(s, "k_zero", st);
+        k_zero_vec(F, s->nrows_owned, st, nsm);
+        launches++;
+    }
+    if (jac) {
+        ProfScope ps(s, "k_zero_rows2d", st);
+        const long long nrows = (long long)s->nu[0] * s->nu[1];
+        k_zero_rows2d<P><<<(unsigned)((nrows * 32 + 255) / 256), 256, 0, st>>>(s->dev, val);
+        launches++;
+    }
+    {
+        ProfScope ps(s, "k_fused2d", st);
+        if (jac) k_fused2d<P, PH, MODE, true><<<grid, 256, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
+        else k_fused2d<P, PH, MODE, false><<<grid, 256, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
+        launches++;
+    }
+    s->last_launches = launches;
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) { set_error(std::string("fused2d launch: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return IGA_OK;
+}
+
+// dispatch: returns IGA_ERR_STATE if the fused 2D path does not apply (caller falls back)
+iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                          const double *Ud, double *val, double *F, cudaStream_t st, int nsm) {
+    if (s->dim != 2 || s->dof != 1 || s->nranks != 1) return IGA_ERR_STATE;
+    if (!s->dev.ax[0].uniform || !s->dev.ax[1].uniform) return IGA_ERR_STATE;
+    if (s->p[0] != s->p[1]) return IGA_ERR_STATE;
+    const int p = s->p[0];
+    const bool nurbs = s->mode == MODE_NURBS;
+    if (ph->kind == IGA_PHYS_LAPLACE) {
+        if (p == 2) return nurbs ? run_fused2d<2, PhysLaplace, MODE_NURBS>(s, ph, a, b, U, Ud, val, F, st, nsm)
+                                 : run_fused2d<2, PhysLaplace, MODE_PARAM>(s, ph, a, b, U, Ud, val, F, st, nsm);
+        if (p == 3) return nurbs ? run_fused2d<3, PhysLaplace, MODE_NURBS>(s, ph, a, b, U, Ud, val, F, st, nsm)
+                                 : run_fused2d<3, PhysLaplace, MODE_PARAM>(s, ph, a, b, U, Ud, val, F, st, nsm);
+    }
+    if (ph->kind == IGA_PHYS_CAHN_HILLIARD) {
+        if (p == 2) return nurbs ? run_fused2d<2, PhysCahnHilliard, MODE_NURBS>(s, ph, a, b, U, Ud, val, F, st, nsm)
+                                 : run_fused2d<2, PhysCahnHilliard, MODE_PARAM>(s, ph, a, b, U, Ud, val, F, st, nsm);
+        if (p == 3) return nurbs ? run_fused2d<3, PhysCahnHilliard, MODE_NURBS>(s, ph, a, b, U, Ud, val, F, st, nsm)
+                                 : run_fused2d<3, PhysCahnHilliard, MODE_PARAM>(s, ph, a, b, U, Ud, val, F, st, nsm);
+    }
+    return IGA_ERR_STATE;
+}
+
+}  // namespace iga

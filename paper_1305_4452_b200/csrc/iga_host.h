@@ -26,6 +26,7 @@ struct iga_space_s {
     size_t work_bytes = 0;
     int *errflag = nullptr;
     int last_launches = 0;
+    int force_split = 0;                 // 1: use the generic split kernels (tests / A-B checks)
     // kernel timing hook (iga_profile_*)
     struct ProfRec { const char *name; cudaEvent_t a, b; };
     bool prof_on = false;
@@ -49,5 +50,8 @@ struct ProfScope {
 void set_error(const std::string &msg);
 iga_status launch_form(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
                        const double *Udot, double *csr_val, double *F, cudaStream_t st);
+void k_zero_vec(double *p, long long n, cudaStream_t st, int nsm);
+iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                          const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st);
 }  // namespace iga

@@ -35,6 +35,10 @@ struct AxisDev {
     long long T;              // sum of rowW over the owned range
     int own_lo, own_hi;       // owned function range [lo, hi)
     int el_lo, el_hi;         // this rank's element range [lo, hi)
+    const int *suplo;         // [nu] first element of the (cyclic) support of function g
+    const int *supcnt;        // [nu] number of elements in that support
+    const int *posd;          // [nu][2p+1] position of column g+delta in row g's list, or -1
+    int uniform;              // first[e+1] == first[e] + 1 for all e (simple interior knots)
 };
 
 struct SpaceDev {

@@ -345,6 +345,10 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             if ((st = upload(s, (int **)&ax.rowW, one_i)) != IGA_OK) goto fail;
             if ((st = upload(s, (long long **)&ax.rowS, zl)) != IGA_OK) goto fail;
             if ((st = upload(s, (int **)&ax.cols, zc)) != IGA_OK) goto fail;
+            if ((st = upload(s, (int **)&ax.suplo, z)) != IGA_OK) goto fail;
+            if ((st = upload(s, (int **)&ax.supcnt, one_i)) != IGA_OK) goto fail;
+            if ((st = upload(s, (int **)&ax.posd, z)) != IGA_OK) goto fail;
+            ax.uniform = 1;
             ax.colmax = 1; ax.T = 1; ax.own_lo = 0; ax.own_hi = 1; ax.el_lo = 0; ax.el_hi = 1;
             s->own_lo[a] = 0; s->own_hi[a] = 1; s->el_lo[a] = 0; s->el_hi[a] = 1;
             continue;
@@ -433,6 +437,37 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         for (int g = 0; g < nu; g++)
             if (last_el[g] >= el_lo && last_el[g] < el_hi) { own_lo = std::min(own_lo, g); own_hi = std::max(own_hi, g + 1); }
         if (own_hi <= own_lo) { own_lo = own_hi = 0; }
+        // cyclic support [suplo, suplo+supcnt) of each unique function, and delta positions
+        std::vector<int> suplo(nu, 0), supcnt(nu, 0), posd((size_t)nu * (2 * p + 1), -1);
+        {
+            std::vector<std::vector<int>> sup(nu);
+            for (int e = 0; e < nel; e++)
+                for (int al = 0; al <= p; al++) sup[(first[e] + al) % nu].push_back(e);
+            for (int g = 0; g < nu; g++) {
+                auto &v = sup[g];
+                std::sort(v.begin(), v.end());
+                v.erase(std::unique(v.begin(), v.end()), v.end());
+                const int c = (int)v.size();
+                int lo = c ? v[0] : 0;
+                // cyclic start: the element whose predecessor (mod nel) is not in the support
+                for (int k = 0; k < c; k++) {
+                    const int prev = (v[k] - 1 + nel) % nel;
+                    if (!std::binary_search(v.begin(), v.end(), prev)) { lo = v[k]; break; }
+                }
+                suplo[g] = lo;
+                supcnt[g] = c;
+                for (int dl = -p; dl <= p; dl++) {
+                    if (!s->periodic[a] && (g + dl < 0 || g + dl >= nu)) continue;   // no wrap on open axes
+                    const int col = (((g + dl) % nu) + nu) % nu;
+                    const auto &cs = colset[g];
+                    auto it = std::lower_bound(cs.begin(), cs.end(), col);
+                    if (it != cs.end() && *it == col) posd[(size_t)g * (2 * p + 1) + dl + p] = (int)(it - cs.begin());
+                }
+            }
+        }
+        int uniform = 1;
+        for (int e = 0; e + 1 < nel; e++)
+            if (first[e + 1] != first[e] + 1) uniform = 0;
         std::vector<long long> rowS(nu, 0);
         long long T = 0;
         for (int g = own_lo; g < own_hi; g++) { rowS[g] = T; T += rowW[g]; }
@@ -453,6 +488,10 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         if ((st = upload(s, (int **)&ax.rowW, rowW)) != IGA_OK) goto fail;
         if ((st = upload(s, (long long **)&ax.rowS, rowS)) != IGA_OK) goto fail;
         if ((st = upload(s, (int **)&ax.cols, cols)) != IGA_OK) goto fail;
+        if ((st = upload(s, (int **)&ax.suplo, suplo)) != IGA_OK) goto fail;
+        if ((st = upload(s, (int **)&ax.supcnt, supcnt)) != IGA_OK) goto fail;
+        if ((st = upload(s, (int **)&ax.posd, posd)) != IGA_OK) goto fail;
+        ax.uniform = uniform;
         if ((st = dalloc(s, &dtab, (size_t)nel * nq * 3 * (p + 1))) != IGA_OK) goto fail;
         {
             const int nt = nel * nq;
@@ -645,6 +684,13 @@ iga_status iga_space_check(iga_space s, void *stream) {
 }
 
 int iga_last_launch_count(iga_space s) { return s ? s->last_launches : 0; }
+
+iga_status iga_space_set_option(iga_space s, const char *key, long long value) {
+    if (!s || !key) { set_error("null argument"); return IGA_ERR_PARAM; }
+    if (std::strcmp(key, "split") == 0) { s->force_split = value != 0; return IGA_OK; }
+    set_error(std::string("unknown option ") + key);
+    return IGA_ERR_PARAM;
+}
 
 iga_status iga_profile_enable(iga_space s, int on) {
     if (!s) { set_error("null space"); return IGA_ERR_PARAM; }

@@ -21,8 +21,10 @@ def _gpu():
     return iga
 
 
-def _gpu_assemble(iga, w, a=None, b=None, params=None, Udot=None, want_F=True):
+def _gpu_assemble(iga, w, a=None, b=None, params=None, Udot=None, want_F=True, split=False):
     sp = iga.Space.from_workload(w)
+    if split:
+        sp.set_option("split", 1)
     dev = torch.device("cuda", 0)
     U = torch.from_numpy(w.U).to(dev)
     Ud = torch.from_numpy(Udot if Udot is not None else w.Udot).to(dev)
@@ -39,14 +41,19 @@ def _gpu_assemble(iga, w, a=None, b=None, params=None, Udot=None, want_F=True):
 SMALL = [(1, 16), (1, 5), (2, 3), (2, 16), (3, 5), (3, 12), (4, 2), (4, 5), (5, 5), (5, 7)]
 
 
-@pytest.mark.parametrize("cid,n", SMALL)
-def test_small_full_parity(cid, n):
-    """Whole matrix vs dense-then-CSR oracle on small meshes (several elements, ragged sizes)."""
+SMALL_2D_TILES = [(1, 17), (2, 9), (2, 21), (3, 16), (3, 33), (3, 40)]   # several tiles + ragged tails
+
+
+@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("cid,n", SMALL + SMALL_2D_TILES)
+def test_small_full_parity(cid, n, split):
+    """Whole matrix vs dense-then-CSR oracle on small meshes (several elements / tiles, ragged
+    sizes), through both the fused kernels and the generic split path."""
     iga = _gpu()
     w = workloads.make(cid, n=n)
     rng = np.random.default_rng(100 + cid)
     Ud = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3) else w.Udot
-    sp, rp, ci, vals, F, Fr = _gpu_assemble(iga, w, Udot=Ud)
+    sp, rp, ci, vals, F, Fr = _gpu_assemble(iga, w, Udot=Ud, split=split)
     osp = oracle.Space.from_workload(w)
     K, T, Fo = osp.assemble_dense(w.phys, w.params, w.a, w.b, w.U, Ud)
     orp, oci, ovals = oracle.dense_to_csr(K, T)
