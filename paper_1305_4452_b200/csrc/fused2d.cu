@@ -23,6 +23,7 @@ namespace iga {
 template <int P> struct Tile2 {
     static constexpr int TE0 = P == 3 ? 8 : 16;
     static constexpr int TE1 = 16;
+    static constexpr int NWARP = 12;                          // 384 threads (168 regs), 1 CTA / SM
     static constexpr int NB0 = TE0 + P, NB1 = TE1 + P;      // touched node box (uniform knots)
     static constexpr int NSL = (2 * P + 1) * (2 * P + 1);   // stencil slots per row
 };
@@ -34,15 +35,18 @@ __device__ __forceinline__ bool complete_axis(const AxisDev &ax, int g, int T, i
     return hi < ax.nel && lo >= T * TE && hi < (T + 1) * TE;
 }
 
+// element's nodes in the tile box: local function A = (a0, a1) -> box index base + a0*NB1 + a1
+template <int NP1, int NB1>
 struct SmemNodes2 {
     const double *pu, *pud, *pw, *px0, *px1;
-    int idx[16];
+    int base;
     bool hud;
-    __device__ double u(int A, int) const { return pu[idx[A]]; }
-    __device__ double ud(int A, int) const { return pud[idx[A]]; }
-    __device__ bool has_ud() const { return hud; }
-    __device__ double w(int A) const { return pw ? pw[idx[A]] : 1.0; }
-    __device__ double x(int A, int i) const { return i == 0 ? px0[idx[A]] : px1[idx[A]]; }
+    __device__ __forceinline__ int idx(int A) const { return base + (A / NP1) * NB1 + A % NP1; }
+    __device__ __forceinline__ double u(int A, int) const { return pu[idx(A)]; }
+    __device__ __forceinline__ double ud(int A, int) const { return pud[idx(A)]; }
+    __device__ __forceinline__ bool has_ud() const { return hud; }
+    __device__ __forceinline__ double w(int A) const { return pw ? pw[idx(A)] : 1.0; }
+    __device__ __forceinline__ double x(int A, int i) const { return i == 0 ? px0[idx(A)] : px1[idx(A)]; }
 };
 
 // test-side sum factorisation of one column (trial function (b0,b1)) in 2D
@@ -125,7 +129,7 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
 }
 
 template <int P, class PH, int MODE, bool JAC>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(32 * Tile2<P>::NWARP, 1)
 k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1) {
     using L = Lists<PH, 2, MODE>;
@@ -134,7 +138,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     constexpr int NP1 = P + 1, NQ1 = P + 1, NQ = NQ1 * NQ1, NEN = NP1 * NP1;
     constexpr int G = NEN;                  // lanes per element group
     constexpr int GPW = 32 / G;             // groups per warp
-    constexpr int NWARP = 8, NGRP = NWARP * GPW;
+    constexpr int NWARP = TL::NWARP, NGRP = NWARP * GPW;
     constexpr int NB0 = TL::NB0, NB1 = TL::NB1, NBN = NB0 * NB1, NSL = TL::NSL, W2 = 2 * P + 1;
     constexpr int NE = L::NE, NR = L::NR;
     constexpr int SCR = (JAC ? NE : 0) + NR;
@@ -230,12 +234,11 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 const double wq = qwb[le0 * NQ1 + q0] * qwb[TL::TE1 * NQ1 + le1 * NQ1 + q1];
                 const double xq[2] = {qxb[le0 * NQ1 + q0], qxb[TL::TE1 * NQ1 + le1 * NQ1 + q1]};
                 const double hp[2] = {hpb[le0], hpb[TL::TE1 + le1]};
-                SmemNodes2 nodes;
+                SmemNodes2<NP1, NB1> nodes;
                 nodes.pu = nU; nodes.pud = nUd; nodes.pw = s.wts ? nw : nullptr; nodes.px0 = nx0; nodes.px1 = nx1;
                 nodes.hud = Ud != nullptr;
-#pragma unroll
-                for (int A = 0; A < NEN; A++) nodes.idx[A] = (fo0 + A / NP1) * NB1 + fo1 + A % NP1;
-                errbits |= pointwise_qp<2, P, PH, MODE, JAC>(s, prm, a, b, v, wq, xq, hp, nodes,
+                nodes.base = fo0 * NB1 + fo1;
+                errbits |= pointwise_qp<2, P, PH, MODE, JAC, SmemNodes2<NP1, NB1>, true>(s, prm, a, b, v, wq, xq, hp, nodes,
                                                              JAC ? gs + t : nullptr, NQ,
                                                              Fout ? gs + (JAC ? NE * NQ : 0) + t : nullptr, NQ);
             }
@@ -250,19 +253,22 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     double acc = 0.0;
 #pragma unroll
                     for (int q = 0; q < NQ; q++) {
-                        double vv[2][3][NP1];
+                        const int q0 = q / NQ1, q1 = q % NQ1;
+                        double va0[3], va1[3];
 #pragma unroll
-                        for (int k = 0; k < 3; k++)
-#pragma unroll
-                            for (int x = 0; x < NP1; x++) {
-                                vv[0][k][x] = tb0[((q / NQ1) * 3 + k) * NP1 + x];
-                                vv[1][k][x] = tb1[((q % NQ1) * 3 + k) * NP1 + x];
-                            }
-                        const int aa[3] = {c0, c1, 0};
+                        for (int k = 0; k < 3; k++) {
+                            va0[k] = tb0[(q0 * 3 + k) * NP1 + c0];
+                            va1[k] = tb1[(q1 * 3 + k) * NP1 + c1];
+                        }
                         static_for<NR>([&](auto RR) {
                             constexpr int rr = decltype(RR)::value;
                             constexpr int c = L::R.c[rr];
-                            acc += kind_value<KS, 2, c, NP1>(vv, aa) * Rg[rr * NQ + q];
+                            double pv = 0.0;
+                            static_for<KS::nterms(c)>([&](auto TT) {
+                                constexpr int tt = decltype(TT)::value;
+                                pv += va0[KS::ord(c, tt, 0)] * va1[KS::ord(c, tt, 1)];
+                            });
+                            acc += pv * Rg[rr * NQ + q];
                         });
                     }
                     atomicAdd(Fb + nidx, sw * acc);
@@ -350,7 +356,7 @@ static size_t fused2d_smem(bool jac) {
     using L = Lists<PH, 2, MODE>;
     using TL = Tile2<P>;
     constexpr int NQ1 = P + 1, NP1 = P + 1, NQ = NQ1 * NQ1;
-    constexpr int NGRP = 8 * (32 / (NP1 * NP1));
+    constexpr int NGRP = TL::NWARP * (32 / (NP1 * NP1));
     const int NBN = TL::NB0 * TL::NB1;
     size_t n = (jac ? (size_t)NBN * TL::NSL : 0) + 6 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
                + 2 * TL::TE1 + (size_t)NGRP * ((jac ? L::NE : 0) + L::NR) * NQ;
@@ -376,8 +382,9 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
         attr[jac] = true;
     }
     int occ = 1;
-    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, true>, 256, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, false>, 256, smem);
+    constexpr int NT = 32 * TL::NWARP;
+    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, true>, NT, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, false>, NT, smem);
     occ = std::max(occ, 1);
     const int grid = std::min(nt0 * nt1, nsm * occ);
     int launches = 0;
@@ -394,8 +401,8 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
     }
     {
         ProfScope ps(s, "k_fused2d", st);
-        if (jac) k_fused2d<P, PH, MODE, true><<<grid, 256, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
-        else k_fused2d<P, PH, MODE, false><<<grid, 256, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
+        if (jac) k_fused2d<P, PH, MODE, true><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
+        else k_fused2d<P, PH, MODE, false><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
         launches++;
     }
     s->last_launches = launches;

@@ -31,7 +31,7 @@ __device__ __forceinline__ double kind_value(const V &v, const int *aa) {
 
 // Nodes: accessor with u(A,m), ud(A,m), has_ud(), w(A), x(A,i) for the element's local functions.
 // Returns error bits (1: detJ <= 0, 2: non-finite).
-template <int DIM, int P, class PH, int MODE, bool JAC, class Nodes>
+template <int DIM, int P, class PH, int MODE, bool JAC, class Nodes, bool UNROLL_A = false>
 __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, double a, double b,
                                             const double (&v)[DIM][3][P + 1], double wq, const double (&xq)[DIM],
                                             const double (&hp)[DIM], const Nodes &nodes, double *__restrict__ Dt,
@@ -55,8 +55,7 @@ __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, d
     const bool nurbs_geom = (MODE == MODE_NURBS) && s.geom == IGA_GEOM_NURBS;
 
     constexpr int NEN = ipow(NP1, DIM);
-#pragma unroll 1
-    for (int A = 0; A < NEN; A++) {
+    auto body = [&](int A) {
         int aa[3] = {0, 0, 0};
         {
             int r = A;
@@ -89,6 +88,12 @@ __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, d
             for (int c = 0; c < NC; c++) Phi[m][c] += uA * Pc[c];
             if (nodes.has_ud()) Phit[m] += wA * nodes.ud(A, m) * Pc[0];
         }
+    };
+    if constexpr (UNROLL_A) {
+        static_for<NEN>([&](auto AA) { body(decltype(AA)::value); });
+    } else {
+#pragma unroll 1
+        for (int A = 0; A < NEN; A++) body(A);
     }
 
     Fields<DIM, M> F;

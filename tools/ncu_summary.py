@@ -1,0 +1,23 @@
+import csv, subprocess, sys
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(out.splitlines()))
+h, u, v = r[0], r[1], r[2]
+keys = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum', 'launch__registers_per_thread',
+        'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active', 'sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active',
+        'smsp__inst_executed.sum', 'sm__warps_active.avg.pct_of_peak_sustained_active', 'smsp__issue_active.avg.pct_of_peak_sustained_active',
+        'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 'smsp__sass_inst_executed_op_local_ld.sum',
+        'smsp__inst_executed_pipe_fp64.sum', 'sm__sass_thread_inst_executed_op_dfma_pred_on.sum',
+        'smsp__sass_inst_executed_op_shared_atom.sum', 'smsp__sass_inst_executed_op_shared_ld.sum',
+        'smsp__sass_inst_executed_op_shared_st.sum', 'smsp__sass_inst_executed_op_global_red.sum',
+        'lts__t_sectors_op_red.sum', 'sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active',
+        'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum']
+for i, name in enumerate(h):
+    if name in keys:
+        print(f"{name:70s} {v[i]:>18s} {u[i]}")
+    elif name.startswith('smsp__average_warps_issue_stalled') and name.endswith('per_issue_active.ratio'):
+        try:
+            if float(v[i]) >= 0.2:
+                print(f"{name:70s} {v[i]:>18s}")
+        except ValueError:
+            pass
