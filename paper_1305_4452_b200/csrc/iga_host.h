@@ -53,5 +53,7 @@ iga_status launch_form(iga_space_s *s, const iga_phys *phys, double a, double b,
 void k_zero_vec(double *p, long long n, cudaStream_t st, int nsm);
 iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
+iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                          const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st);
 }  // namespace iga

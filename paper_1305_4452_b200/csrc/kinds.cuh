@@ -113,7 +113,44 @@ struct Lists {
                 if (crmask(c, i)) { L.c[L.n] = c; L.i[L.n] = i; L.n++; }
         return L;
     }
+    // the same entries ordered by (i, j, c, c2): one contiguous run per component pair
+    static constexpr EList make_eij() {
+        EList L{};
+        L.n = 0;
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < M; j++)
+                for (int c = 0; c < NC; c++)
+                    for (int c2 = 0; c2 < NC; c2++)
+                        if (cmask(c, i, c2, j)) {
+                            L.c[L.n] = c; L.i[L.n] = i; L.c2[L.n] = c2; L.j[L.n] = j; L.n++;
+                        }
+        return L;
+    }
     static constexpr EList E = make_e();
+    static constexpr EList EIJ = make_eij();
+    static constexpr int eij_start(int i, int j) {
+        for (int e = 0; e < EIJ.n; e++)
+            if (EIJ.i[e] == i && EIJ.j[e] == j) return e;
+        return EIJ.n;
+    }
+    static constexpr int eij_count(int i, int j) {
+        int n = 0;
+        for (int e = 0; e < EIJ.n; e++)
+            if (EIJ.i[e] == i && EIJ.j[e] == j) n++;
+        return n;
+    }
+    // position of entry ee (in E order) within EIJ
+    static constexpr int eij_of(int ee) {
+        for (int e = 0; e < EIJ.n; e++)
+            if (EIJ.i[e] == E.i[ee] && EIJ.j[e] == E.j[ee] && EIJ.c[e] == E.c[ee] && EIJ.c2[e] == E.c2[ee]) return e;
+        return -1;
+    }
+    // is (c, i) a test row of some entry with trial component j
+    static constexpr bool test_used_ij(int c, int i, int j) {
+        for (int e = 0; e < EIJ.n; e++)
+            if (EIJ.c[e] == c && EIJ.i[e] == i && EIJ.j[e] == j) return true;
+        return false;
+    }
     static constexpr RList R = make_r();
     static constexpr int NE = E.n;
     static constexpr int NR = R.n;
@@ -128,6 +165,13 @@ struct Lists {
         return false;
     }
     static_assert(NE <= MAXE && NR <= MAXR, "coefficient list too long");
+    // dense per-(i,j) blocks over the union of test kinds (TK) and trial kinds (QK)
+    static constexpr int NTK = [] { int n = 0; for (int c = 0; c < NC; c++) if (test_used(c)) n++; return n; }();
+    static constexpr int NQK = [] { int n = 0; for (int c = 0; c < NC; c++) if (trial_used(c)) n++; return n; }();
+    static constexpr int tk(int t) { int n = 0; for (int c = 0; c < NC; c++) if (test_used(c)) { if (n == t) return c; n++; } return -1; }
+    static constexpr int qk(int t) { int n = 0; for (int c = 0; c < NC; c++) if (trial_used(c)) { if (n == t) return c; n++; } return -1; }
+    static constexpr int tk_of(int c) { int n = 0; for (int x = 0; x < NC; x++) if (test_used(x)) { if (x == c) return n; n++; } return -1; }
+    static constexpr int qk_of(int c) { int n = 0; for (int x = 0; x < NC; x++) if (trial_used(x)) { if (x == c) return n; n++; } return -1; }
 };
 
 // compile-time loop
