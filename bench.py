@@ -188,6 +188,9 @@ def run_iga(args, w, ws, rank, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     sp = iga.Space.from_workload(w, device=local)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        sp.set_option(k, int(v))
     stream = torch.cuda.current_stream()
     U = torch.from_numpy(w.U).to(dev)
     Ud = torch.from_numpy(w.Udot).to(dev)
@@ -348,6 +351,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="elements per axis (default: BASELINE size)")
     ap.add_argument("--impl", default="iga", choices=["iga", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--opt", action="append", default=[], help="libiga option key=value (experiments)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "iga" else args.warmup
     ws, rank, local = dist_env()

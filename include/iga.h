@@ -133,8 +133,9 @@ iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, d
 iga_status iga_space_check(iga_space s, void *stream);
 
 /* Tuning / testing options: "split" = 1 forces the generic two-kernel path (pointwise kernel +
- * contraction kernel through an HBM workspace) instead of the fused kernels; 0 restores the
- * default.  Returns IGA_ERR_PARAM for an unknown key. */
+ * contraction kernel through an HBM workspace) instead of the fused kernels; "general" = 1
+ * disables the uniform-table fast paths (per-element tables always read from memory); 0
+ * restores the default.  Returns IGA_ERR_PARAM for an unknown key. */
 iga_status iga_space_set_option(iga_space s, const char *key, long long value);
 
 /* Number of kernel launches the last form / pattern call issued (for the bench's gpu_launches). */

@@ -1,21 +1,23 @@
 // fused3d.cu -- K3/K4 for 3D parametric spaces (configs 4, 5): one fused kernel per call.
 //
-// Persistent CTAs walk the element grid; per element the CTA runs Alg. 4 in phases
-// separated by __syncthreads, everything staged in shared memory:
-//   1. stage U_e, the element's 1D tables (3 axes), Gauss weights, CSR row starts and the
-//      per-element column-offset table colOff[A][B] (closed form from the Alg. 3 tables);
-//   2. field kinds at every point  Phi[q][m][k] = sum_A U_Am P_k(A,q)  (thread per (q, m)) and the
-//      trial-kind values P_c(B,q) of every function (thread per (c, q, B));
+// Persistent CTAs (two per SM, so that one CTA's latency-bound point phase overlaps the other's
+// FP64-bound contraction) walk the element grid; per element a CTA runs Alg. 4 in
+// phases separated by __syncthreads, everything staged in shared memory:
+//   1. stage the element's 1D tables, Gauss weights, node numbers, U_e, CSR row starts and the
+//      column-offset table colOff[A][B] (closed forms of the per-axis Alg. 3 tables);
+//   2. field kinds at every point  Phi[q][m][k] = sum_A U_Am P_k(A,q)  (thread per (q, m));
 //   3. per point: physics state + residual coefficients r~ (thread per q);
 //   4. Jacobian coefficients: warp-uniform trial column (k2, j), lane = q -> dense per-(i,j)
 //      blocks D[q][i,j][test kind][trial kind];
-//   5. test-side sum factorisation, warp = component pair (i, j), lane = trial function B:
-//      H(q) = D_(i,j)(q) P(B,q), then contraction over q2, q1, q0 with the 1D tables
-//      (729 FMA per column for p = 2 instead of 19683 for the rank form); the block goes to a
-//      shared staging array in CSR-segment order [A][i][B][j];
-//   6. F_e: warp = component i, lane = A, same kinds / tables;
-//   7. emission: warp = row (A, i), lanes = consecutive (B, j) -> red.global.add.f64 into the CSR
-//      values (runs of p+1 nodes x m dofs are contiguous in CSR), F likewise.
+//   5. test-side sum factorisation: thread = (trial function B, trial component j), one pass per
+//      test component i: H(q) = D_(i,j)(q) P(B,q), then the contraction over q2, q1, q0 with the
+//      1D tables (729 FMA per column for p = 2 instead of 19683 for the rank form); the column is
+//      added straight into the CSR values with red.global.add.f64 -- consecutive threads hold
+//      consecutive (B, j), i.e. contiguous runs of a CSR row (coalesced);
+//   6. F_e[A, i] (thread per (A, i)).
+// On uniform meshes (all elements share the 1D tables -- translation invariance of uniform
+// B-splines) the test-side tables travel as a __grid_constant__ parameter: immediates in the
+// unrolled contraction.
 #include <cstdio>
 
 #include "iga_host.h"
@@ -23,17 +25,25 @@
 
 namespace iga {
 
+template <int P>
+struct UniTab {
+    double t[3][P + 1][3][P + 1];   // [axis][q][k][a]
+    double qw[3][P + 1];
+    double hp[3];
+};
+
 template <int P, class PH>
 struct F3 {
     static constexpr int M = PH::M;
     static constexpr int NP1 = P + 1, NQ1 = P + 1, NQ = NQ1 * NQ1 * NQ1, NEN = NP1 * NP1 * NP1;
     static constexpr int NCOMBO = M * M;
-    static constexpr int NWARP = NCOMBO % 9 == 0 ? 9 : 8;       // m=3: 9 pairs, m=4: 2 per warp
-    static constexpr int NT = 32 * NWARP;
+    static constexpr int NT = ((NEN * M + 31) / 32) * 32;       // one thread per (B, j): 128 (m=4), 96 (m=3)
+    static constexpr int NWARP = NT / 32;
     using L = Lists<PH, 3, MODE_PARAM>;
     using KS = typename L::KS;
     static constexpr int NKS = KS::NKS, NC = KS::NC, NR = L::NR, NTK = L::NTK, NQK = L::NQK;
-    static constexpr int DB = NTK * NQK;                      // dense block per (i, j)
+    static constexpr int DB = (NTK * NQK + 1) / 2 * 2;        // dense block per (i, j), padded even
+    static constexpr int DQS = NCOMBO * DB + 2;               // q stride (+2: spread smem banks)
     using State = typename PH::template State<3>;
     static constexpr int STD = (sizeof(State) + 7) / 8;      // doubles per state
     // shared-memory carve-up (in doubles)
@@ -43,30 +53,33 @@ struct F3 {
     static constexpr int O_QW = O_TAB + 3 * NQ1 * 3 * NP1;   // [3][NQ1]
     static constexpr int O_QX = O_QW + 3 * NQ1;              // [3][NQ1]
     static constexpr int O_HP = O_QX + 3 * NQ1;              // [4]
-    static constexpr int O_PHI = O_HP + 4;                   // [NQ][M][NKS+1]  (+1: udot)
-    static constexpr int O_ST = O_PHI + NQ * M * (NKS + 1);  // [NQ][STD]
+    static constexpr int O_ST = O_HP + 4;                    // [NQ][STD]
     static constexpr int O_DV = O_ST + NQ * STD;             // [NQ]
-    static constexpr int O_PB = O_DV + NQ;                   // [NQK][NQ][NEN]  trial kind values
-    static constexpr int O_R = O_PB + NQK * NQ * NEN;        // [NR][NQ]
-    static constexpr int O_D = O_R + NR * NQ;                // [NQ][M*M][NTK][NQK]
-    static constexpr int O_KE = O_D + NQ * NCOMBO * DB;      // [NEN][M][NEN][M]
-    static constexpr int O_FE = O_KE + NEN * M * NEN * M;    // [NEN][M]
-    static constexpr int O_RS = O_FE + NEN * M;              // long long [NEN*M] row starts
+    static constexpr int O_R = O_DV + NQ;                    // [NR][NQ]
+    static constexpr int O_D = (O_R + NR * NQ + 1) / 2 * 2;  // [NQ][DQS]  (16-byte aligned)
+    static constexpr int O_PHI = O_D;                        // [NQ][M][NKS+1]  overlays D (dead before D)
+    static constexpr int O_RS = O_D + NQ * DQS;              // long long [NEN*M] row starts
     static constexpr int O_ND = O_RS + NEN * M;              // long long [NEN] nodes
     static constexpr int O_CO = O_ND + NEN;                  // int [NEN][NEN] column offsets (in nodes)
     static constexpr size_t SMEM = (size_t)O_CO * sizeof(double) + (size_t)NEN * NEN * sizeof(int);
+    static_assert(NQ * M * (NKS + 1) <= NQ * DQS, "Phi must fit in the D region");
 };
 
-// test-side sum factorisation in 3D of one column: trial function B, component pair ij.
+// test-side sum factorisation in 3D of one column (trial function B = (b0,b1,b2), pair ij):
 //   Kc[A] = sum_q sum_{tk,qk} P_tk(A,q) D[q][ij][tk][qk] P_qk(B,q)
-template <class F>
+// Trial values P_qk(B,q) are formed on the fly from the lane's 1D values (smem table).
+template <class F, bool UNI, int P>
 __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double *__restrict__ Dsm, int ij,
-                                              const double *__restrict__ Pb, int B, const double *__restrict__ tab) {
+                                              int b0, int b1, int b2, const double *__restrict__ tab,
+                                              const UniTab<P> &ut) {
     using L = typename F::L;
     using KS = typename F::KS;
     constexpr int NP1 = F::NP1, NQ1 = F::NQ1, NEN = F::NEN, NTK = F::NTK, NQK = F::NQK, DB = F::DB;
-    auto T = [&](int d, int q, int k, int a) -> double { return tab[((d * NQ1 + q) * 3 + k) * NP1 + a]; };
-    // which stage tracks exist (test kinds' separable terms)
+    auto T = [&](int d, int q, int k, int a) -> double {
+        if constexpr (UNI) return ut.t[d][q][k][a];
+        else return tab[((d * NQ1 + q) * 3 + k) * NP1 + a];
+    };
+    auto TS = [&](int d, int q, int k, int a) -> double { return tab[((d * NQ1 + q) * 3 + k) * NP1 + a]; };
     constexpr auto used01 = [](int o0, int o1) {
         for (int t = 0; t < NTK; t++) {
             const int c = L::tk(t);
@@ -87,6 +100,9 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
     for (int A = 0; A < NEN; A++) Kc[A] = 0.0;
 #pragma unroll 1
     for (int q0 = 0; q0 < NQ1; q0++) {
+        double n0[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) n0[k] = TS(0, q0, k, b0);
         double Tt[3][NP1][NP1];
 #pragma unroll
         for (int o = 0; o < 3; o++)
@@ -94,8 +110,11 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
             for (int x = 0; x < NP1; x++)
 #pragma unroll
                 for (int y = 0; y < NP1; y++) Tt[o][x][y] = 0.0;
-#pragma unroll 1
+#pragma unroll
         for (int q1 = 0; q1 < NQ1; q1++) {
+            double n1[3];
+#pragma unroll
+            for (int k = 0; k < 3; k++) n1[k] = TS(1, q1, k, b1);
             double S[3][3][NP1];
 #pragma unroll
             for (int o = 0; o < 3; o++)
@@ -106,16 +125,34 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
 #pragma unroll
             for (int q2 = 0; q2 < NQ1; q2++) {
                 const int q = (q0 * NQ1 + q1) * NQ1 + q2;
-                double pb[NQK];
+                double n2[3];
 #pragma unroll
-                for (int k = 0; k < NQK; k++) pb[k] = Pb[(k * F::NQ + q) * NEN + B];
-                const double *Dq = Dsm + (q * F::NCOMBO + ij) * DB;
+                for (int k = 0; k < 3; k++) n2[k] = TS(2, q2, k, b2);
+                double pb[NQK];
+                static_for<NQK>([&](auto K) {
+                    constexpr int kq = decltype(K)::value;
+                    constexpr int c = L::qk(kq);
+                    double v = 0.0;
+                    static_for<KS::nterms(c)>([&](auto TT) {
+                        constexpr int s = decltype(TT)::value;
+                        v += n0[KS::ord(c, s, 0)] * n1[KS::ord(c, s, 1)] * n2[KS::ord(c, s, 2)];
+                    });
+                    pb[kq] = v;
+                });
+                const double2 *Dq2 = reinterpret_cast<const double2 *>(Dsm + q * F::DQS + ij * DB);
+                double dd[DB];
+#pragma unroll
+                for (int x = 0; x < DB / 2; x++) {
+                    const double2 v2 = Dq2[x];
+                    dd[2 * x] = v2.x;
+                    dd[2 * x + 1] = v2.y;
+                }
                 double H[NTK];
 #pragma unroll
                 for (int t = 0; t < NTK; t++) {
                     double h = 0.0;
 #pragma unroll
-                    for (int k = 0; k < NQK; k++) h += Dq[t * NQK + k] * pb[k];
+                    for (int k = 0; k < NQK; k++) h += dd[t * NQK + k] * pb[k];
                     H[t] = h;
                 }
                 static_for<NTK>([&](auto TK) {
@@ -136,9 +173,9 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
                     if constexpr (used01(o0, o1)) {
 #pragma unroll
                         for (int a1 = 0; a1 < NP1; a1++) {
-                            const double n1 = T(1, q1, o1, a1);
+                            const double t1 = T(1, q1, o1, a1);
 #pragma unroll
-                            for (int a2 = 0; a2 < NP1; a2++) Tt[o0][a1][a2] += n1 * S[o0][o1][a2];
+                            for (int a2 = 0; a2 < NP1; a2++) Tt[o0][a1][a2] += t1 * S[o0][o1][a2];
                         }
                     }
                 });
@@ -149,21 +186,22 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
             if constexpr (used0(o0)) {
 #pragma unroll
                 for (int a0 = 0; a0 < NP1; a0++) {
-                    const double n0 = T(0, q0, o0, a0);
+                    const double t0 = T(0, q0, o0, a0);
 #pragma unroll
                     for (int a1 = 0; a1 < NP1; a1++)
 #pragma unroll
-                        for (int a2 = 0; a2 < NP1; a2++) Kc[(a0 * NP1 + a1) * NP1 + a2] += n0 * Tt[o0][a1][a2];
+                        for (int a2 = 0; a2 < NP1; a2++) Kc[(a0 * NP1 + a1) * NP1 + a2] += t0 * Tt[o0][a1][a2];
                 }
             }
         });
     }
 }
 
-template <int P, class PH, bool JAC>
-__global__ void __launch_bounds__(F3<P, PH>::NT, 1)
+template <int P, class PH, bool JAC, bool UNI>
+__global__ void __launch_bounds__(F3<P, PH>::NT, 2)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
-          double *__restrict__ val, double *__restrict__ Fout, long long nelem) {
+          double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
+          int dbg) {
     using F = F3<P, PH>;
     using L = typename F::L;
     using KS = typename F::KS;
@@ -172,16 +210,20 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     constexpr int NKS = F::NKS, NR = F::NR, NTK = F::NTK, NQK = F::NQK, DB = F::DB;
     extern __shared__ __align__(16) double sm[];
     double *sU = sm + F::O_U, *sUd = sm + F::O_UD, *sTab = sm + F::O_TAB, *sQW = sm + F::O_QW, *sQX = sm + F::O_QX;
-    double *sHP = sm + F::O_HP, *sPhi = sm + F::O_PHI, *sDV = sm + F::O_DV, *sPb = sm + F::O_PB, *sR = sm + F::O_R;
-    double *sD = sm + F::O_D, *sKe = sm + F::O_KE, *sFe = sm + F::O_FE;
+    double *sHP = sm + F::O_HP, *sPhi = sm + F::O_PHI, *sDV = sm + F::O_DV, *sR = sm + F::O_R, *sD = sm + F::O_D;
     State *sSt = reinterpret_cast<State *>(sm + F::O_ST);
     long long *sRS = reinterpret_cast<long long *>(sm + F::O_RS);   // [NEN*M] CSR start of row (A, i)
     long long *sNode = reinterpret_cast<long long *>(sm + F::O_ND); // [NEN]
     int *sCO = reinterpret_cast<int *>(sm + F::O_CO);               // [NEN][NEN] column offset (nodes)
+    __shared__ int sG[3 * NP1], sW[3 * NP1], sPosE[3 * NP1 * NP1];
+    __shared__ long long sS[3 * NP1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     int errbits = 0;
     const int n1 = s.ax[1].el_hi - s.ax[1].el_lo, n2 = s.ax[2].el_hi - s.ax[2].el_lo;
-    auto TB = [&](int d, int q, int k, int aa) -> double { return sTab[((d * NQ1 + q) * 3 + k) * NP1 + aa]; };
+    auto TB = [&](int d, int q, int k, int aa) -> double {
+        if constexpr (UNI) return ut.t[d][q][k][aa];
+        else return sTab[((d * NQ1 + q) * 3 + k) * NP1 + aa];
+    };
 
     for (long long el = blockIdx.x; el < nelem; el += gridDim.x) {
         int e[3];
@@ -191,54 +233,70 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             e[1] = s.ax[1].el_lo + (int)(r % n1); r /= n1;
             e[0] = s.ax[0].el_lo + (int)r;
         }
-        // ---- 1. stage ----
-        for (int i = tid; i < 3 * NQ1 * 3 * NP1; i += F::NT) {
-            const int d = i / (NQ1 * 3 * NP1), r = i % (NQ1 * 3 * NP1);
-            sTab[i] = s.ax[d].tab[(size_t)e[d] * NQ1 * 3 * NP1 + r];
-        }
-        for (int i = tid; i < 3 * NQ1; i += F::NT) {
-            const int d = i / NQ1, q = i % NQ1;
-            sQW[i] = s.ax[d].qw[(size_t)e[d] * NQ1 + q];
-            sQX[i] = s.ax[d].qx[(size_t)e[d] * NQ1 + q];
-        }
-        if (tid < 3) sHP[tid] = s.ax[tid].hpar[e[tid]];
-        for (int A = tid; A < NEN; A += F::NT) {
-            int g[3], W[3];
-            long long S[3], T[3];
-            int rr = A;
-            for (int d = 2; d >= 0; d--) {
-                const int aa = rr % NP1;
-                rr /= NP1;
-                g[d] = s.ax[d].first[e[d]] + aa;
-                if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
-                W[d] = s.ax[d].rowW[g[d]];
-                S[d] = s.ax[d].rowS[g[d]];
-                T[d] = s.ax[d].T;
+        // ---- 1. stage: tables, per-axis function data, position tables (one round trip) ----
+        for (int i = tid; i < 3 * NQ1 * 3 * NP1 + 6 * NQ1 + 3 + 3 * NP1 + 3 * NP1 * NP1; i += F::NT) {
+            int k = i;
+            if (k < 3 * NQ1 * 3 * NP1) {
+                const int d = k / (NQ1 * 3 * NP1), r = k % (NQ1 * 3 * NP1);
+                sTab[k] = s.ax[d].tab[(size_t)e[d] * NQ1 * 3 * NP1 + r];
+                continue;
             }
-            const long long node = ((long long)g[0] * s.ax[1].nu + g[1]) * s.ax[2].nu + g[2];
-            sNode[A] = node;
-            const long long base = (long long)M * M * (S[0] * T[1] * T[2] + W[0] * S[1] * T[2] + (long long)W[0] * W[1] * S[2]);
-            const long long Wn = (long long)W[0] * W[1] * W[2];
-            for (int i = 0; i < M; i++) sRS[A * M + i] = base + i * Wn * M;
-            // column offsets (in nodes) of every B in row A: ((pos0 W1 + pos1) W2 + pos2)
-            const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
-            const int *p0 = s.ax[0].pos + (size_t)e[0] * NP1 * NP1 + a0 * NP1;
-            const int *p1 = s.ax[1].pos + (size_t)e[1] * NP1 * NP1 + a1 * NP1;
-            const int *p2 = s.ax[2].pos + (size_t)e[2] * NP1 * NP1 + a2 * NP1;
-            for (int B = 0; B < NEN; B++) {
-                const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
-                sCO[A * NEN + B] = (p0[b0] * W[1] + p1[b1]) * W[2] + p2[b2];
+            k -= 3 * NQ1 * 3 * NP1;
+            if (k < 6 * NQ1) {
+                const int w = k / (3 * NQ1), r = k % (3 * NQ1), d = r / NQ1, q = r % NQ1;
+                if (w == 0) sQW[r] = s.ax[d].qw[(size_t)e[d] * NQ1 + q];
+                else sQX[r] = s.ax[d].qx[(size_t)e[d] * NQ1 + q];
+                continue;
+            }
+            k -= 6 * NQ1;
+            if (k < 3) { sHP[k] = s.ax[k].hpar[e[k]]; continue; }
+            k -= 3;
+            if (k < 3 * NP1) {
+                const int d = k / NP1, aa = k % NP1;
+                int g = s.ax[d].first[e[d]] + aa;
+                if (g >= s.ax[d].nu) g -= s.ax[d].nu;
+                sG[k] = g;
+                sW[k] = s.ax[d].rowW[g];
+                sS[k] = s.ax[d].rowS[g];
+                continue;
+            }
+            k -= 3 * NP1;
+            {
+                const int d = k / (NP1 * NP1);
+                sPosE[k] = s.ax[d].pos[(size_t)e[d] * NP1 * NP1 + k % (NP1 * NP1)];
             }
         }
         __syncthreads();
-        for (int i = tid; i < NEN * M; i += F::NT) {
-            const long long node = sNode[i / M];
-            sU[i] = U[node * M + i % M];
-            sUd[i] = Ud ? Ud[node * M + i % M] : 0.0;
+        {
+            const long long T1 = s.ax[1].T, T2 = s.ax[2].T;
+            const long long nu1 = s.ax[1].nu, nu2 = s.ax[2].nu;
+            for (int i = tid; i < NEN * NEN + NEN * M; i += F::NT) {
+                if (i < NEN * NEN) {
+                    const int A = i / NEN, B = i - A * NEN;
+                    const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
+                    const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
+                    sCO[i] = (sPosE[a0 * NP1 + b0] * sW[NP1 + a1] + sPosE[NP1 * NP1 + a1 * NP1 + b1]) * sW[2 * NP1 + a2]
+                             + sPosE[2 * NP1 * NP1 + a2 * NP1 + b2];
+                } else {
+                    const int k = i - NEN * NEN, A = k / M, m = k - A * M;
+                    const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
+                    const long long node = ((long long)sG[a0] * nu1 + sG[NP1 + a1]) * nu2 + sG[2 * NP1 + a2];
+                    sU[k] = U[node * M + m];
+                    sUd[k] = Ud ? Ud[node * M + m] : 0.0;
+                    if (m == 0) {
+                        sNode[A] = node;
+                        const long long W0 = sW[a0], W1 = sW[NP1 + a1], W2 = sW[2 * NP1 + a2];
+                        const long long base = (long long)M * M * (sS[a0] * T1 * T2 + W0 * sS[NP1 + a1] * T2 + W0 * W1 * sS[2 * NP1 + a2]);
+                        const long long Wn = W0 * W1 * W2;
+#pragma unroll
+                        for (int ii = 0; ii < M; ii++) sRS[A * M + ii] = base + ii * Wn * M;
+                    }
+                }
+            }
         }
         __syncthreads();
 
-        // ---- 2. field kinds per (q, m) and trial-kind values per (k, q, B) ----
+        // ---- 2. field kinds per (q, m) ----
         for (int task = tid; task < NQ * M; task += F::NT) {
             const int q = task / M, m = task % M;
             const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
@@ -251,9 +309,9 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 double v[3][3];
 #pragma unroll
                 for (int k = 0; k < 3; k++) {
-                    v[0][k] = TB(0, q0, k, a0);
-                    v[1][k] = TB(1, q1, k, a1);
-                    v[2][k] = TB(2, q2, k, a2);
+                    v[0][k] = sTab[((0 * NQ1 + q0) * 3 + k) * NP1 + a0];
+                    v[1][k] = sTab[((1 * NQ1 + q1) * 3 + k) * NP1 + a1];
+                    v[2][k] = sTab[((2 * NQ1 + q2) * 3 + k) * NP1 + a2];
                 }
                 const double uA = sU[A * M + m];
                 static_for<NKS>([&](auto K) {
@@ -270,25 +328,6 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 #pragma unroll
             for (int k = 0; k <= NKS; k++) sPhi[(q * M + m) * (NKS + 1) + k] = acc[k];
         }
-        if (JAC)
-            for (int task = tid; task < NQK * NQ * NEN; task += F::NT) {
-                const int kk = task / (NQ * NEN), q = (task / NEN) % NQ, B = task % NEN;
-                const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
-                const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
-                double pv = 0.0;
-                static_for<NQK>([&](auto K) {
-                    constexpr int kq = decltype(K)::value;
-                    constexpr int cc = L::qk(kq);
-                    if (kk == kq) {
-                        static_for<KS::nterms(cc)>([&](auto TT) {
-                            constexpr int t = decltype(TT)::value;
-                            pv += TB(0, q0, KS::ord(cc, t, 0), b0) * TB(1, q1, KS::ord(cc, t, 1), b1)
-                                  * TB(2, q2, KS::ord(cc, t, 2), b2);
-                        });
-                    }
-                });
-                sPb[task] = pv;
-            }
         __syncthreads();
 
         // ---- 3. per-point state + residual coefficients ----
@@ -350,7 +389,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                             PH::template dcol<3>(st, k2, j, a, b, col);
 #pragma unroll
                             for (int i = 0; i < M; i++) {
-                                double *dst = sD + (q * F::NCOMBO + i * M + j) * DB + kq;
+                                double *dst = sD + q * F::DQS + (i * M + j) * DB + kq;
                                 static_for<NTK>([&](auto TK) {
                                     constexpr int t = decltype(TK)::value;
                                     const double v = col[L::tk(t) * M + i] * dV;
@@ -365,35 +404,42 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             }
             __syncthreads();
 
-            // ---- 5. test-side sum factorisation, warp = (i, j) pairs, lane = B ----
-            for (int combo = warp; combo < F::NCOMBO; combo += F::NWARP) {
-                if (lane < NEN) {
+            // ---- 5. test-side sum factorisation + coalesced emission, thread = (B, j) ----
+            if (tid < NEN * M) {
+                const int B = tid / M, J = tid - B * M;
+                const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
+#pragma unroll 1
+                for (int I = 0; I < M; I++) {
                     double Kc[NEN];
-                    tsf_column_3d<F>(Kc, sD, combo, sPb, lane, sTab);
-                    const int I = combo / M, J = combo % M, B = lane;
+                    if (!(dbg & 1)) tsf_column_3d<F, UNI, P>(Kc, sD, I * M + J, b0, b1, b2, sTab, ut);
+                    else {
 #pragma unroll
-                    for (int A = 0; A < NEN; A++) sKe[((A * M + I) * NEN + B) * M + J] = Kc[A];
+                        for (int A = 0; A < NEN; A++) Kc[A] = sD[A * 7 + J];
+                    }
+                    if (!(dbg & 2)) {
+#pragma unroll
+                        for (int A = 0; A < NEN; A++)
+                            atomicAdd(val + sRS[A * M + I] + (long long)sCO[A * NEN + B] * M + J, Kc[A]);
+                    } else {
+                        double sum = 0.0;
+#pragma unroll
+                        for (int A = 0; A < NEN; A++) sum += Kc[A];
+                        if (sum == 1.2345e300) val[0] = sum;
+                    }
                 }
             }
         }
-        // ---- 6. residual F_e[A, i]: warp = i, lane = A ----
-        if (Fout && warp < M && lane < NEN) {
-            const int A = lane;
+        // ---- 6. residual F_e[A, i], thread = (A, i) (q fully unrolled) ----
+        if (Fout && tid < NEN * M) {
+            const int A = tid / M, Ii = tid - A * M;
             const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
             static_for<M>([&](auto II) {
                 constexpr int I = decltype(II)::value;
-                if (warp == I) {
+                if (Ii == I) {
                     double acc = 0.0;
-#pragma unroll 1
-                    for (int q = 0; q < NQ; q++) {
-                        const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
-                        double v[3][3];
-#pragma unroll
-                        for (int k = 0; k < 3; k++) {
-                            v[0][k] = TB(0, q0, k, a0);
-                            v[1][k] = TB(1, q1, k, a1);
-                            v[2][k] = TB(2, q2, k, a2);
-                        }
+                    static_for<NQ>([&](auto QQ) {
+                        constexpr int q = decltype(QQ)::value;
+                        constexpr int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
                         static_for<NR>([&](auto RR) {
                             constexpr int rr = decltype(RR)::value;
                             constexpr int c = L::R.c[rr];
@@ -401,56 +447,47 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                                 double pv = 0.0;
                                 static_for<KS::nterms(c)>([&](auto TT) {
                                     constexpr int t = decltype(TT)::value;
-                                    pv += v[0][KS::ord(c, t, 0)] * v[1][KS::ord(c, t, 1)] * v[2][KS::ord(c, t, 2)];
+                                    pv += TB(0, q0, KS::ord(c, t, 0), a0) * TB(1, q1, KS::ord(c, t, 1), a1)
+                                          * TB(2, q2, KS::ord(c, t, 2), a2);
                                 });
                                 acc += pv * sR[rr * NQ + q];
                             }
                         });
-                    }
-                    sFe[A * M + I] = acc;
+                    });
+                    atomicAdd(Fout + sNode[A] * M + I, acc);
                 }
             });
         }
-        __syncthreads();
-
-        // ---- 7. emission: warp = row (A, i), lanes = consecutive (B, j) ----
-        if constexpr (JAC) {
-            for (int row = warp; row < NEN * M; row += F::NWARP) {
-                const int A = row / M;
-                const long long rs = sRS[row];
-                const double *src = sKe + (size_t)row * NEN * M;
-                const int *co = sCO + A * NEN;
-                for (int t = lane; t < NEN * M; t += 32) {
-                    const int B = t / M, j = t - B * M;
-                    atomicAdd(val + rs + (long long)co[B] * M + j, src[t]);
-                }
-            }
-        }
-        if (Fout)
-            for (int task = tid; task < NEN * M; task += F::NT) atomicAdd(Fout + sNode[task / M] * M + task % M, sFe[task]);
         __syncthreads();
     }
     if (errbits) atomicOr(s.errflag, errbits);
 }
 
-template <int P, class PH>
+template <int P, class PH, bool UNI>
 static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
                               const double *Ud, double *val, double *F, cudaStream_t st, int nsm) {
     using FF = F3<P, PH>;
     Prm prm;
     for (int i = 0; i < 8; i++) prm.p[i] = phys->p[i];
+    UniTab<P> ut{};
+    if (UNI)
+        for (int d = 0; d < 3; d++) {
+            for (int i = 0; i < (P + 1) * 3 * (P + 1); i++) (&ut.t[d][0][0][0])[i] = s->tab0[d][i];
+            for (int q = 0; q <= P; q++) ut.qw[d][q] = s->qw0[d][q];
+            ut.hp[d] = s->hp0[d];
+        }
     const bool jac = val != nullptr;
     const size_t smem = FF::SMEM;
     static bool attr[2] = {false, false};
     if (!attr[jac]) {
-        cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused3d<P, PH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                             : cudaFuncSetAttribute(k_fused3d<P, PH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused3d<P, PH, true, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                             : cudaFuncSetAttribute(k_fused3d<P, PH, false, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ce != cudaSuccess) { set_error(std::string("fused3d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
         attr[jac] = true;
     }
     int occ = 1;
-    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, true>, FF::NT, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, false>, FF::NT, smem);
+    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, true, UNI>, FF::NT, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, false, UNI>, FF::NT, smem);
     occ = std::max(occ, 1);
     const long long nel = s->nel_local;
     const int grid = (int)std::min<long long>(nel, (long long)nsm * occ);
@@ -459,11 +496,12 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
     if (F) { ProfScope ps(s, "k_zero", st); k_zero_vec(F, s->nrows_owned, st, nsm); launches++; }
     {
         ProfScope ps(s, "k_fused3d", st);
-        if (jac) k_fused3d<P, PH, true><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel);
-        else k_fused3d<P, PH, false><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel);
+        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg);
+        else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg);
         launches++;
     }
     s->last_launches = launches;
+    s->last_occupancy = occ;
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) { set_error(std::string("fused3d launch: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
     return IGA_OK;
@@ -473,8 +511,13 @@ iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm) {
     if (s->dim != 3 || s->mode != MODE_PARAM || s->nranks != 1) return IGA_ERR_STATE;
     if (s->p[0] != 2 || s->p[1] != 2 || s->p[2] != 2) return IGA_ERR_STATE;
-    if (ph->kind == IGA_PHYS_NS_VMS && s->dof == 4) return run_fused3d<2, PhysNSVMS>(s, ph, a, b, U, Ud, val, F, st, nsm);
-    if (ph->kind == IGA_PHYS_NEOHOOKE && s->dof == 3) return run_fused3d<2, PhysNeoHooke>(s, ph, a, b, U, Ud, val, F, st, nsm);
+    const bool uni = s->tab_uniform[0] && s->tab_uniform[1] && s->tab_uniform[2] && !s->force_general;
+    if (ph->kind == IGA_PHYS_NS_VMS && s->dof == 4)
+        return uni ? run_fused3d<2, PhysNSVMS, true>(s, ph, a, b, U, Ud, val, F, st, nsm)
+                   : run_fused3d<2, PhysNSVMS, false>(s, ph, a, b, U, Ud, val, F, st, nsm);
+    if (ph->kind == IGA_PHYS_NEOHOOKE && s->dof == 3)
+        return uni ? run_fused3d<2, PhysNeoHooke, true>(s, ph, a, b, U, Ud, val, F, st, nsm)
+                   : run_fused3d<2, PhysNeoHooke, false>(s, ph, a, b, U, Ud, val, F, st, nsm);
     return IGA_ERR_STATE;
 }
 

@@ -26,7 +26,15 @@ struct iga_space_s {
     size_t work_bytes = 0;
     int *errflag = nullptr;
     int last_launches = 0;
-    int force_split = 0;                 // 1: use the generic split kernels (tests / A-B checks)
+    int force_split = 0;
+    int force_general = 0;
+    int last_occupancy = 0;
+    int dbg = 0;                         // experiment bits (bench A/B only; results invalid when set)               // 1: never use the uniform-table fast paths
+    // per axis: all elements share the same 1D tables / weights / span length (uniform knots,
+    // translation invariance; equal to 1e-13 relative) -> element-0 copies (host)
+    int tab_uniform[3] = {0, 0, 0};
+    std::vector<double> tab0[3], qw0[3];
+    double hp0[3] = {1.0, 1.0, 1.0};                 // 1: use the generic split kernels (tests / A-B checks)
     // kernel timing hook (iga_profile_*)
     struct ProfRec { const char *name; cudaEvent_t a, b; };
     bool prof_on = false;

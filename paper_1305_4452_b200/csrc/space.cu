@@ -500,6 +500,26 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             if (ce != cudaSuccess) { st = IGA_ERR_CUDA; set_error(cudaGetErrorString(ce)); goto fail; }
         }
         ax.tab = dtab;
+        {
+            // uniform-table detection (element-0 tables reused by the fused kernels' fast path)
+            std::vector<double> ht((size_t)nel * nq * 3 * (p + 1));
+            CUDA_TRY(cudaMemcpy(ht.data(), dtab, ht.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            const size_t per = (size_t)nq * 3 * (p + 1);
+            double mx = 0.0;
+            for (size_t k = 0; k < per; k++) mx = std::max(mx, std::fabs(ht[k]));
+            bool uni = true;
+            for (int e = 1; e < nel && uni; e++) {
+                for (size_t k = 0; k < per; k++)
+                    if (std::fabs(ht[e * per + k] - ht[k]) > 1e-13 * mx) { uni = false; break; }
+                for (int q = 0; q < nq && uni; q++)
+                    if (std::fabs(qw[(size_t)e * nq + q] - qw[q]) > 1e-14 * std::fabs(qw[q])) uni = false;
+                if (std::fabs(hpar[e] - hpar[0]) > 1e-14 * hpar[0]) uni = false;
+            }
+            s->tab_uniform[a] = uni ? 1 : 0;
+            s->tab0[a].assign(ht.begin(), ht.begin() + per);
+            s->qw0[a].assign(qw.begin(), qw.begin() + nq);
+            s->hp0[a] = hpar[0];
+        }
         nnodes *= nu;
         nrows_nodes *= (own_hi - own_lo);
     }
@@ -688,6 +708,8 @@ int iga_last_launch_count(iga_space s) { return s ? s->last_launches : 0; }
 iga_status iga_space_set_option(iga_space s, const char *key, long long value) {
     if (!s || !key) { set_error("null argument"); return IGA_ERR_PARAM; }
     if (std::strcmp(key, "split") == 0) { s->force_split = value != 0; return IGA_OK; }
+    if (std::strcmp(key, "general") == 0) { s->force_general = value != 0; return IGA_OK; }
+    if (std::strcmp(key, "dbg") == 0) { s->dbg = (int)value; return IGA_OK; }
     set_error(std::string("unknown option ") + key);
     return IGA_ERR_PARAM;
 }
