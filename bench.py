@@ -51,57 +51,87 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and throttle reasons sampled with NVML (every ~1 ms) during the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    The GPU is found by PCI bus id (CUDA and NVML orderings can differ).  At least one sample is
+    always taken (at exit) so that short regions still report a clock."""
 
-    def __init__(self, gpu_index: int):
-        self.gpu = gpu_index
-        self.proc = None
-        self.lines = []
+    BAD = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+           "sw_power_cap": 0x4, "hw_power_brake": 0x80}
+
+    def __init__(self, cuda_index: int):
+        self.idx = cuda_index
+        self.samples, self.reasons, self.mx = [], set(), None
+        self._stop = threading.Event()
+        self.h = None
+
+    def _sample(self, nv):
+        self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for nm, bit in self.BAD.items():
+            if r & bit:
+                self.reasons.add(nm)
+
+    def _loop(self, nv):
+        while not self._stop.is_set():
+            try:
+                self._sample(nv)
+            except Exception:
+                return
+            time.sleep(0.001)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            self.nv = nv
+            try:
+                p = torch.cuda.get_device_properties(self.idx)
+                bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._loop, args=(nv,), daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        if self.h is not None:
+            self._stop.set()
+            self.t.join(timeout=2)
             try:
-                self.proc.wait(timeout=5)
+                self._sample(self.nv)
             except Exception:
-                self.proc.kill()
+                pass
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
+
+
+def box_procs(n: int, dim: int):
+    """ranks per axis for n GPUs: split the largest factor 2 first over the leading axes"""
+    procs = [1] * dim
+    k, a = n, 0
+    while k > 1:
+        f = 2 if k % 2 == 0 else k
+        procs[a % dim] *= f
+        k //= f
+        a += 1
+    return procs
+
+
+def owned_rows(w, sp):
+    """global dof indices of the space's owned node box (node-major, dof innermost)"""
+    idx = np.zeros(1, dtype=np.int64)
+    for a in range(w.dim):
+        g = np.arange(sp.owned_lo[a], sp.owned_hi[a], dtype=np.int64)
+        idx = (idx[:, None] * w.nfun[a] + g[None, :]).reshape(-1)
+    return (idx[:, None] * w.dof + np.arange(w.dof)[None, :]).reshape(-1)
 
 
 def dist_env():
@@ -184,16 +214,26 @@ def run_iga(args, w, ws, rank, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    procs = None
     if ws > 1:
+        # box decomposition of the element grid; libiga's own NCCL communicator
+        # carries the ghost-U and halo-row exchanges, torch.distributed only ships its unique id
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    sp = iga.Space.from_workload(w, device=local)
+        procs = box_procs(ws, w.dim)
+        obj = [iga.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        sp = iga.Space.from_workload(w, device=local, dist={"rank": rank, "nranks": ws, "procs": procs,
+                                                            "transport": iga.XPORT_NCCL, "nccl_id": obj[0]})
+    else:
+        sp = iga.Space.from_workload(w, device=local)
     for kv in args.opt:
         k, v = kv.split("=")
         sp.set_option(k, int(v))
     stream = torch.cuda.current_stream()
-    U = torch.from_numpy(w.U).to(dev)
-    Ud = torch.from_numpy(w.Udot).to(dev)
+    own = owned_rows(w, sp)
+    U = torch.from_numpy(w.U[own]).to(dev)
+    Ud = torch.from_numpy(w.Udot[own]).to(dev)
     rp, ci = sp.csr_pattern()
     vals = torch.empty(sp.nnz, dtype=torch.float64, device=dev)
     F = torch.empty(sp.nrows, dtype=torch.float64, device=dev)
@@ -235,33 +275,57 @@ def run_iga(args, w, ws, rank, local):
         ms, _ = timed_region(args.steps)
     sp.check()
     step_ms = sum(ms) / len(ms)
+    nqp_total = sp.nqp
     if ws > 1:
         t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         step_ms = float(t.item())
-    nqp_total = sp.nqp * ws
+        q = torch.tensor([float(sp.nqp)], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(q)
+        nqp_total = int(q.item())
     value = nqp_total / (step_ms * 1e-3)
 
     # per-kernel device times (second pass with the kernel timing hook on)
     _, prof = timed_region(args.steps, profile=True)
 
-    # end-to-end through the host-buffer C-ABI call (pinned buffers, copies inside the timed region)
-    Uh = torch.from_numpy(w.U).pin_memory()
-    Udh = torch.from_numpy(w.Udot).pin_memory()
+    # end to end from pinned host buffers: single rank through the host-buffer C-ABI call
+    # (iga_form_jacobian_host); multi-rank through the device call with the owned-vector H2D and
+    # the owned values / residual D2H copies inside the timed region (max over ranks)
+    Uh = torch.from_numpy(w.U[own]).pin_memory()
+    Udh = torch.from_numpy(w.Udot[own]).pin_memory()
     vh = torch.empty(sp.nnz, dtype=torch.float64).pin_memory()
     fh = torch.empty(sp.nrows, dtype=torch.float64).pin_memory()
     e2e_steps = max(3, min(args.steps, 10))
-    sp.form_jacobian_host(ph, w.a, w.b, Uh, Udh, vh, fh)
+
+    def e2e_step():
+        if ws == 1:
+            sp.form_jacobian_host(ph, w.a, w.b, Uh, Udh, vh, fh)
+        else:
+            U.copy_(Uh, non_blocking=True)
+            Ud.copy_(Udh, non_blocking=True)
+            step()
+            vh.copy_(vals, non_blocking=True)
+            fh.copy_(F, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
     e2e_ms = []
     for _ in range(e2e_steps):
         flush.zero_()
+        if ws > 1:
+            torch.distributed.barrier()
         a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a_ev.record(stream)
-        sp.form_jacobian_host(ph, w.a, w.b, Uh, Udh, vh, fh)
+        e2e_step()
         b_ev.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(a_ev.elapsed_time(b_ev))
-    e2e_val = nqp_total / (statistics.mean(e2e_ms) * 1e-3)
+    e2e_t = statistics.mean(e2e_ms)
+    if ws > 1:
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_val = nqp_total / (e2e_t * 1e-3)
 
     if rank != 0:
         if ws > 1:
@@ -273,14 +337,19 @@ def run_iga(args, w, ws, rank, local):
     dom = max(kern, key=lambda k: kern[k][1])
     n_l, tot_ms = kern[dom]
     avg_ms = tot_ms / n_l
-    nqp_launch = sp.nqp / max(1, kern["k_contract"][0] // args.steps) if "k_contract" in kern else sp.nqp
     cid = w.cid
-    if dom == "k_contract":
+    # the assembly kernels (fused 2D / 3D, or the split contraction) carry the whole element
+    # contraction: FP64-ALU bound; their algorithmic flops per launch are
+    # (F_J + F_R) x the quadrature points that launch integrates
+    ASSEMBLY = ("k_fused2d", "k_fused3d", "k_contract")
+    if dom in ASSEMBLY:
+        launches_per_step = max(1.0, kern[dom][0] / args.steps)
+        nqp_launch = sp.nqp / launches_per_step
         alg = (F_J[cid] + F_R[cid]) * nqp_launch
         bound, unit, peak = "alu", "TFLOP/s", P64_NOMINAL_TFLOPS
         achieved = alg / (avg_ms * 1e-3) / 1e12
     elif dom == "k_point":
-        # pointwise stage: no algorithmic flops in the model; its HBM stream is the coefficient workspace
+        # pointwise stage of the split path: no algorithmic flops in the model
         alg = None
         bound, unit, peak = "alu", "TFLOP/s", P64_NOMINAL_TFLOPS
         achieved = 0.0
@@ -318,11 +387,13 @@ def run_iga(args, w, ws, rank, local):
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak" if ws > 1 else "weak",
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "nqp": sp.nqp, "nelem": w.nelem, "ndof": sp.ndof, "nnz": sp.nnz,
                    "degree": w.degree[0], "dof_per_node": w.dof, "l2": "flushed (512 MiB write) between steps",
-                   "step": "iga_form_jacobian(a,b) with residual F fused"},
+                   "step": "iga_form_jacobian(a,b) with residual F fused",
+                   "parallelism": f"box {'x'.join(map(str, procs))} over {ws} GPUs (NCCL ghost/halo exchange)"
+                   if ws > 1 else "1 GPU"},
         "roofline": {"bound": bound, "kernel": dom, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak if peak else None, "traffic": traffic,
                      "peak_source": "148 SM x 64 DFMA/clk x 2 x 1.965 GHz (B200 unit counts, DESIGN.md)"
@@ -331,8 +402,8 @@ def run_iga(args, w, ws, rank, local):
                      "kernel_launches_per_step": {k: v[0] / args.steps for k, v in kern.items()},
                      "step_roofline_ms": t_roof * 1e3, "step_frac": t_roof * 1e3 / step_ms},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(2 * 8 * sp.ndof),
-                "d2h_bytes_per_step": int(8 * (sp.nnz + sp.nrows)), "ms_per_step": statistics.mean(e2e_ms)},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(2 * 8 * sp.nrows * ws),
+                "d2h_bytes_per_step": int(8 * (sp.nnz + sp.nrows) * ws), "ms_per_step": e2e_t},
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clocks,
     }
@@ -358,8 +429,6 @@ def main():
     w = workloads.make(args.config, n=args.n)
     if args.impl == "reference":
         return run_reference(args, w, ws, rank)
-    if ws > 1:
-        raise SystemExit("multi-GPU box decomposition is not wired into bench.py yet")
     return run_iga(args, w, ws, rank, local)
 
 

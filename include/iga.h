@@ -69,13 +69,51 @@ typedef struct {
     const double *weights;         /* host [n0][n1][n2] projective weights > 0, NULL => 1      */
 } iga_space_desc;
 
-/* Box decomposition of the element grid over ranks.
- * NULL => one rank owns everything. procs[d] ranks along axis d, rank = (r0*p1+r1)*p2+r2. */
+/* Box decomposition of the element grid over ranks ("partitioning of the
+ * [parametric] domain").  NULL => one rank owns everything.
+ * procs[d] ranks along axis d, rank = (r0*p1+r1)*p2+r2; elements of axis d split as
+ * b_r = floor(N r / P); a function belongs to the rank owning the last element of
+ * its support (SURVEY A-9), so every rank's touched-but-not-owned ("halo") functions sit just
+ * above its owned range and belong to its upper neighbours.  Each rank needs >= p elements per
+ * partitioned axis (IGA_ERR_PARAM otherwise).
+ * transport: IGA_XPORT_NCCL -- one process per GPU; nccl_id is an ncclUniqueId (from
+ *            iga_nccl_unique_id on one rank, broadcast by the caller) identical on all ranks;
+ *            iga_form_* then run the ghost / halo exchanges with NCCL send/recv on the stream.
+ *            IGA_XPORT_LOCAL -- all ranks' spaces live in this process (one GPU; tests): the
+ *            forms go through iga_form_*_group, exchanges are device copies. */
+enum { IGA_XPORT_NCCL = 0, IGA_XPORT_LOCAL = 1 };
 typedef struct {
     int rank;
     int nranks;
     int procs[3];
+    int transport;
+    unsigned char nccl_id[128];
 } iga_dist;
+
+/* One message of the halo-row exchange (the ghost-U exchange is the same list reversed):
+ * subbox = bits (axis 0 = 4, axis 1 = 2, axis 2 = 1) of the axes on which the box is the halo
+ * layer; box_lo/box_n = the box in the touched-box (send) or owned-box (receive) local indices
+ * of the reporting rank; rows = nodes * dof; values = CSR values of those full rows. */
+typedef struct {
+    int peer;
+    int subbox;
+    int64_t rows;
+    int64_t values;
+    int box_lo[3];
+    int box_n[3];
+} iga_msg;
+
+/* Host only -- needs no GPU and allocates nothing on a device: the decomposition seen by rank
+ * dist->rank (owned function box [own_lo, own_hi), element box [el_lo, el_hi), touched box
+ * extent ext_n = owned + halo per axis) and its messages: `send` = its halo rows to their
+ * owners, `recv` = partial rows from its lower neighbours.  Up to max_msgs of each are
+ * written; *nsend / *nrecv give the full counts (at most 7 each). */
+iga_status iga_dist_plan(const iga_space_desc *desc, const iga_dist *dist, int64_t own_lo[3],
+                         int64_t own_hi[3], int64_t el_lo[3], int64_t el_hi[3], int64_t ext_n[3],
+                         int max_msgs, iga_msg *send, int *nsend, iga_msg *recv, int *nrecv);
+
+/* A fresh ncclUniqueId (128 bytes) for IGA_XPORT_NCCL (dlopen's libnccl.so.2). */
+iga_status iga_nccl_unique_id(unsigned char out[128]);
 
 /* Create a space on CUDA device `device`.  Copies all host inputs.  Builds the per-axis
  * quadrature rule (Gauss-Legendre, A-6), the 1D basis tables at the Gauss points (kernel K1)
@@ -110,8 +148,10 @@ typedef struct {
     double p[8];
 } iga_phys;
 
-/* Residual R(U, Udot) (Alg. 4).  U, Udot: device fp64 [ndof_global] (single rank) -- Udot may
- * be NULL (=> 0).  F: device fp64 [nrows_owned], overwritten. */
+/* Residual R(U, Udot) (Alg. 4).  U, Udot: device fp64 [nrows_owned] (the owned box, node-major,
+ * dof innermost; = all dofs on a single rank) -- Udot may be NULL (=> 0).  F: device fp64
+ * [nrows_owned], overwritten.  Multi-rank (IGA_XPORT_NCCL): collective over all ranks (every
+ * rank calls with its owned vectors); the ghost-U and halo exchanges run on `stream`. */
 iga_status iga_form_residual(iga_space s, const iga_phys *phys, const double *U,
                              const double *Udot, double *F, void *stream);
 
@@ -127,6 +167,17 @@ iga_status iga_form_jacobian(iga_space s, const iga_phys *phys, double a, double
 iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, double b,
                                   const double *U_host, const double *Udot_host,
                                   double *csr_val_host, double *F_host, void *stream);
+
+/* In-process multi-rank forms (IGA_XPORT_LOCAL): spaces[k] must be rank k of the same
+ * decomposition, all on one device; U[k], Udot[k] (NULL entries allowed for Udot when all are
+ * NULL), csr_val[k], F[k] are that rank's owned vectors / values (device).  Ranks' kernels run
+ * one after another on `stream`, the exchanges are device copies between their buffers. */
+iga_status iga_form_jacobian_group(int n, const iga_space *spaces, const iga_phys *phys, double a,
+                                   double b, const double *const *U, const double *const *Udot,
+                                   double *const *csr_val, double *const *F, void *stream);
+iga_status iga_form_residual_group(int n, const iga_space *spaces, const iga_phys *phys,
+                                   const double *const *U, const double *const *Udot,
+                                   double *const *F, void *stream);
 
 /* Synchronises `stream` and reports (then clears) the device error flag of the last form
  * call: IGA_OK, IGA_ERR_SINGULAR_MAP or IGA_ERR_NONFINITE. */

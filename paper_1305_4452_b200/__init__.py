@@ -39,7 +39,16 @@ class _Desc(C.Structure):
 
 
 class _Dist(C.Structure):
-    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("procs", C.c_int * 3)]
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("procs", C.c_int * 3), ("transport", C.c_int),
+                ("nccl_id", C.c_ubyte * 128)]
+
+
+class _Msg(C.Structure):
+    _fields_ = [("peer", C.c_int), ("subbox", C.c_int), ("rows", C.c_int64), ("values", C.c_int64),
+                ("box_lo", C.c_int * 3), ("box_n", C.c_int * 3)]
+
+
+XPORT_NCCL, XPORT_LOCAL = 0, 1
 
 
 class _Phys(C.Structure):
@@ -51,7 +60,8 @@ _lib = None
 EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
            "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
-           "iga_microbench", "iga_space_set_option"]
+           "iga_microbench", "iga_space_set_option", "iga_form_jacobian_group", "iga_form_residual_group",
+           "iga_dist_plan", "iga_nccl_unique_id"]
 
 
 def lib():
@@ -83,11 +93,19 @@ def lib():
         L.iga_space_set_option.restype = C.c_int
         L.iga_microbench.argtypes = [C.c_int, C.c_int, C.c_longlong]
         L.iga_microbench.restype = C.c_double
+        L.iga_form_jacobian_group.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(_Phys), C.c_double, C.c_double,
+                                              C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]
+        L.iga_form_residual_group.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(_Phys), C.POINTER(vp), C.POINTER(vp),
+                                              C.POINTER(vp), vp]
+        L.iga_dist_plan.argtypes = [C.POINTER(_Desc), C.POINTER(_Dist), lp, lp, lp, lp, lp, C.c_int,
+                                    C.POINTER(_Msg), C.POINTER(C.c_int), C.POINTER(_Msg), C.POINTER(C.c_int)]
+        L.iga_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte * 128)]
         L.iga_last_error.restype = C.c_char_p
         L.iga_version.restype = C.c_char_p
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
                   "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
-                  "iga_profile_reset"):
+                  "iga_profile_reset", "iga_form_jacobian_group", "iga_form_residual_group", "iga_dist_plan",
+                  "iga_nccl_unique_id"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -136,6 +154,103 @@ def microbench(device: int = 0, which=None, param: int = 0) -> dict:
     return out
 
 
+def _make_desc(dim, degree, knots, periodic, continuity, dof, quad, geometry, ctrl=None, weights=None):
+    """iga_space_desc from host arrays; returns (desc, keep-alive list)."""
+    d = _Desc()
+    d.dim = dim
+    keep = []
+    for a in range(3):
+        if a < dim:
+            k = np.ascontiguousarray(knots[a], dtype=np.float64)
+            keep.append(k)
+            d.degree[a] = int(degree[a])
+            d.n_knots[a] = len(k)
+            d.knots[a] = k.ctypes.data_as(C.POINTER(C.c_double))
+            d.periodic[a] = int(periodic[a])
+            d.periodic_continuity[a] = int(continuity[a])
+            d.quad[a] = int(quad[a]) if quad is not None else 0
+    d.dof = dof
+    d.geometry = geometry
+    if ctrl is not None:
+        c = np.ascontiguousarray(ctrl, dtype=np.float64).reshape(-1)
+        keep.append(c)
+        d.ctrl = c.ctypes.data_as(C.POINTER(C.c_double))
+    if weights is not None:
+        w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+        keep.append(w)
+        d.weights = w.ctypes.data_as(C.POINTER(C.c_double))
+    return d, keep
+
+
+def _make_dist(dist) -> _Dist:
+    """dist = {"rank", "nranks", "procs", ["transport"], ["nccl_id": 128 bytes]}"""
+    dd = _Dist()
+    dd.rank, dd.nranks = int(dist["rank"]), int(dist["nranks"])
+    for a in range(3):
+        dd.procs[a] = int(dist["procs"][a]) if a < len(dist["procs"]) else 1
+    dd.transport = int(dist.get("transport", XPORT_NCCL))
+    uid = dist.get("nccl_id")
+    if uid is not None:
+        for i, b in enumerate(bytes(uid)[:128]):
+            dd.nccl_id[i] = b
+    return dd
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId for an IGA_XPORT_NCCL decomposition (broadcast it to every rank)."""
+    buf = (C.c_ubyte * 128)()
+    _check(lib().iga_nccl_unique_id(C.byref(buf)))
+    return bytes(buf)
+
+
+def dist_plan(w, dist) -> dict:
+    """Host-only box decomposition + exchange plan of rank dist["rank"] for workload `w` (no GPU)."""
+    d, keep = _make_desc(w.dim, w.degree, w.knots, w.periodic, w.continuity, w.dof, w.quad, w.geometry, w.ctrl,
+                         w.weights)
+    dd = _make_dist(dist)
+    arrs = [(C.c_int64 * 3)() for _ in range(5)]
+    snd, rcv = (_Msg * 8)(), (_Msg * 8)()
+    ns, nr = C.c_int(), C.c_int()
+    _check(lib().iga_dist_plan(C.byref(d), C.byref(dd), *arrs, 8, snd, C.byref(ns), rcv, C.byref(nr)))
+
+    def msgs(a, n):
+        return [{"peer": a[k].peer, "subbox": a[k].subbox, "rows": a[k].rows, "values": a[k].values,
+                 "box_lo": list(a[k].box_lo), "box_n": list(a[k].box_n)} for k in range(n)]
+    own_lo, own_hi, el_lo, el_hi, ext_n = [list(x) for x in arrs]
+    return {"own_lo": own_lo, "own_hi": own_hi, "el_lo": el_lo, "el_hi": el_hi, "ext_n": ext_n,
+            "send": msgs(snd, ns.value), "recv": msgs(rcv, nr.value)}
+
+
+def _pp(ts):
+    return (C.c_void_p * len(ts))(*[(t.data_ptr() if t is not None else None) for t in ts])
+
+
+def form_jacobian_group(spaces, phys, a, b, Us, Udots=None, vals=None, Fs=None, want_F=False, stream=None):
+    """In-process multi-rank Jacobian (IGA_XPORT_LOCAL): spaces[k] = rank k; returns (vals, Fs)."""
+    import torch
+    n = len(spaces)
+    if vals is None:
+        vals = [torch.empty(sp.nnz, dtype=torch.float64, device=Us[k].device) for k, sp in enumerate(spaces)]
+    if want_F and Fs is None:
+        Fs = [torch.empty(sp.nrows, dtype=torch.float64, device=Us[k].device) for k, sp in enumerate(spaces)]
+    hs = (C.c_void_p * n)(*[sp.h.value for sp in spaces])
+    _check(lib().iga_form_jacobian_group(n, hs, C.byref(phys), float(a), float(b), _pp(Us),
+                                         _pp(Udots) if Udots is not None else None, _pp(vals),
+                                         _pp(Fs) if Fs is not None else None, _stream(stream)))
+    return vals, Fs
+
+
+def form_residual_group(spaces, phys, Us, Udots=None, Fs=None, stream=None):
+    import torch
+    n = len(spaces)
+    if Fs is None:
+        Fs = [torch.empty(sp.nrows, dtype=torch.float64, device=Us[k].device) for k, sp in enumerate(spaces)]
+    hs = (C.c_void_p * n)(*[sp.h.value for sp in spaces])
+    _check(lib().iga_form_residual_group(n, hs, C.byref(phys), _pp(Us), _pp(Udots) if Udots is not None else None,
+                                         _pp(Fs), _stream(stream)))
+    return Fs
+
+
 class Space:
     """An IGA space on one CUDA device (iga_space_create).  Inputs are host arrays."""
 
@@ -165,12 +280,7 @@ class Space:
             w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
             self._keep.append(w)
             d.weights = w.ctypes.data_as(C.POINTER(C.c_double))
-        dd = None
-        if dist is not None:
-            dd = _Dist()
-            dd.rank, dd.nranks = dist["rank"], dist["nranks"]
-            for a in range(3):
-                dd.procs[a] = dist["procs"][a] if a < len(dist["procs"]) else 1
+        dd = _make_dist(dist) if dist is not None else None
         h = C.c_void_p()
         _check(L.iga_space_create(C.byref(d), C.byref(dd) if dd is not None else None, device, C.byref(h)))
         self.h = h

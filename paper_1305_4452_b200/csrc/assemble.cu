@@ -37,10 +37,11 @@ __device__ __forceinline__ void elem_coords(const SpaceDev &s, long long el, int
 struct GlobalNodes {
     const SpaceDev *s;
     const double *U, *Ud;
-    long long node[64];
+    long long node[64];      // global node (geometry: control points, weights)
+    long long lnode[64];     // touched-box node (fields U, Udot)
     int M;
-    __device__ double u(int A, int m) const { return __ldg(U + node[A] * M + m); }
-    __device__ double ud(int A, int m) const { return __ldg(Ud + node[A] * M + m); }
+    __device__ double u(int A, int m) const { return __ldg(U + lnode[A] * M + m); }
+    __device__ double ud(int A, int m) const { return __ldg(Ud + lnode[A] * M + m); }
     __device__ bool has_ud() const { return Ud != nullptr; }
     __device__ double w(int A) const { return s->wts ? __ldg(s->wts + node[A]) : 1.0; }
     __device__ double x(int A, int i) const { return __ldg(s->ctrl + node[A] * s->dim + i); }
@@ -92,6 +93,7 @@ k_point(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, c
             if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
         }
         nodes.node[A] = node_index(s, g[0], g[1], g[2]);
+        nodes.lnode[A] = local_node(s, g[0], g[1], g[2]);
     }
     const int bad = pointwise_qp<DIM, P, PH, MODE, JAC>(s, prm, a, b, v, wq, xq, hp, nodes, Dt + t, ldq,
                                                         Rt ? Rt + t : nullptr, ldq);
@@ -111,9 +113,10 @@ k_contract(SpaceDev s, const double *__restrict__ Dt, const double *__restrict__
     constexpr int NQ = ipow(NQ1, DIM), NEN = ipow(NP1, DIM);
     constexpr int NC = KS::NC;
     __shared__ double tabs[DIM][NQ1][3][NP1];
-    __shared__ long long nodeS[NEN], rowL[NEN];
+    __shared__ double *rowP[NEN];               // CSR row of (A, i = 0): owned -> val, halo -> halo buffer
+    __shared__ long long rowL[NEN];             // touched-box node of A (F layout)
     __shared__ double sA[NEN];
-    __shared__ int Wn[NEN], W1n[NEN], W2n[NEN], own[NEN];
+    __shared__ int Wn[NEN], W1n[NEN], W2n[NEN];
     __shared__ int posT[DIM][NP1][NP1];
     extern __shared__ double dyn[];
     double *Ds = dyn;                                   // [NE][NQ]
@@ -141,25 +144,18 @@ k_contract(SpaceDev s, const double *__restrict__ Dt, const double *__restrict__
         int aa[3] = {0, 0, 0};
         int r = A;
         for (int d = DIM - 1; d >= 0; d--) { aa[d] = r % NP1; r /= NP1; }
-        int g[3] = {0, 0, 0}, l[3] = {0, 0, 0}, Wd[3] = {1, 1, 1};
-        long long Sd[3] = {0, 0, 0}, Td[3] = {1, 1, 1};
-        int ok = 1;
+        int g[3] = {0, 0, 0}, Wd[3] = {1, 1, 1};
         for (int d = 0; d < DIM; d++) {
             g[d] = s.ax[d].first[e[d]] + aa[d];
             if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
-            l[d] = g[d] - s.ax[d].own_lo;
-            if (l[d] < 0 || g[d] >= s.ax[d].own_hi) ok = 0;
             Wd[d] = s.ax[d].rowW[g[d]];
-            Sd[d] = s.ax[d].rowS[g[d]];
-            Td[d] = s.ax[d].T;
         }
-        own[A] = ok;
-        nodeS[A] = (long long)M * M * (Sd[0] * Td[1] * Td[2] + Wd[0] * Sd[1] * Td[2] + (long long)Wd[0] * Wd[1] * Sd[2]);
+        int Wtot = 1;
+        rowP[A] = val ? row_start(s, val, g[0], g[1], g[2], 0, M, &Wtot) : nullptr;
         Wn[A] = Wd[0] * Wd[1] * Wd[2];
         W1n[A] = Wd[1];
         W2n[A] = Wd[2];
-        const int n1o = s.ax[1].own_hi - s.ax[1].own_lo, n2o = s.ax[2].own_hi - s.ax[2].own_lo;
-        rowL[A] = (((long long)l[0] * n1o + l[1]) * n2o + l[2]) * M;
+        rowL[A] = local_node(s, g[0], g[1], g[2]) * M;
         sA[A] = (MODE == MODE_NURBS && s.wts) ? s.wts[node_index(s, g[0], g[1], g[2])] : 1.0;
     }
     __syncthreads();
@@ -167,7 +163,6 @@ k_contract(SpaceDev s, const double *__restrict__ Dt, const double *__restrict__
     // ---- residual: thread per test function A --------------------------------------------
     if (Fout) {
         for (int A = tid; A < NEN; A += blockDim.x) {
-            if (!own[A]) continue;
             int aa[3] = {0, 0, 0};
             int r = A;
 #pragma unroll
@@ -203,7 +198,6 @@ k_contract(SpaceDev s, const double *__restrict__ Dt, const double *__restrict__
     if constexpr (JAC) {
         for (int idx = tid; idx < NEN * NEN; idx += blockDim.x) {
             const int A = idx / NEN, B = idx % NEN;
-            if (!own[A]) continue;
             int aa[3] = {0, 0, 0}, bb[3] = {0, 0, 0};
             {
                 int r = A, r2 = B;
@@ -249,7 +243,7 @@ k_contract(SpaceDev s, const double *__restrict__ Dt, const double *__restrict__
             const double sc = sA[A] * sA[B];
 #pragma unroll
             for (int i = 0; i < M; i++) {
-                double *dst = val + nodeS[A] + (long long)i * Wn[A] * M + off;
+                double *dst = rowP[A] + (long long)i * Wn[A] * M + off;
 #pragma unroll
                 for (int j = 0; j < M; j++) atomicAdd(dst + j, sc * K[i][j]);
             }

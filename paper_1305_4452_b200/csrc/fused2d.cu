@@ -28,11 +28,12 @@ template <int P> struct Tile2 {
     static constexpr int NSL = (2 * P + 1) * (2 * P + 1);   // stencil slots per row
 };
 
-// per axis: is function g (unique) complete in tile T of width TE (all support elements inside)
-__device__ __forceinline__ bool complete_axis(const AxisDev &ax, int g, int T, int TE) {
+// per axis: is function g (unique) complete in the tile's element range [elo, elo + TE) (all
+// support elements inside; the cyclic support of a wrapped periodic function never is)
+__device__ __forceinline__ bool complete_axis(const AxisDev &ax, int g, int elo, int TE) {
     const int lo = ax.suplo[g], c = ax.supcnt[g];
     const int hi = lo + c - 1;
-    return hi < ax.nel && lo >= T * TE && hi < (T + 1) * TE;
+    return hi < ax.nel && lo >= elo && hi < elo + TE;
 }
 
 // element's nodes in the tile box: local function A = (a0, a1) -> box index base + a0*NB1 + a1
@@ -164,8 +165,8 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
     for (int tile = blockIdx.x; tile < ntile0 * ntile1; tile += gridDim.x) {
         const int T0 = tile / ntile1, T1 = tile % ntile1;
-        const int e0lo = T0 * TL::TE0, e1lo = T1 * TL::TE1;
-        const int ne0 = min(TL::TE0, A0.nel - e0lo), ne1 = min(TL::TE1, A1.nel - e1lo);
+        const int e0lo = A0.el_lo + T0 * TL::TE0, e1lo = A1.el_lo + T1 * TL::TE1;
+        const int ne0 = min(TL::TE0, A0.el_hi - e0lo), ne1 = min(TL::TE1, A1.el_hi - e1lo);
         const int F00 = A0.first[e0lo], F01 = A1.first[e1lo];
         const int nb0 = ne0 + P, nb1 = ne1 + P;
         // ---- stage the tile: zero rows/F, node data, tables ----
@@ -178,9 +179,10 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 int g0 = F00 + l0, g1 = F01 + l1;
                 if (g0 >= A0.nu) g0 -= A0.nu;
                 if (g1 >= A1.nu) g1 -= A1.nu;
-                const long long node = (long long)g0 * A1.nu + g1;
-                nU[i] = U[node];
-                nUd[i] = Ud ? Ud[node] : 0.0;
+                const long long node = (long long)g0 * A1.nu + g1;             // geometry: global
+                const long long lnode = local_node(s, g0, g1, 0);               // fields: touched box
+                nU[i] = U[lnode];
+                nUd[i] = Ud ? Ud[lnode] : 0.0;
                 nw[i] = s.wts ? s.wts[node] : 1.0;
                 if (s.geom == IGA_GEOM_NURBS) {
                     nx0[i] = s.ctrl[node * 2];
@@ -305,12 +307,16 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 const int p0 = A0.posd[g0 * W2 + d0 + P], p1 = A1.posd[g1 * W2 + d1 + P];
                 if (p0 < 0 || p1 < 0) continue;
                 const bool uniq = (l0 < A0.nu && l0 + A0.nu >= nb0) && (l1 < A1.nu && l1 + A1.nu >= nb1);
-                const bool comp = uniq && complete_axis(A0, g0, T0, TEd[0]) && complete_axis(A1, g1, T1, TEd[1]);
-                const long long addr = A0.rowS[g0] * T1s + (long long)A0.rowW[g0] * A1.rowS[g1]
+                const bool comp = uniq && complete_axis(A0, g0, e0lo, TEd[0]) && complete_axis(A1, g1, e1lo, TEd[1]);
+                // closed-form CSR position over the touched box (row_start, m = 1, trivial axis 2)
+                const int m0 = local_fn(A0, g0), m1 = local_fn(A1, g1);
+                const int sg0 = m0 >= A0.n_own, sg1 = m1 >= A1.n_own;
+                double *base = (sg0 | sg1) ? s.halo + s.hbase[(sg0 * 2 + sg1) * 2] : val;
+                const long long addr = A0.lS[m0] * (sg1 ? A1.Th : T1s) + (long long)A0.rowW[g0] * A1.lS[m1]
                                        + (long long)p0 * A1.rowW[g1] + p1;
                 const double vv = rows[i];
-                if (comp) val[addr] = vv;
-                else if (vv != 0.0) atomicAdd(val + addr, vv);
+                if (comp) base[addr] = vv;
+                else if (vv != 0.0) atomicAdd(base + addr, vv);
             }
         }
         if (Fout) {
@@ -320,35 +326,12 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 int g0 = F00 + l0, g1 = F01 + l1;
                 if (g0 >= A0.nu) g0 -= A0.nu;
                 if (g1 >= A1.nu) g1 -= A1.nu;
-                if (Fb[i] != 0.0) atomicAdd(Fout + (long long)g0 * A1.nu + g1, Fb[i]);
+                if (Fb[i] != 0.0) atomicAdd(Fout + local_node(s, g0, g1, 0), Fb[i]);
             }
         }
         __syncthreads();
     }
     if (errbits) atomicOr(s.errflag, errbits);
-}
-
-// zero the CSR rows that are NOT complete inside their owner tile (they receive red.add)
-template <int P>
-__global__ void k_zero_rows2d(SpaceDev s, double *__restrict__ val) {
-    using TL = Tile2<P>;
-    const AxisDev &A0 = s.ax[0], &A1 = s.ax[1];
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const long long nrows = (long long)A0.nu * A1.nu;
-    if (warp >= nrows) return;
-    const int g0 = (int)(warp / A1.nu), g1 = (int)(warp % A1.nu);
-    const int T0 = A0.suplo[g0] / TL::TE0, T1 = A1.suplo[g1] / TL::TE1;
-    // same test as the fused kernel's write-out, including the unique-copy condition
-    const int l0 = ((g0 - A0.first[T0 * TL::TE0]) % A0.nu + A0.nu) % A0.nu;
-    const int l1 = ((g1 - A1.first[T1 * TL::TE1]) % A1.nu + A1.nu) % A1.nu;
-    const int nb0 = min(TL::TE0, A0.nel - T0 * TL::TE0) + P, nb1 = min(TL::TE1, A1.nel - T1 * TL::TE1) + P;
-    const bool uniq = (l0 + A0.nu >= nb0) && (l1 + A1.nu >= nb1);
-    const bool comp = uniq && complete_axis(A0, g0, T0, TL::TE0) && complete_axis(A1, g1, T1, TL::TE1);
-    if (comp) return;
-    const long long start = A0.rowS[g0] * A1.T + (long long)A0.rowW[g0] * A1.rowS[g1];
-    const int len = A0.rowW[g0] * A1.rowW[g1];
-    for (int k = lane; k < len; k += 32) val[start + k] = 0.0;
 }
 
 template <int P, class PH, int MODE>
@@ -370,7 +353,8 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
     Prm prm;
     for (int i = 0; i < 8; i++) prm.p[i] = phys->p[i];
     const bool jac = val != nullptr;
-    const int nt0 = (s->nel[0] + TL::TE0 - 1) / TL::TE0, nt1 = (s->nel[1] + TL::TE1 - 1) / TL::TE1;
+    const int ne0 = s->el_hi[0] - s->el_lo[0], ne1 = s->el_hi[1] - s->el_lo[1];
+    const int nt0 = (ne0 + TL::TE0 - 1) / TL::TE0, nt1 = (ne1 + TL::TE1 - 1) / TL::TE1;
     const size_t smem = fused2d_smem<P, PH, MODE>(jac);
     static bool attr[2] = {false, false};
     if (!attr[jac]) {
@@ -394,9 +378,10 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
         launches++;
     }
     if (jac) {
-        ProfScope ps(s, "k_zero_rows2d", st);
-        const long long nrows = (long long)s->nu[0] * s->nu[1];
-        k_zero_rows2d<P><<<(unsigned)((nrows * 32 + 255) / 256), 256, 0, st>>>(s->dev, val);
+        // rows not complete inside one tile receive red.add: zero the whole value array (a plain
+        // streaming write, cheaper than selecting the boundary rows)
+        ProfScope ps(s, "k_zero", st);
+        k_zero_vec(val, s->nnz_owned, st, nsm);
         launches++;
     }
     {
@@ -414,7 +399,7 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
 // dispatch: returns IGA_ERR_STATE if the fused 2D path does not apply (caller falls back)
 iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm) {
-    if (s->dim != 2 || s->dof != 1 || s->nranks != 1) return IGA_ERR_STATE;
+    if (s->dim != 2 || s->dof != 1) return IGA_ERR_STATE;
     if (!s->dev.ax[0].uniform || !s->dev.ax[1].uniform) return IGA_ERR_STATE;
     if (s->p[0] != s->p[1]) return IGA_ERR_STATE;
     const int p = s->p[0];

@@ -212,10 +212,13 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     double *sU = sm + F::O_U, *sUd = sm + F::O_UD, *sTab = sm + F::O_TAB, *sQW = sm + F::O_QW, *sQX = sm + F::O_QX;
     double *sHP = sm + F::O_HP, *sPhi = sm + F::O_PHI, *sDV = sm + F::O_DV, *sR = sm + F::O_R, *sD = sm + F::O_D;
     State *sSt = reinterpret_cast<State *>(sm + F::O_ST);
-    long long *sRS = reinterpret_cast<long long *>(sm + F::O_RS);   // [NEN*M] CSR start of row (A, i)
-    long long *sNode = reinterpret_cast<long long *>(sm + F::O_ND); // [NEN]
+    // [NEN*M] CSR row (A, i): offset of its first value from `val`, in doubles.  Halo rows live in
+    // the halo buffer; their offsets are taken in the flat 64-bit address space (both arrays are
+    // 8-byte aligned) so the scatter below addresses everything from the uniform `val` register.
+    long long *sRS = reinterpret_cast<long long *>(sm + F::O_RS);
+    long long *sNode = reinterpret_cast<long long *>(sm + F::O_ND); // [NEN] touched-box node of A
     int *sCO = reinterpret_cast<int *>(sm + F::O_CO);               // [NEN][NEN] column offset (nodes)
-    __shared__ int sG[3 * NP1], sW[3 * NP1], sPosE[3 * NP1 * NP1];
+    __shared__ int sG[3 * NP1], sW[3 * NP1], sPosE[3 * NP1 * NP1], sSeg[3 * NP1];
     __shared__ long long sS[3 * NP1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     int errbits = 0;
@@ -257,7 +260,9 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 if (g >= s.ax[d].nu) g -= s.ax[d].nu;
                 sG[k] = g;
                 sW[k] = s.ax[d].rowW[g];
-                sS[k] = s.ax[d].rowS[g];
+                const int l = local_fn(s.ax[d], g);
+                sS[k] = s.ax[d].lS[l];
+                sSeg[k] = l >= s.ax[d].n_own;
                 continue;
             }
             k -= 3 * NP1;
@@ -268,8 +273,6 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         }
         __syncthreads();
         {
-            const long long T1 = s.ax[1].T, T2 = s.ax[2].T;
-            const long long nu1 = s.ax[1].nu, nu2 = s.ax[2].nu;
             for (int i = tid; i < NEN * NEN + NEN * M; i += F::NT) {
                 if (i < NEN * NEN) {
                     const int A = i / NEN, B = i - A * NEN;
@@ -280,13 +283,19 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 } else {
                     const int k = i - NEN * NEN, A = k / M, m = k - A * M;
                     const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
-                    const long long node = ((long long)sG[a0] * nu1 + sG[NP1 + a1]) * nu2 + sG[2 * NP1 + a2];
+                    const long long node = local_node(s, sG[a0], sG[NP1 + a1], sG[2 * NP1 + a2]);
                     sU[k] = U[node * M + m];
                     sUd[k] = Ud ? Ud[node * M + m] : 0.0;
                     if (m == 0) {
+                        // closed-form row start (iga_internal.cuh row_start) from the staged
+                        // per-axis segment prefixes
                         sNode[A] = node;
+                        const int s0 = sSeg[a0], s1 = sSeg[NP1 + a1], s2 = sSeg[2 * NP1 + a2];
+                        const long long T1 = s1 ? s.ax[1].Th : s.ax[1].T, T2 = s2 ? s.ax[2].Th : s.ax[2].T;
                         const long long W0 = sW[a0], W1 = sW[NP1 + a1], W2 = sW[2 * NP1 + a2];
-                        const long long base = (long long)M * M * (sS[a0] * T1 * T2 + W0 * sS[NP1 + a1] * T2 + W0 * W1 * sS[2 * NP1 + a2]);
+                        const int sub = (s0 * 2 + s1) * 2 + s2;
+                        long long base = (long long)M * M * (sS[a0] * T1 * T2 + W0 * sS[NP1 + a1] * T2 + W0 * W1 * sS[2 * NP1 + a2]);
+                        if (sub) base += ((long long)(uintptr_t)(s.halo + s.hbase[sub]) - (long long)(uintptr_t)val) / 8;
                         const long long Wn = W0 * W1 * W2;
 #pragma unroll
                         for (int ii = 0; ii < M; ii++) sRS[A * M + ii] = base + ii * Wn * M;
@@ -509,7 +518,7 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
 
 iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm) {
-    if (s->dim != 3 || s->mode != MODE_PARAM || s->nranks != 1) return IGA_ERR_STATE;
+    if (s->dim != 3 || s->mode != MODE_PARAM) return IGA_ERR_STATE;
     if (s->p[0] != 2 || s->p[1] != 2 || s->p[2] != 2) return IGA_ERR_STATE;
     const bool uni = s->tab_uniform[0] && s->tab_uniform[1] && s->tab_uniform[2] && !s->force_general;
     if (ph->kind == IGA_PHYS_NS_VMS && s->dof == 4)

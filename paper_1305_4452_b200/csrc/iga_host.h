@@ -5,6 +5,20 @@
 
 #include "iga_internal.cuh"
 
+namespace iga {
+// per-axis host data (space.cu axis_host): everything about one parametric axis, including the
+// box decomposition of its elements over all P rank coordinates
+struct AxisHost {
+    int p = 0, nel = 0, nu = 0, nfun = 0, nq = 0, periodic = 0, colmax = 1, uniform = 1;
+    std::vector<double> U, hpar, qx, qw;
+    std::vector<int> first, rowW, cols, pos, suplo, supcnt, posd;
+    std::vector<int> el_lo, el_hi, own_lo, own_hi, halo;   // [P] per rank coordinate
+};
+iga_status axis_host(const iga_space_desc *d, int a, int P, AxisHost &H);
+struct DistState;   // dist.cu: multi-rank buffers, exchange plan, transport
+int dist_transport(const DistState *D);
+}  // namespace iga
+
 struct iga_space_s {
     int device = 0;
     iga::SpaceDev dev{};                 // device view (pointers into `allocs`)
@@ -18,6 +32,10 @@ struct iga_space_s {
     // distribution (box decomposition)
     int rank = 0, nranks = 1, procs[3] = {1, 1, 1}, rcoord[3] = {0, 0, 0};
     int own_lo[3] = {0, 0, 0}, own_hi[3] = {1, 1, 1};
+    int halo[3] = {0, 0, 0};             // halo functions per axis (touched, owned by the upper neighbour)
+    long long Th[3] = {0, 0, 0};
+    iga::AxisHost part[3];
+    iga::DistState *dist = nullptr;
     int el_lo[3] = {0, 0, 0}, el_hi[3] = {1, 1, 1};
     long long ndof_global = 0, nrows_owned = 0, nnz_owned = 0, nqp_local = 0, nel_local = 0;
     // device allocations owned by the space
@@ -64,4 +82,13 @@ iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b
 iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st);
+// dist.cu
+iga_status dist_setup(iga_space_s *s, const iga_dist *dist);
+void dist_destroy(iga_space_s *s);
+iga_status dist_form(iga_space_s **sp, int n, const iga_phys *ph, double a, double b, const double *const *U,
+                     const double *const *Ud, double *const *val, double *const *F, cudaStream_t st);
+iga_status nccl_unique_id(unsigned char out[128]);
+iga_status dist_plan_host(const iga_space_desc *d, const iga_dist *dist, int64_t own_lo[3], int64_t own_hi[3],
+                          int64_t el_lo[3], int64_t el_hi[3], int64_t ext_n[3], int max_msgs, iga_msg *send,
+                          int *nsend, iga_msg *recv, int *nrecv);
 }  // namespace iga

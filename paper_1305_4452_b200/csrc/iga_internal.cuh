@@ -39,6 +39,12 @@ struct AxisDev {
     const int *supcnt;        // [nu] number of elements in that support
     const int *posd;          // [nu][2p+1] position of column g+delta in row g's list, or -1
     int uniform;              // first[e+1] == first[e] + 1 for all e (simple interior knots)
+    // touched box of this rank (box decomposition): local index l = g - own_lo
+    // (mod nu) in [0, x_n); l < n_own are owned functions, the next x_n - n_own are the halo
+    // (owned by the upper neighbour).  Single rank: own_lo = 0, n_own = x_n = nu.
+    int n_own, x_n;
+    const long long *lS;      // [x_n] prefix of rowW restarting at the owned/halo boundary
+    long long Th;             // sum of rowW over the halo segment
 };
 
 struct SpaceDev {
@@ -50,10 +56,59 @@ struct SpaceDev {
     const double *wts;        // [nnodes]        (or nullptr)
     long long nnodes;
     int *errflag;             // device error flag (bit 0: detJ<=0, bit 1: non-finite)
+    // multi-rank: CSR rows of halo functions (sub-box id s != 0, bit d-1-a set = halo on axis a)
+    // accumulate into the library's halo buffer at hbase[s]; owned rows (s = 0) into csr_val
+    double *halo;
+    long long hbase[8];
 };
+
+// local (touched-box) index of unique function g on an axis
+__host__ __device__ inline int local_fn(const AxisDev &ax, int g) {
+    int l = g - ax.own_lo;
+    if (l < 0) l += ax.nu;
+    return l;
+}
+
+// node index in the touched box (the layout of U / Udot / F inside the kernels; equal to the
+// global node index on a single rank)
+__host__ __device__ inline long long local_node(const SpaceDev &s, int g0, int g1, int g2) {
+    return ((long long)local_fn(s.ax[0], g0) * s.ax[1].x_n + local_fn(s.ax[1], g1)) * s.ax[2].x_n + local_fn(s.ax[2], g2);
+}
+
+// CSR row of functions (g0, g1, g2), component i: pointer to its first value and its width W
+// (nodes).  Closed form over the touched box:
+//   start = m^2 (S0 T1 T2 + W0 S1 T2 + W0 W1 S2) + i W m,  T_a = owned or halo segment total.
+__device__ inline double *row_start(const SpaceDev &s, double *val, int g0, int g1, int g2, int i, int m,
+                                    int *W_out = nullptr) {
+    const int g[3] = {g0, g1, g2};
+    long long S[3], T[3];
+    int W[3], sub = 0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+        const AxisDev &ax = s.ax[a];
+        const int l = local_fn(ax, g[a]);
+        const int seg = l >= ax.n_own;
+        sub = sub * 2 + seg;
+        S[a] = ax.lS[l];
+        T[a] = seg ? ax.Th : ax.T;
+        W[a] = ax.rowW[g[a]];
+    }
+    const long long Wn = (long long)W[0] * W[1] * W[2];
+    if (W_out) *W_out = (int)Wn;
+    double *base = sub ? s.halo + s.hbase[sub] : val;
+    return base + (long long)m * m * (S[0] * T[1] * T[2] + W[0] * S[1] * T[2] + (long long)W[0] * W[1] * S[2])
+           + (long long)i * Wn * m;
+}
 
 __host__ __device__ inline long long node_index(const SpaceDev &s, int g0, int g1, int g2) {
     return ((long long)g0 * s.ax[1].nu + g1) * s.ax[2].nu + g2;
+}
+
+// out-of-line copy for register-critical kernels (keeps the address arithmetic out of their
+// register allocation)
+static __device__ __noinline__ double *row_start_ni(const SpaceDev &s, double *val, int g0, int g1, int g2, int m,
+                                                    int *W_out) {
+    return row_start(s, val, g0, g1, g2, 0, m, W_out);
 }
 
 }  // namespace iga

@@ -272,10 +272,163 @@ static void free_space(iga_space_s *s) {
     cudaGetDevice(&prev);
     cudaSetDevice(s->device);
     prof_collect(s);
+    dist_destroy(s);
     for (cudaEvent_t e : s->prof_pool) cudaEventDestroy(e);
     for (void *p : s->allocs) cudaFree(p);
     cudaSetDevice(prev);
     delete s;
+}
+
+
+// ------------------------------------------------------------------------------------------
+// per-axis host setup (no CUDA): knots (Alg. 1 unclamping), elements, Gauss rule, Alg. 3
+// stencils, supports, and the box decomposition of the axis over P rank coordinates
+// (b_r = floor(N r / P)) with DOF ownership A-9 (owner of a function = owner of the
+// last element of its support).  Touched-but-not-owned functions ("halo") must be the next
+// `halo` functions after the owned range, owned by coordinate c+1 (mod P on periodic axes):
+// true for uniform knots with >= p elements per rank; anything else is rejected.
+// ------------------------------------------------------------------------------------------
+iga_status axis_host(const iga_space_desc *d, int a, int P, AxisHost &H) {
+    const int p = d->degree[a];
+    if (p < 1 || p > MAXP) { set_error("degree must be 1..3"); return IGA_ERR_PARAM; }
+    const int nk = d->n_knots[a];
+    if (nk < 2 * (p + 1) || !d->knots[a]) { set_error("too few knots"); return IGA_ERR_DOMAIN; }
+    std::vector<double> U(d->knots[a], d->knots[a] + nk);
+    for (int i = 0; i + 1 < nk; i++)
+        if (!(U[i] <= U[i + 1])) { set_error("knots must be non-decreasing"); return IGA_ERR_DOMAIN; }
+    const int nfun = nk - p - 1;
+    int nu = nfun;
+    H.periodic = d->periodic[a] ? 1 : 0;
+    if (H.periodic) {
+        const int k = d->periodic_continuity[a];
+        if (k < 0 || k > p - 1) { set_error("periodic continuity must be in [0, p-1]"); return IGA_ERR_DOMAIN; }
+        if (d->geometry == IGA_GEOM_NURBS) { set_error("periodic NURBS geometry (Alg. 2) not supported"); return IGA_ERR_PARAM; }
+        unclamp(U, p, k);
+        nu = nfun - (k + 1);
+    }
+    // elements: nonzero spans inside [U_p, U_nfun]
+    std::vector<int> first;
+    std::vector<double> hpar;
+    for (int sp = p; sp < nfun; sp++)
+        if (U[sp] < U[sp + 1]) { first.push_back(sp - p); hpar.push_back(U[sp + 1] - U[sp]); }
+    const int nel = (int)first.size();
+    if (H.periodic && nu < 2 * p + 1) { set_error("periodic axis needs >= 2p+1 functions"); return IGA_ERR_DOMAIN; }
+    const int nq = d->quad[a] > 0 ? d->quad[a] : p + 1;
+    std::vector<double> gx, gw;
+    gauss_legendre(nq, gx, gw);
+    std::vector<double> qx((size_t)nel * nq), qw((size_t)nel * nq);
+    for (int e = 0; e < nel; e++) {
+        const double lo = U[first[e] + p], hi = U[first[e] + p + 1];
+        for (int q = 0; q < nq; q++) {
+            qx[(size_t)e * nq + q] = 0.5 * (lo + hi) + 0.5 * (hi - lo) * gx[q];
+            qw[(size_t)e * nq + q] = gw[q] * 0.5 * (hi - lo);
+        }
+    }
+    // Alg. 3 on every representative i of each unique function, wrapped mod nu
+    std::vector<std::vector<int>> colset(nu);
+    for (int i = 0; i < nfun; i++) {
+        int k = i;
+        while (k + 1 < nk && U[k] == U[k + 1]) k++;
+        const int l = k - p;
+        k = i + p + 1;
+        while (k - 1 >= 0 && U[k] == U[k - 1]) k--;
+        const int r = k - 1;
+        auto &cs = colset[i % nu];
+        for (int j = l; j <= r; j++) cs.push_back(((j % nu) + nu) % nu);
+    }
+    int colmax = 1;
+    std::vector<int> rowW(nu);
+    for (int g = 0; g < nu; g++) {
+        auto &cs = colset[g];
+        std::sort(cs.begin(), cs.end());
+        cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
+        rowW[g] = (int)cs.size();
+        colmax = std::max(colmax, rowW[g]);
+    }
+    std::vector<int> cols((size_t)nu * colmax, 0);
+    for (int g = 0; g < nu; g++) std::copy(colset[g].begin(), colset[g].end(), cols.begin() + (size_t)g * colmax);
+    // per element: position of column function beta in row function alpha's list
+    std::vector<int> pos((size_t)nel * (p + 1) * (p + 1));
+    for (int e = 0; e < nel; e++)
+        for (int al = 0; al <= p; al++)
+            for (int be = 0; be <= p; be++) {
+                const int ga = (first[e] + al) % nu, gb = (first[e] + be) % nu;
+                const auto &cs = colset[ga];
+                pos[((size_t)e * (p + 1) + al) * (p + 1) + be] = (int)(std::lower_bound(cs.begin(), cs.end(), gb) - cs.begin());
+            }
+    // ownership (A-9)
+    std::vector<int> last_el(nu, -1);
+    for (int e = 0; e < nel; e++)
+        for (int al = 0; al <= p; al++) {
+            const int i = first[e] + al;
+            if (i < nu) last_el[i] = std::max(last_el[i], e);     // representative i = g
+        }
+    for (int g = 0; g < nu; g++)
+        if (last_el[g] < 0) last_el[g] = nel - 1;
+    if (P < 1 || P > nel) { set_error("more ranks than elements on an axis"); return IGA_ERR_PARAM; }
+    H.el_lo.assign(P, 0); H.el_hi.assign(P, 0); H.own_lo.assign(P, 0); H.own_hi.assign(P, 0); H.halo.assign(P, 0);
+    for (int c = 0; c < P; c++) {
+        const int el_lo = (int)((long long)nel * c / P), el_hi = (int)((long long)nel * (c + 1) / P);
+        int own_lo = nu, own_hi = 0, cnt = 0;
+        for (int g = 0; g < nu; g++)
+            if (last_el[g] >= el_lo && last_el[g] < el_hi) { own_lo = std::min(own_lo, g); own_hi = std::max(own_hi, g + 1); cnt++; }
+        if (own_hi <= own_lo || cnt != own_hi - own_lo) { set_error("rank owns no (or a non-contiguous set of) functions on an axis"); return IGA_ERR_PARAM; }
+        H.el_lo[c] = el_lo; H.el_hi[c] = el_hi; H.own_lo[c] = own_lo; H.own_hi[c] = own_hi;
+    }
+    for (int c = 0; c < P; c++) {
+        // touched functions of coordinate c's elements
+        std::vector<char> touched(nu, 0);
+        for (int e = H.el_lo[c]; e < H.el_hi[c]; e++)
+            for (int al = 0; al <= p; al++) touched[(first[e] + al) % nu] = 1;
+        int nt = 0;
+        for (int g = 0; g < nu; g++) nt += touched[g];
+        const int n_own = H.own_hi[c] - H.own_lo[c];
+        const int h = nt - n_own;
+        bool ok = h >= 0 && (P > 1 || h == 0);
+        for (int l = 0; ok && l < nt; l++) ok = touched[(H.own_lo[c] + l) % nu] != 0;
+        if (ok && h > 0) {
+            const int cn = H.periodic ? (c + 1) % P : c + 1;
+            ok = cn < P && cn != c && (H.own_lo[cn] == H.own_hi[c] % nu) && (H.own_hi[cn] - H.own_lo[cn] >= h);
+        }
+        if (!ok) { set_error("box decomposition: a rank's halo is not owned by its upper neighbour (too many ranks for this axis?)"); return IGA_ERR_PARAM; }
+        H.halo[c] = h;
+    }
+    // cyclic support [suplo, suplo+supcnt) of each unique function, and delta positions
+    std::vector<int> suplo(nu, 0), supcnt(nu, 0), posd((size_t)nu * (2 * p + 1), -1);
+    {
+        std::vector<std::vector<int>> sup(nu);
+        for (int e = 0; e < nel; e++)
+            for (int al = 0; al <= p; al++) sup[(first[e] + al) % nu].push_back(e);
+        for (int g = 0; g < nu; g++) {
+            auto &v = sup[g];
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+            const int c = (int)v.size();
+            int lo = c ? v[0] : 0;
+            // cyclic start: the element whose predecessor (mod nel) is not in the support
+            for (int k = 0; k < c; k++) {
+                const int prev = (v[k] - 1 + nel) % nel;
+                if (!std::binary_search(v.begin(), v.end(), prev)) { lo = v[k]; break; }
+            }
+            suplo[g] = lo;
+            supcnt[g] = c;
+            for (int dl = -p; dl <= p; dl++) {
+                if (!H.periodic && (g + dl < 0 || g + dl >= nu)) continue;   // no wrap on open axes
+                const int col = (((g + dl) % nu) + nu) % nu;
+                const auto &cs = colset[g];
+                auto it = std::lower_bound(cs.begin(), cs.end(), col);
+                if (it != cs.end() && *it == col) posd[(size_t)g * (2 * p + 1) + dl + p] = (int)(it - cs.begin());
+            }
+        }
+    }
+    int uniform = 1;
+    for (int e = 0; e + 1 < nel; e++)
+        if (first[e + 1] != first[e] + 1) uniform = 0;
+    H.p = p; H.nel = nel; H.nu = nu; H.nfun = nfun; H.nq = nq; H.colmax = colmax; H.uniform = uniform;
+    H.U = std::move(U); H.first = std::move(first); H.hpar = std::move(hpar); H.qx = std::move(qx); H.qw = std::move(qw);
+    H.rowW = std::move(rowW); H.cols = std::move(cols); H.pos = std::move(pos);
+    H.suplo = std::move(suplo); H.supcnt = std::move(supcnt); H.posd = std::move(posd);
+    return IGA_OK;
 }
 
 static iga_status create(const iga_space_desc *d, const iga_dist *dist, int device, iga_space *out) {
@@ -348,130 +501,34 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             if ((st = upload(s, (int **)&ax.suplo, z)) != IGA_OK) goto fail;
             if ((st = upload(s, (int **)&ax.supcnt, one_i)) != IGA_OK) goto fail;
             if ((st = upload(s, (int **)&ax.posd, z)) != IGA_OK) goto fail;
+            if ((st = upload(s, (long long **)&ax.lS, zl)) != IGA_OK) goto fail;
+            ax.n_own = 1; ax.x_n = 1; ax.Th = 0;
             ax.uniform = 1;
             ax.colmax = 1; ax.T = 1; ax.own_lo = 0; ax.own_hi = 1; ax.el_lo = 0; ax.el_hi = 1;
             s->own_lo[a] = 0; s->own_hi[a] = 1; s->el_lo[a] = 0; s->el_hi[a] = 1;
             continue;
         }
-        const int p = d->degree[a];
-        if (p < 1 || p > MAXP) { st = IGA_ERR_PARAM; set_error("degree must be 1..3"); goto fail; }
-        const int nk = d->n_knots[a];
-        if (nk < 2 * (p + 1) || !d->knots[a]) { st = IGA_ERR_DOMAIN; set_error("too few knots"); goto fail; }
-        std::vector<double> U(d->knots[a], d->knots[a] + nk);
-        for (int i = 0; i + 1 < nk; i++)
-            if (!(U[i] <= U[i + 1])) { st = IGA_ERR_DOMAIN; set_error("knots must be non-decreasing"); goto fail; }
-        const int nfun = nk - p - 1;
-        int nu = nfun;
-        s->periodic[a] = d->periodic[a] ? 1 : 0;
-        if (s->periodic[a]) {
-            const int k = d->periodic_continuity[a];
-            if (k < 0 || k > p - 1) { st = IGA_ERR_DOMAIN; set_error("periodic continuity must be in [0, p-1]"); goto fail; }
-            if (d->geometry == IGA_GEOM_NURBS) { st = IGA_ERR_PARAM; set_error("periodic NURBS geometry (Alg. 2) not supported"); goto fail; }
-            unclamp(U, p, k);
-            nu = nfun - (k + 1);
-        }
-        // elements: nonzero spans inside [U_p, U_nfun]
-        std::vector<int> first;
-        std::vector<double> hpar;
-        for (int sp = p; sp < nfun; sp++)
-            if (U[sp] < U[sp + 1]) { first.push_back(sp - p); hpar.push_back(U[sp + 1] - U[sp]); }
-        const int nel = (int)first.size();
-        if (s->periodic[a] && nu < 2 * p + 1) { st = IGA_ERR_DOMAIN; set_error("periodic axis needs >= 2p+1 functions"); goto fail; }
-        const int nq = d->quad[a] > 0 ? d->quad[a] : p + 1;
-        std::vector<double> gx, gw;
-        gauss_legendre(nq, gx, gw);
-        std::vector<double> qx((size_t)nel * nq), qw((size_t)nel * nq);
-        for (int e = 0; e < nel; e++) {
-            const double lo = U[first[e] + p], hi = U[first[e] + p + 1];
-            for (int q = 0; q < nq; q++) {
-                qx[(size_t)e * nq + q] = 0.5 * (lo + hi) + 0.5 * (hi - lo) * gx[q];
-                qw[(size_t)e * nq + q] = gw[q] * 0.5 * (hi - lo);
-            }
-        }
-        // Alg. 3 on every representative i of each unique function, wrapped mod nu
-        std::vector<std::vector<int>> colset(nu);
-        for (int i = 0; i < nfun; i++) {
-            int k = i;
-            while (k + 1 < nk && U[k] == U[k + 1]) k++;
-            const int l = k - p;
-            k = i + p + 1;
-            while (k - 1 >= 0 && U[k] == U[k - 1]) k--;
-            const int r = k - 1;
-            auto &cs = colset[i % nu];
-            for (int j = l; j <= r; j++) cs.push_back(((j % nu) + nu) % nu);
-        }
-        int colmax = 1;
-        std::vector<int> rowW(nu);
-        for (int g = 0; g < nu; g++) {
-            auto &cs = colset[g];
-            std::sort(cs.begin(), cs.end());
-            cs.erase(std::unique(cs.begin(), cs.end()), cs.end());
-            rowW[g] = (int)cs.size();
-            colmax = std::max(colmax, rowW[g]);
-        }
-        std::vector<int> cols((size_t)nu * colmax, 0);
-        for (int g = 0; g < nu; g++) std::copy(colset[g].begin(), colset[g].end(), cols.begin() + (size_t)g * colmax);
-        // per element: position of column function beta in row function alpha's list
-        std::vector<int> pos((size_t)nel * (p + 1) * (p + 1));
-        for (int e = 0; e < nel; e++)
-            for (int al = 0; al <= p; al++)
-                for (int be = 0; be <= p; be++) {
-                    const int ga = (first[e] + al) % nu, gb = (first[e] + be) % nu;
-                    const auto &cs = colset[ga];
-                    const int ps = (int)(std::lower_bound(cs.begin(), cs.end(), gb) - cs.begin());
-                    pos[((size_t)e * (p + 1) + al) * (p + 1) + be] = ps;
-                }
-        // box decomposition of elements (b_r = floor(N r / P)) and dof ownership
-        // (A-9: owner of a function = owner of the last element of its support)
-        const int P = s->procs[a], rc = s->rcoord[a];
-        const int el_lo = (int)((long long)nel * rc / P), el_hi = (int)((long long)nel * (rc + 1) / P);
-        std::vector<int> last_el(nu, -1);
-        for (int e = 0; e < nel; e++)
-            for (int al = 0; al <= p; al++) {
-                const int i = first[e] + al;
-                if (i < nu) last_el[i] = std::max(last_el[i], e);     // representative i = g
-            }
-        for (int g = 0; g < nu; g++)
-            if (last_el[g] < 0) last_el[g] = nel - 1;
-        int own_lo = nu, own_hi = 0;
-        for (int g = 0; g < nu; g++)
-            if (last_el[g] >= el_lo && last_el[g] < el_hi) { own_lo = std::min(own_lo, g); own_hi = std::max(own_hi, g + 1); }
-        if (own_hi <= own_lo) { own_lo = own_hi = 0; }
-        // cyclic support [suplo, suplo+supcnt) of each unique function, and delta positions
-        std::vector<int> suplo(nu, 0), supcnt(nu, 0), posd((size_t)nu * (2 * p + 1), -1);
-        {
-            std::vector<std::vector<int>> sup(nu);
-            for (int e = 0; e < nel; e++)
-                for (int al = 0; al <= p; al++) sup[(first[e] + al) % nu].push_back(e);
-            for (int g = 0; g < nu; g++) {
-                auto &v = sup[g];
-                std::sort(v.begin(), v.end());
-                v.erase(std::unique(v.begin(), v.end()), v.end());
-                const int c = (int)v.size();
-                int lo = c ? v[0] : 0;
-                // cyclic start: the element whose predecessor (mod nel) is not in the support
-                for (int k = 0; k < c; k++) {
-                    const int prev = (v[k] - 1 + nel) % nel;
-                    if (!std::binary_search(v.begin(), v.end(), prev)) { lo = v[k]; break; }
-                }
-                suplo[g] = lo;
-                supcnt[g] = c;
-                for (int dl = -p; dl <= p; dl++) {
-                    if (!s->periodic[a] && (g + dl < 0 || g + dl >= nu)) continue;   // no wrap on open axes
-                    const int col = (((g + dl) % nu) + nu) % nu;
-                    const auto &cs = colset[g];
-                    auto it = std::lower_bound(cs.begin(), cs.end(), col);
-                    if (it != cs.end() && *it == col) posd[(size_t)g * (2 * p + 1) + dl + p] = (int)(it - cs.begin());
-                }
-            }
-        }
-        int uniform = 1;
-        for (int e = 0; e + 1 < nel; e++)
-            if (first[e + 1] != first[e] + 1) uniform = 0;
-        std::vector<long long> rowS(nu, 0);
-        long long T = 0;
+        AxisHost H;
+        if ((st = axis_host(d, a, s->procs[a], H)) != IGA_OK) goto fail;
+        const int p = H.p, nel = H.nel, nu = H.nu, nfun = H.nfun, nq = H.nq;
+        const int rc = s->rcoord[a];
+        const int el_lo = H.el_lo[rc], el_hi = H.el_hi[rc], own_lo = H.own_lo[rc], own_hi = H.own_hi[rc];
+        const int halo = H.halo[rc], n_own = own_hi - own_lo;
+        std::vector<double> &U = H.U, &qx = H.qx, &qw = H.qw, &hpar = H.hpar;
+        std::vector<int> &first = H.first, &rowW = H.rowW, &cols = H.cols, &pos = H.pos;
+        std::vector<int> &suplo = H.suplo, &supcnt = H.supcnt, &posd = H.posd;
+        const int colmax = H.colmax, uniform = H.uniform;
+        s->periodic[a] = H.periodic;
+        // closed-form CSR row starts over the touched box: prefix sums of the Alg. 3 widths,
+        // restarting at the owned / halo segment boundary (local index l = g - own_lo mod nu)
+        std::vector<long long> rowS(nu, 0), lS(n_own + halo + 1, 0);
+        long long T = 0, Th = 0;
         for (int g = own_lo; g < own_hi; g++) { rowS[g] = T; T += rowW[g]; }
-
+        for (int l = 0; l < n_own; l++) lS[l] = rowS[own_lo + l];
+        for (int l = n_own; l < n_own + halo; l++) { lS[l] = Th; Th += rowW[(own_lo + l) % nu]; }
+        s->halo[a] = halo;
+        s->Th[a] = Th;
+        s->part[a] = H;
         s->p[a] = p; s->nel[a] = nel; s->nu[a] = nu; s->nq[a] = nq; s->nfun[a] = nfun;
         s->U[a] = U; s->rowW[a] = rowW; s->cols[a] = cols; s->colmax[a] = colmax;
         s->own_lo[a] = own_lo; s->own_hi[a] = own_hi; s->el_lo[a] = el_lo; s->el_hi[a] = el_hi;
@@ -491,6 +548,8 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         if ((st = upload(s, (int **)&ax.suplo, suplo)) != IGA_OK) goto fail;
         if ((st = upload(s, (int **)&ax.supcnt, supcnt)) != IGA_OK) goto fail;
         if ((st = upload(s, (int **)&ax.posd, posd)) != IGA_OK) goto fail;
+        if ((st = upload(s, (long long **)&ax.lS, lS)) != IGA_OK) goto fail;
+        ax.n_own = n_own; ax.x_n = n_own + halo; ax.Th = Th;
         ax.uniform = uniform;
         if ((st = dalloc(s, &dtab, (size_t)nel * nq * 3 * (p + 1))) != IGA_OK) goto fail;
         {
@@ -555,6 +614,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         if ((st = dalloc(s, &s->errflag, 1)) != IGA_OK) goto fail;
         CUDA_TRY(cudaMemset(s->errflag, 0, sizeof(int)));
         s->dev.errflag = s->errflag;
+        if (s->nranks > 1 && (st = dist_setup(s, dist)) != IGA_OK) goto fail;
         // quadrature-point coefficient workspace: <= 4 GiB, sized to the local element count
         size_t want = (size_t)s->nqp_local * 512 * sizeof(double);
         const size_t cap = (size_t)4 << 30;
@@ -620,8 +680,43 @@ iga_status iga_csr_pattern(iga_space s, int64_t *row_ptr, int32_t *col_idx, void
 
 static iga_status check_phys(iga_space s, const iga_phys *phys) {
     if (!s || !phys) { set_error("null argument"); return IGA_ERR_PARAM; }
-    if (s->nranks > 1) { set_error("multi-rank forms go through iga_form_*_dist"); return IGA_ERR_STATE; }
     return IGA_OK;
+}
+
+// single-space form: one rank, or one rank of an NCCL decomposition
+static iga_status form_one(iga_space s, const iga_phys *phys, double a, double b, const double *U, const double *Ud,
+                           double *val, double *F, cudaStream_t st) {
+    if (s->nranks > 1) {
+        if (!s->dist || dist_transport(s->dist) != IGA_XPORT_NCCL) {
+            set_error("IGA_XPORT_LOCAL spaces form through iga_form_*_group");
+            return IGA_ERR_STATE;
+        }
+        return dist_form(&s, 1, phys, a, b, &U, &Ud, &val, &F, st);
+    }
+    return launch_form(s, phys, a, b, U, Ud, val, F, st);
+}
+
+static iga_status form_group(int n, const iga_space *spaces, const iga_phys *phys, double a, double b,
+                             const double *const *U, const double *const *Ud, double *const *val, double *const *F,
+                             cudaStream_t st) {
+    if (n < 1 || n > 64 || !spaces || !phys || !U) { set_error("bad group arguments"); return IGA_ERR_PARAM; }
+    std::vector<iga_space_s *> sp(n);
+    for (int k = 0; k < n; k++) {
+        sp[k] = spaces[k];
+        if (!sp[k] || sp[k]->nranks != n || sp[k]->rank != k || sp[k]->device != sp[0]->device) {
+            set_error("group: spaces[k] must be rank k of an n-rank decomposition on one device");
+            return IGA_ERR_PARAM;
+        }
+        if (n > 1 && (!sp[k]->dist || dist_transport(sp[k]->dist) != IGA_XPORT_LOCAL)) {
+            set_error("group forms need IGA_XPORT_LOCAL spaces");
+            return IGA_ERR_STATE;
+        }
+    }
+    std::vector<const double *> Ud0(n, nullptr);
+    std::vector<double *> v0(n, nullptr), F0(n, nullptr);
+    if (n == 1) return launch_form(sp[0], phys, a, b, U[0], Ud ? Ud[0] : nullptr, val ? val[0] : nullptr,
+                                   F ? F[0] : nullptr, st);
+    return dist_form(sp.data(), n, phys, a, b, U, Ud ? Ud : Ud0.data(), val ? val : v0.data(), F ? F : F0.data(), st);
 }
 
 iga_status iga_form_residual(iga_space s, const iga_phys *phys, const double *U, const double *Udot, double *F,
@@ -632,7 +727,7 @@ iga_status iga_form_residual(iga_space s, const iga_phys *phys, const double *U,
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(s->device);
-    st = launch_form(s, phys, 0.0, 0.0, U, Udot, nullptr, F, (cudaStream_t)stream);
+    st = form_one(s, phys, 0.0, 0.0, U, Udot, nullptr, F, (cudaStream_t)stream);
     cudaSetDevice(prev);
     return st;
 }
@@ -645,7 +740,7 @@ iga_status iga_form_jacobian(iga_space s, const iga_phys *phys, double a, double
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(s->device);
-    st = launch_form(s, phys, a, b, U, Udot, csr_val, F, (cudaStream_t)stream);
+    st = form_one(s, phys, a, b, U, Udot, csr_val, F, (cudaStream_t)stream);
     cudaSetDevice(prev);
     return st;
 }
@@ -655,6 +750,7 @@ iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, d
     iga_status st = check_phys(s, phys);
     if (st != IGA_OK) return st;
     if (!U_host || !csr_val_host) { set_error("U and csr_val are required"); return IGA_ERR_PARAM; }
+    if (s->nranks > 1) { set_error("the host-buffer variant is single-rank"); return IGA_ERR_STATE; }
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(s->device);
@@ -704,6 +800,42 @@ iga_status iga_space_check(iga_space s, void *stream) {
 }
 
 int iga_last_launch_count(iga_space s) { return s ? s->last_launches : 0; }
+
+iga_status iga_form_jacobian_group(int n, const iga_space *spaces, const iga_phys *phys, double a, double b,
+                                   const double *const *U, const double *const *Udot, double *const *csr_val,
+                                   double *const *F, void *stream) {
+    if (!csr_val) { set_error("csr_val is required"); return IGA_ERR_PARAM; }
+    if (n < 1 || !spaces || !spaces[0]) { set_error("bad group arguments"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(spaces[0]->device);
+    iga_status st = form_group(n, spaces, phys, a, b, U, Udot, csr_val, F, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
+iga_status iga_form_residual_group(int n, const iga_space *spaces, const iga_phys *phys, const double *const *U,
+                                   const double *const *Udot, double *const *F, void *stream) {
+    if (!F) { set_error("F is required"); return IGA_ERR_PARAM; }
+    if (n < 1 || !spaces || !spaces[0]) { set_error("bad group arguments"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(spaces[0]->device);
+    iga_status st = form_group(n, spaces, phys, 0.0, 0.0, U, Udot, nullptr, F, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
+iga_status iga_dist_plan(const iga_space_desc *desc, const iga_dist *dist, int64_t own_lo[3], int64_t own_hi[3],
+                         int64_t el_lo[3], int64_t el_hi[3], int64_t ext_n[3], int max_msgs, iga_msg *send, int *nsend,
+                         iga_msg *recv, int *nrecv) {
+    return dist_plan_host(desc, dist, own_lo, own_hi, el_lo, el_hi, ext_n, max_msgs, send, nsend, recv, nrecv);
+}
+
+iga_status iga_nccl_unique_id(unsigned char out[128]) {
+    if (!out) { set_error("null argument"); return IGA_ERR_PARAM; }
+    return nccl_unique_id(out);
+}
 
 iga_status iga_space_set_option(iga_space s, const char *key, long long value) {
     if (!s || !key) { set_error("null argument"); return IGA_ERR_PARAM; }
