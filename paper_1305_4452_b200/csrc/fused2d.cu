@@ -153,6 +153,12 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     double *qxb = qwb + 2 * TL::TE1 * NQ1;              // [2][TE][NQ1]  coordinates
     double *hpb = qxb + 2 * TL::TE1 * NQ1;              // [2][TE]
     double *scr = hpb + 2 * TL::TE1;                    // [NGRP][SCR][NQ]
+    // write-out metadata of the tile's rows (computed once per node, not per entry)
+    long long *rowOff = reinterpret_cast<long long *>(scr + (size_t)NGRP * SCR * NQ);   // [NBN] CSR row start - val
+    int *rowW1 = reinterpret_cast<int *>(rowOff + NBN);     // [NBN] Alg. 3 width along axis 1
+    int *rowSt = rowW1 + NBN;                               // [NBN] -1 outside / 0 boundary (red.add) / 1 complete
+    int *pd0 = rowSt + NBN;                                 // [NB0][W2] position of column g0+delta in row g0
+    int *pd1 = pd0 + NB0 * W2;                              // [NB1][W2]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int grp_in_warp = lane / G, t = lane % G;
@@ -175,6 +181,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         for (int i = tid; i < NBN; i += blockDim.x) {
             Fb[i] = 0.0;
             const int l0 = i / NB1, l1 = i % NB1;
+            int st = -1;
             if (l0 < nb0 && l1 < nb1) {
                 int g0 = F00 + l0, g1 = F01 + l1;
                 if (g0 >= A0.nu) g0 -= A0.nu;
@@ -188,6 +195,33 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     nx0[i] = s.ctrl[node * 2];
                     nx1[i] = s.ctrl[node * 2 + 1];
                 }
+                if (JAC) {
+                    // closed-form CSR row start over the touched box (row_start with m = 1 and a
+                    // trivial axis 2); halo rows as offsets from val in the flat address space
+                    const int m0 = local_fn(A0, g0), m1 = local_fn(A1, g1);
+                    const int sg0 = m0 >= A0.n_own, sg1 = m1 >= A1.n_own;
+                    long long off = A0.lS[m0] * (sg1 ? A1.Th : A1.T) + (long long)A0.rowW[g0] * A1.lS[m1];
+                    if (sg0 | sg1)
+                        off += ((long long)(uintptr_t)(s.halo + s.hbase[(sg0 * 2 + sg1) * 2]) - (long long)(uintptr_t)val) / 8;
+                    rowOff[i] = off;
+                    rowW1[i] = A1.rowW[g1];
+                    // complete = every support element inside this tile and the row appears once in
+                    // the tile box (small periodic meshes wrap the box onto itself) -> plain store;
+                    // otherwise red.add of the partial sums
+                    const bool uniq = (l0 < A0.nu && l0 + A0.nu >= nb0) && (l1 < A1.nu && l1 + A1.nu >= nb1);
+                    st = (uniq && complete_axis(A0, g0, e0lo, TEd[0]) && complete_axis(A1, g1, e1lo, TEd[1])) ? 1 : 0;
+                }
+            }
+            if (JAC) rowSt[i] = st;
+        }
+        if (JAC) {
+            for (int i = tid; i < (NB0 + NB1) * W2; i += blockDim.x) {
+                const int d = i >= NB0 * W2, k = d ? i - NB0 * W2 : i;
+                const int l = k / W2, dl = k % W2;
+                const AxisDev &ax = d ? A1 : A0;
+                int g = (d ? F01 : F00) + l;
+                if (g >= ax.nu) g -= ax.nu;
+                pd0[i] = (l < (d ? nb1 : nb0)) ? ax.posd[g * W2 + dl] : -1;
             }
         }
         for (int i = tid; i < 2 * TL::TE1 * NQ1 * 3 * NP1; i += blockDim.x) {
@@ -294,29 +328,19 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         __syncthreads();
 
         // ---- write-out: complete rows with plain stores, boundary rows with red.add ----
-        const long long T1s = A1.T;
         if (JAC) {
             for (int i = tid; i < NBN * NSL; i += blockDim.x) {
-                const int node = i / NSL, slot = i % NSL;
-                const int l0 = node / NB1, l1 = node % NB1;
-                if (l0 >= nb0 || l1 >= nb1) continue;
-                int g0 = F00 + l0, g1 = F01 + l1;
-                if (g0 >= A0.nu) g0 -= A0.nu;
-                if (g1 >= A1.nu) g1 -= A1.nu;
-                const int d0 = slot / W2 - P, d1 = slot % W2 - P;
-                const int p0 = A0.posd[g0 * W2 + d0 + P], p1 = A1.posd[g1 * W2 + d1 + P];
+                const int node = i / NSL, slot = i - node * NSL;
+                const int st = rowSt[node];
+                if (st < 0) continue;
+                const int l0 = node / NB1, l1 = node - l0 * NB1;
+                const int d0 = slot / W2, d1 = slot - d0 * W2;
+                const int p0 = pd0[l0 * W2 + d0], p1 = pd1[l1 * W2 + d1];
                 if (p0 < 0 || p1 < 0) continue;
-                const bool uniq = (l0 < A0.nu && l0 + A0.nu >= nb0) && (l1 < A1.nu && l1 + A1.nu >= nb1);
-                const bool comp = uniq && complete_axis(A0, g0, e0lo, TEd[0]) && complete_axis(A1, g1, e1lo, TEd[1]);
-                // closed-form CSR position over the touched box (row_start, m = 1, trivial axis 2)
-                const int m0 = local_fn(A0, g0), m1 = local_fn(A1, g1);
-                const int sg0 = m0 >= A0.n_own, sg1 = m1 >= A1.n_own;
-                double *base = (sg0 | sg1) ? s.halo + s.hbase[(sg0 * 2 + sg1) * 2] : val;
-                const long long addr = A0.lS[m0] * (sg1 ? A1.Th : T1s) + (long long)A0.rowW[g0] * A1.lS[m1]
-                                       + (long long)p0 * A1.rowW[g1] + p1;
+                double *dst = val + rowOff[node] + (long long)p0 * rowW1[node] + p1;
                 const double vv = rows[i];
-                if (comp) base[addr] = vv;
-                else if (vv != 0.0) atomicAdd(base + addr, vv);
+                if (st) *dst = vv;
+                else if (vv != 0.0) atomicAdd(dst, vv);
             }
         }
         if (Fout) {
@@ -343,7 +367,8 @@ static size_t fused2d_smem(bool jac) {
     const int NBN = TL::NB0 * TL::NB1;
     size_t n = (jac ? (size_t)NBN * TL::NSL : 0) + 6 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
                + 2 * TL::TE1 + (size_t)NGRP * ((jac ? L::NE : 0) + L::NR) * NQ;
-    return n * sizeof(double);
+    // row metadata: rowOff (8 B) + rowW1, rowSt (4 B each) per node, posd tables
+    return n * sizeof(double) + (size_t)NBN * 16 + (size_t)(TL::NB0 + TL::NB1) * (2 * P + 1) * sizeof(int);
 }
 
 template <int P, class PH, int MODE>

@@ -306,7 +306,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         __syncthreads();
 
         // ---- 2. field kinds per (q, m) ----
-        for (int task = tid; task < NQ * M; task += F::NT) {
+        for (int task = (dbg & 4) ? NQ * M : tid; task < NQ * M; task += F::NT) {
             const int q = task / M, m = task % M;
             const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
             double acc[NKS + 1];
@@ -340,7 +340,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         __syncthreads();
 
         // ---- 3. per-point state + residual coefficients ----
-        if (tid < NQ) {
+        if (tid < NQ && !(dbg & 8)) {
             const int q = tid;
             const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
             Fields<3, M> Fq;
@@ -384,7 +384,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
         // ---- 4. Jacobian coefficients: warp-uniform trial column (k2 = qk(kq), j), lane = q ----
         if constexpr (JAC) {
-            for (int kj = warp; kj < NQK * M; kj += F::NWARP) {
+            for (int kj = (dbg & 16) ? NQK * M : warp; kj < NQK * M; kj += F::NWARP) {
                 if (lane < NQ) {
                     const int q = lane;
                     const State st = sSt[q];
@@ -439,7 +439,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             }
         }
         // ---- 6. residual F_e[A, i], thread = (A, i) (q fully unrolled) ----
-        if (Fout && tid < NEN * M) {
+        if (Fout && tid < NEN * M && !(dbg & 32)) {
             const int A = tid / M, Ii = tid - A * M;
             const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
             static_for<M>([&](auto II) {
