@@ -50,12 +50,28 @@ struct SmemNodes2 {
     __device__ __forceinline__ double x(int A, int i) const { return i == 0 ? px0[idx(A)] : px1[idx(A)]; }
 };
 
+// uniform knots: every element shares the 1D tables (translation invariance of uniform
+// B-splines); they travel as a __grid_constant__ parameter so the unrolled test-side
+// contraction reads them as constant-bank operands instead of shared-memory loads
+template <int P>
+struct UniTab2 {
+    double t[2][P + 1][3][P + 1];   // [axis][q][k][a]
+};
+
 // test-side sum factorisation of one column (trial function (b0,b1)) in 2D
-template <class L, class KS, int P>
+template <class L, class KS, int P, bool UNI>
 __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], const double *__restrict__ Dg,
                                               const double *__restrict__ tb0, const double *__restrict__ tb1,
-                                              int b0, int b1) {
+                                              int b0, int b1, const UniTab2<P> &ut) {
     constexpr int NP1 = P + 1, NQ1 = P + 1, NQ = NQ1 * NQ1, NC = KS::NC;
+    auto T0 = [&](int q, int k, int a) -> double {
+        if constexpr (UNI) return ut.t[0][q][k][a];
+        else return tb0[(q * 3 + k) * NP1 + a];
+    };
+    auto T1 = [&](int q, int k, int a) -> double {
+        if constexpr (UNI) return ut.t[1][q][k][a];
+        else return tb1[(q * 3 + k) * NP1 + a];
+    };
     // tb_d layout: [q][k][a]
 #pragma unroll
     for (int A = 0; A < NP1 * NP1; A++) Kc[A] = 0.0;
@@ -100,7 +116,7 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
                         constexpr int t = decltype(T)::value;
                         constexpr int o0 = KS::ord(c, t, 0), o1 = KS::ord(c, t, 1);
 #pragma unroll
-                        for (int a1 = 0; a1 < NP1; a1++) S[o0][a1] += H[c] * tb1[(q1 * 3 + o1) * NP1 + a1];
+                        for (int a1 = 0; a1 < NP1; a1++) S[o0][a1] += H[c] * T1(q1, o1, a1);
                     });
                 }
             });
@@ -121,7 +137,7 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
             if (!used) continue;
 #pragma unroll
             for (int a0 = 0; a0 < NP1; a0++) {
-                const double n0 = tb0[(q0 * 3 + o0) * NP1 + a0];
+                const double n0 = T0(q0, o0, a0);
 #pragma unroll
                 for (int a1 = 0; a1 < NP1; a1++) Kc[a0 * NP1 + a1] += n0 * S[o0][a1];
             }
@@ -129,10 +145,11 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
     }
 }
 
-template <int P, class PH, int MODE, bool JAC>
+template <int P, class PH, int MODE, bool JAC, bool UNI>
 __global__ void __launch_bounds__(32 * Tile2<P>::NWARP, 1)
 k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
-          double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1) {
+          double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1,
+          const __grid_constant__ UniTab2<P> ut) {
     using L = Lists<PH, 2, MODE>;
     using KS = typename L::KS;
     using TL = Tile2<P>;
@@ -312,7 +329,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 // (3) Jacobian column B = t
                 if constexpr (JAC) {
                     double Kc[NEN];
-                    tsf_column_2d<L, KS, P>(Kc, gs, tb0, tb1, c0, c1);
+                    tsf_column_2d<L, KS, P, UNI>(Kc, gs, tb0, tb1, c0, c1, ut);
 #pragma unroll
                     for (int A = 0; A < NEN; A++) {
                         const int a0 = A / NP1, a1 = A % NP1;
@@ -371,6 +388,28 @@ static size_t fused2d_smem(bool jac) {
     return n * sizeof(double) + (size_t)NBN * 16 + (size_t)(TL::NB0 + TL::NB1) * (2 * P + 1) * sizeof(int);
 }
 
+template <int P, class PH, int MODE, bool JAC, bool UNI>
+static iga_status launch_k2(iga_space_s *s, const Prm &prm, double a, double b, const double *U, const double *Ud,
+                            double *val, double *F, int nt0, int nt1, const UniTab2<P> &ut, cudaStream_t st, int nsm) {
+    using TL = Tile2<P>;
+    constexpr int NT = 32 * TL::NWARP;
+    const size_t smem = fused2d_smem<P, PH, MODE>(JAC);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t ce = cudaFuncSetAttribute(k_fused2d<P, PH, MODE, JAC, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem);
+        if (ce != cudaSuccess) { set_error(std::string("fused2d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+        attr = true;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, JAC, UNI>, NT, smem);
+    occ = std::max(occ, 1);
+    const int grid = std::min(nt0 * nt1, nsm * occ);
+    ProfScope ps(s, "k_fused2d", st);
+    k_fused2d<P, PH, MODE, JAC, UNI><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1, ut);
+    return IGA_OK;
+}
+
 template <int P, class PH, int MODE>
 iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U, const double *Ud,
                        double *val, double *F, cudaStream_t st, int nsm) {
@@ -380,22 +419,11 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
     const bool jac = val != nullptr;
     const int ne0 = s->el_hi[0] - s->el_lo[0], ne1 = s->el_hi[1] - s->el_lo[1];
     const int nt0 = (ne0 + TL::TE0 - 1) / TL::TE0, nt1 = (ne1 + TL::TE1 - 1) / TL::TE1;
-    const size_t smem = fused2d_smem<P, PH, MODE>(jac);
-    static bool attr[2] = {false, false};
-    if (!attr[jac]) {
-        cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused2d<P, PH, MODE, true>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                             : cudaFuncSetAttribute(k_fused2d<P, PH, MODE, false>,
-                                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (ce != cudaSuccess) { set_error(std::string("fused2d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
-        attr[jac] = true;
-    }
-    int occ = 1;
-    constexpr int NT = 32 * TL::NWARP;
-    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, true>, NT, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, false>, NT, smem);
-    occ = std::max(occ, 1);
-    const int grid = std::min(nt0 * nt1, nsm * occ);
+    const bool uni = s->tab_uniform[0] && s->tab_uniform[1] && !s->force_general;
+    UniTab2<P> ut{};
+    if (uni)
+        for (int d = 0; d < 2; d++)
+            for (int i = 0; i < (P + 1) * 3 * (P + 1); i++) (&ut.t[d][0][0][0])[i] = s->tab0[d][i];
     int launches = 0;
     if (F) {
         ProfScope ps(s, "k_zero", st);
@@ -409,12 +437,13 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
         k_zero_vec(val, s->nnz_owned, st, nsm);
         launches++;
     }
-    {
-        ProfScope ps(s, "k_fused2d", st);
-        if (jac) k_fused2d<P, PH, MODE, true><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
-        else k_fused2d<P, PH, MODE, false><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1);
-        launches++;
-    }
+    iga_status r;
+    if (jac) r = uni ? launch_k2<P, PH, MODE, true, true>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
+                     : launch_k2<P, PH, MODE, true, false>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
+    else r = uni ? launch_k2<P, PH, MODE, false, true>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
+                 : launch_k2<P, PH, MODE, false, false>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
+    if (r != IGA_OK) return r;
+    launches++;
     s->last_launches = launches;
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) { set_error(std::string("fused2d launch: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }

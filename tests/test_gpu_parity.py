@@ -23,7 +23,9 @@ def _gpu():
 
 def _gpu_assemble(iga, w, a=None, b=None, params=None, Udot=None, want_F=True, split=False):
     sp = iga.Space.from_workload(w)
-    if split:
+    if split == "general":
+        sp.set_option("general", 1)          # fused kernels without the uniform-table fast path
+    elif split:
         sp.set_option("split", 1)
     dev = torch.device("cuda", 0)
     U = torch.from_numpy(w.U).to(dev)
@@ -44,7 +46,7 @@ SMALL = [(1, 16), (1, 5), (2, 3), (2, 16), (3, 5), (3, 12), (4, 2), (4, 5), (5, 
 SMALL_2D_TILES = [(1, 17), (2, 9), (2, 21), (3, 16), (3, 33), (3, 40)]   # several tiles + ragged tails
 
 
-@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("split", [False, True, "general"])
 @pytest.mark.parametrize("cid,n", SMALL + SMALL_2D_TILES)
 def test_small_full_parity(cid, n, split):
     """Whole matrix vs dense-then-CSR oracle on small meshes (several elements / tiles, ragged
