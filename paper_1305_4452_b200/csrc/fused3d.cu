@@ -228,6 +228,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         else return sTab[((d * NQ1 + q) * 3 + k) * NP1 + aa];
     };
 
+    const bool uni_knots = s.ax[0].uniform && s.ax[1].uniform && s.ax[2].uniform;
     for (long long el = blockIdx.x; el < nelem; el += gridDim.x) {
         int e[3];
         {
@@ -236,39 +237,64 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             e[1] = s.ax[1].el_lo + (int)(r % n1); r /= n1;
             e[0] = s.ax[0].el_lo + (int)r;
         }
-        // ---- 1. stage: tables, per-axis function data, position tables (one round trip) ----
-        for (int i = tid; i < 3 * NQ1 * 3 * NP1 + 6 * NQ1 + 3 + 3 * NP1 + 3 * NP1 * NP1; i += F::NT) {
+        auto EL = [&](int d) { return d == 0 ? e[0] : (d == 1 ? e[1] : e[2]); };   // no local-memory indexing
+        // ---- 1. stage: tables, per-axis function data, position tables, and (uniform knots:
+        //         first[e] = first0 + e, no dependent load) U_e -- one global round trip ----
+        const int nU1 = uni_knots ? NEN * M : 0;
+        for (int i = tid; i < 3 * NQ1 * 3 * NP1 + 6 * NQ1 + 3 + 3 * NP1 + 3 * NP1 * NP1 + nU1; i += F::NT) {
             int k = i;
             if (k < 3 * NQ1 * 3 * NP1) {
                 const int d = k / (NQ1 * 3 * NP1), r = k % (NQ1 * 3 * NP1);
-                sTab[k] = s.ax[d].tab[(size_t)e[d] * NQ1 * 3 * NP1 + r];
+                if constexpr (UNI) sTab[k] = (&ut.t[0][0][0][0])[k];
+                else sTab[k] = s.ax[d].tab[(size_t)EL(d) * NQ1 * 3 * NP1 + r];
                 continue;
             }
             k -= 3 * NQ1 * 3 * NP1;
             if (k < 6 * NQ1) {
                 const int w = k / (3 * NQ1), r = k % (3 * NQ1), d = r / NQ1, q = r % NQ1;
-                if (w == 0) sQW[r] = s.ax[d].qw[(size_t)e[d] * NQ1 + q];
-                else sQX[r] = s.ax[d].qx[(size_t)e[d] * NQ1 + q];
+                if (w == 0) {
+                    if constexpr (UNI) sQW[r] = ut.qw[d][q];
+                    else sQW[r] = s.ax[d].qw[(size_t)EL(d) * NQ1 + q];
+                } else sQX[r] = s.ax[d].qx[(size_t)EL(d) * NQ1 + q];
                 continue;
             }
             k -= 6 * NQ1;
-            if (k < 3) { sHP[k] = s.ax[k].hpar[e[k]]; continue; }
+            if (k < 3) {
+                if constexpr (UNI) sHP[k] = ut.hp[k];
+                else sHP[k] = s.ax[k].hpar[EL(k)];
+                continue;
+            }
             k -= 3;
-            if (k < 3 * NP1) {
+            if (k < 3 * NP1 * NP1) {
+                const int d = k / (NP1 * NP1);
+                sPosE[k] = s.ax[d].pos[(size_t)EL(d) * NP1 * NP1 + k % (NP1 * NP1)];
+                continue;
+            }
+            k -= 3 * NP1 * NP1;
+            if (k >= 3 * NP1) {
+                k -= 3 * NP1;
+                const int A = k / M, m = k - A * M;
+                int g[3];
+#pragma unroll
+                for (int d = 0; d < 3; d++) {
+                    const int aa = d == 0 ? A / (NP1 * NP1) : d == 1 ? (A / NP1) % NP1 : A % NP1;
+                    g[d] = s.ax[d].first0 + EL(d) + aa;
+                    if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
+                }
+                const long long node = local_node(s, g[0], g[1], g[2]);
+                sU[k] = U[node * M + m];
+                sUd[k] = Ud ? Ud[node * M + m] : 0.0;
+                continue;
+            }
+            {
                 const int d = k / NP1, aa = k % NP1;
-                int g = s.ax[d].first[e[d]] + aa;
+                int g = (s.ax[d].uniform ? s.ax[d].first0 + EL(d) : s.ax[d].first[EL(d)]) + aa;
                 if (g >= s.ax[d].nu) g -= s.ax[d].nu;
                 sG[k] = g;
                 sW[k] = s.ax[d].rowW[g];
                 const int l = local_fn(s.ax[d], g);
                 sS[k] = s.ax[d].lS[l];
                 sSeg[k] = l >= s.ax[d].n_own;
-                continue;
-            }
-            k -= 3 * NP1;
-            {
-                const int d = k / (NP1 * NP1);
-                sPosE[k] = s.ax[d].pos[(size_t)e[d] * NP1 * NP1 + k % (NP1 * NP1)];
             }
         }
         __syncthreads();
@@ -284,8 +310,10 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     const int k = i - NEN * NEN, A = k / M, m = k - A * M;
                     const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
                     const long long node = local_node(s, sG[a0], sG[NP1 + a1], sG[2 * NP1 + a2]);
-                    sU[k] = U[node * M + m];
-                    sUd[k] = Ud ? Ud[node * M + m] : 0.0;
+                    if (!uni_knots) {
+                        sU[k] = U[node * M + m];
+                        sUd[k] = Ud ? Ud[node * M + m] : 0.0;
+                    }
                     if (m == 0) {
                         // closed-form row start (iga_internal.cuh row_start) from the staged
                         // per-axis segment prefixes
@@ -305,37 +333,75 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         }
         __syncthreads();
 
-        // ---- 2. field kinds per (q, m) ----
+        // ---- 2. field kinds per (q, m), sum factorised over the element's functions:
+        //         Phi_k(q) = sum_a0 T0 (sum_a1 T1 (sum_a2 T2 U)) per separable term of kind k ----
         for (int task = (dbg & 4) ? NQ * M : tid; task < NQ * M; task += F::NT) {
             const int q = task / M, m = task % M;
             const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
-            double acc[NKS + 1];
+            double v0[3][NP1], v1[3][NP1], v2[3][NP1];
 #pragma unroll
-            for (int k = 0; k <= NKS; k++) acc[k] = 0.0;
+            for (int k = 0; k < 3; k++)
 #pragma unroll
-            for (int A = 0; A < NEN; A++) {
-                const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
-                double v[3][3];
-#pragma unroll
-                for (int k = 0; k < 3; k++) {
-                    v[0][k] = sTab[((0 * NQ1 + q0) * 3 + k) * NP1 + a0];
-                    v[1][k] = sTab[((1 * NQ1 + q1) * 3 + k) * NP1 + a1];
-                    v[2][k] = sTab[((2 * NQ1 + q2) * 3 + k) * NP1 + a2];
+                for (int x = 0; x < NP1; x++) {
+                    v0[k][x] = sTab[((0 * NQ1 + q0) * 3 + k) * NP1 + x];
+                    v1[k][x] = sTab[((1 * NQ1 + q1) * 3 + k) * NP1 + x];
+                    v2[k][x] = sTab[((2 * NQ1 + q2) * 3 + k) * NP1 + x];
                 }
-                const double uA = sU[A * M + m];
-                static_for<NKS>([&](auto K) {
-                    constexpr int k = decltype(K)::value;
-                    double pv = 0.0;
-                    static_for<KS::nterms(k)>([&](auto TT) {
-                        constexpr int t = decltype(TT)::value;
-                        pv += v[0][KS::ord(k, t, 0)] * v[1][KS::ord(k, t, 1)] * v[2][KS::ord(k, t, 2)];
-                    });
-                    acc[k] += uA * pv;
-                });
-                acc[NKS] += sUd[A * M + m] * v[0][0] * v[1][0] * v[2][0];
-            }
+            // stage a2: s2[a0][a1][o2] (and the Udot value, order 0 only)
+            double s2[NP1][NP1][3], d2[NP1][NP1];
 #pragma unroll
-            for (int k = 0; k <= NKS; k++) sPhi[(q * M + m) * (NKS + 1) + k] = acc[k];
+            for (int a0 = 0; a0 < NP1; a0++)
+#pragma unroll
+                for (int a1 = 0; a1 < NP1; a1++) {
+                    double u[NP1];
+#pragma unroll
+                    for (int a2 = 0; a2 < NP1; a2++) u[a2] = sU[((a0 * NP1 + a1) * NP1 + a2) * M + m];
+#pragma unroll
+                    for (int o = 0; o < 3; o++) {
+                        double t = 0.0;
+#pragma unroll
+                        for (int a2 = 0; a2 < NP1; a2++) t += v2[o][a2] * u[a2];
+                        s2[a0][a1][o] = t;
+                    }
+                    double t = 0.0;
+#pragma unroll
+                    for (int a2 = 0; a2 < NP1; a2++) t += v2[0][a2] * sUd[((a0 * NP1 + a1) * NP1 + a2) * M + m];
+                    d2[a0][a1] = t;
+                }
+            // stage a1: s1[a0][o1][o2] (unused order pairs are dead code)
+            double s1[NP1][3][3], d1[NP1];
+#pragma unroll
+            for (int a0 = 0; a0 < NP1; a0++) {
+#pragma unroll
+                for (int o1 = 0; o1 < 3; o1++)
+#pragma unroll
+                    for (int o2 = 0; o2 < 3; o2++) {
+                        double t = 0.0;
+#pragma unroll
+                        for (int a1 = 0; a1 < NP1; a1++) t += v1[o1][a1] * s2[a0][a1][o2];
+                        s1[a0][o1][o2] = t;
+                    }
+                double t = 0.0;
+#pragma unroll
+                for (int a1 = 0; a1 < NP1; a1++) t += v1[0][a1] * d2[a0][a1];
+                d1[a0] = t;
+            }
+            double *dst = sPhi + (q * M + m) * (NKS + 1);
+            static_for<NKS>([&](auto K) {
+                constexpr int k = decltype(K)::value;
+                double pv = 0.0;
+                static_for<KS::nterms(k)>([&](auto TT) {
+                    constexpr int t = decltype(TT)::value;
+                    constexpr int o0 = KS::ord(k, t, 0), o1 = KS::ord(k, t, 1), o2 = KS::ord(k, t, 2);
+#pragma unroll
+                    for (int a0 = 0; a0 < NP1; a0++) pv += v0[o0][a0] * s1[a0][o1][o2];
+                });
+                dst[k] = pv;
+            });
+            double pt = 0.0;
+#pragma unroll
+            for (int a0 = 0; a0 < NP1; a0++) pt += v0[0][a0] * d1[a0];
+            dst[NKS] = pt;
         }
         __syncthreads();
 
@@ -384,16 +450,17 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
         // ---- 4. Jacobian coefficients: warp-uniform trial column (k2 = qk(kq), j), lane = q ----
         if constexpr (JAC) {
-            for (int kj = (dbg & 16) ? NQK * M : warp; kj < NQK * M; kj += F::NWARP) {
-                if (lane < NQ) {
-                    const int q = lane;
-                    const State st = sSt[q];
-                    const double dV = sDV[q];
-                    double chk = 0.0;
+            // warp w owns the columns kj = w, w + NWARP, ...: the state stays in registers
+            if (lane < NQ && !(dbg & 16)) {
+                const int q = lane;
+                const State st = sSt[q];
+                const double dV = sDV[q];
+                double chk = 0.0;
+                {
                     static_for<NQK * M>([&](auto KJ) {
                         constexpr int kq = decltype(KJ)::value / M, j = decltype(KJ)::value % M;
                         constexpr int k2 = L::qk(kq);
-                        if (kj == decltype(KJ)::value) {
+                        if (warp == decltype(KJ)::value % F::NWARP) {
                             double col[NKS * M];
                             PH::template dcol<3>(st, k2, j, a, b, col);
 #pragma unroll
@@ -438,30 +505,46 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 }
             }
         }
-        // ---- 6. residual F_e[A, i], thread = (A, i) (q fully unrolled) ----
-        if (Fout && tid < NEN * M && !(dbg & 32)) {
-            const int A = tid / M, Ii = tid - A * M;
+        // ---- 6. residual F_e[A, i]: warp = component i (warp-uniform), lane = A; sum
+        //         factorised per test kind: sum_q0 T0 (sum_q1 T1 (sum_q2 T2 r(q))) ----
+        if (Fout && warp < M && lane < NEN && !(dbg & 32)) {
+            const int A = lane;
             const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
+            double t0[NQ1][3], t1[NQ1][3], t2[NQ1][3];
+#pragma unroll
+            for (int q = 0; q < NQ1; q++)
+#pragma unroll
+                for (int k = 0; k < 3; k++) {
+                    t0[q][k] = sTab[((0 * NQ1 + q) * 3 + k) * NP1 + a0];
+                    t1[q][k] = sTab[((1 * NQ1 + q) * 3 + k) * NP1 + a1];
+                    t2[q][k] = sTab[((2 * NQ1 + q) * 3 + k) * NP1 + a2];
+                }
             static_for<M>([&](auto II) {
                 constexpr int I = decltype(II)::value;
-                if (Ii == I) {
+                if (warp == I) {
                     double acc = 0.0;
-                    static_for<NQ>([&](auto QQ) {
-                        constexpr int q = decltype(QQ)::value;
-                        constexpr int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
-                        static_for<NR>([&](auto RR) {
-                            constexpr int rr = decltype(RR)::value;
-                            constexpr int c = L::R.c[rr];
-                            if constexpr (L::R.i[rr] == I) {
-                                double pv = 0.0;
-                                static_for<KS::nterms(c)>([&](auto TT) {
-                                    constexpr int t = decltype(TT)::value;
-                                    pv += TB(0, q0, KS::ord(c, t, 0), a0) * TB(1, q1, KS::ord(c, t, 1), a1)
-                                          * TB(2, q2, KS::ord(c, t, 2), a2);
-                                });
-                                acc += pv * sR[rr * NQ + q];
-                            }
-                        });
+                    static_for<NR>([&](auto RR) {
+                        constexpr int rr = decltype(RR)::value;
+                        constexpr int c = L::R.c[rr];
+                        if constexpr (L::R.i[rr] == I) {
+                            static_for<KS::nterms(c)>([&](auto TT) {
+                                constexpr int t = decltype(TT)::value;
+                                constexpr int o0 = KS::ord(c, t, 0), o1 = KS::ord(c, t, 1), o2 = KS::ord(c, t, 2);
+#pragma unroll
+                                for (int q0 = 0; q0 < NQ1; q0++) {
+                                    double s1 = 0.0;
+#pragma unroll
+                                    for (int q1 = 0; q1 < NQ1; q1++) {
+                                        double s2 = 0.0;
+#pragma unroll
+                                        for (int q2 = 0; q2 < NQ1; q2++)
+                                            s2 += t2[q2][o2] * sR[rr * NQ + (q0 * NQ1 + q1) * NQ1 + q2];
+                                        s1 += t1[q1][o1] * s2;
+                                    }
+                                    acc += t0[q0][o0] * s1;
+                                }
+                            });
+                        }
                     });
                     atomicAdd(Fout + sNode[A] * M + I, acc);
                 }

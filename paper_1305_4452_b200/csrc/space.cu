@@ -504,6 +504,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             if ((st = upload(s, (long long **)&ax.lS, zl)) != IGA_OK) goto fail;
             ax.n_own = 1; ax.x_n = 1; ax.Th = 0;
             ax.uniform = 1;
+            ax.first0 = 0;
             ax.colmax = 1; ax.T = 1; ax.own_lo = 0; ax.own_hi = 1; ax.el_lo = 0; ax.el_hi = 1;
             s->own_lo[a] = 0; s->own_hi[a] = 1; s->el_lo[a] = 0; s->el_hi[a] = 1;
             continue;
@@ -551,6 +552,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         if ((st = upload(s, (long long **)&ax.lS, lS)) != IGA_OK) goto fail;
         ax.n_own = n_own; ax.x_n = n_own + halo; ax.Th = Th;
         ax.uniform = uniform;
+        ax.first0 = first.empty() ? 0 : first[0];
         if ((st = dalloc(s, &dtab, (size_t)nel * nq * 3 * (p + 1))) != IGA_OK) goto fail;
         {
             const int nt = nel * nq;
