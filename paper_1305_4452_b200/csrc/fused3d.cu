@@ -60,8 +60,7 @@ struct F3 {
     static constexpr int O_PHI = O_D;                        // [NQ][M][NKS+1]  overlays D (dead before D)
     static constexpr int O_RS = O_D + NQ * DQS;              // long long [NEN*M] row starts
     static constexpr int O_ND = O_RS + NEN * M;              // long long [NEN] nodes
-    static constexpr int O_CO = O_ND + NEN;                  // int [NEN][NEN] column offsets (in nodes)
-    static constexpr size_t SMEM = (size_t)O_CO * sizeof(double) + (size_t)NEN * NEN * sizeof(int);
+    static constexpr size_t SMEM = (size_t)(O_ND + NEN) * sizeof(double);
     static_assert(NQ * M * (NKS + 1) <= NQ * DQS, "Phi must fit in the D region");
 };
 
@@ -201,7 +200,7 @@ template <int P, class PH, bool JAC, bool UNI>
 __global__ void __launch_bounds__(F3<P, PH>::NT, 2)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
-          int dbg) {
+          int dbg, int bw) {
     using F = F3<P, PH>;
     using L = typename F::L;
     using KS = typename F::KS;
@@ -217,12 +216,11 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     // 8-byte aligned) so the scatter below addresses everything from the uniform `val` register.
     long long *sRS = reinterpret_cast<long long *>(sm + F::O_RS);
     long long *sNode = reinterpret_cast<long long *>(sm + F::O_ND); // [NEN] touched-box node of A
-    int *sCO = reinterpret_cast<int *>(sm + F::O_CO);               // [NEN][NEN] column offset (nodes)
     __shared__ int sG[3 * NP1], sW[3 * NP1], sPosE[3 * NP1 * NP1], sSeg[3 * NP1];
     __shared__ long long sS[3 * NP1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     int errbits = 0;
-    const int n1 = s.ax[1].el_hi - s.ax[1].el_lo, n2 = s.ax[2].el_hi - s.ax[2].el_lo;
+    const int n0 = s.ax[0].el_hi - s.ax[0].el_lo, n1 = s.ax[1].el_hi - s.ax[1].el_lo, n2 = s.ax[2].el_hi - s.ax[2].el_lo;
     auto TB = [&](int d, int q, int k, int aa) -> double {
         if constexpr (UNI) return ut.t[d][q][k][aa];
         else return sTab[((d * NQ1 + q) * 3 + k) * NP1 + aa];
@@ -230,12 +228,20 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
     const bool uni_knots = s.ax[0].uniform && s.ax[1].uniform && s.ax[2].uniform;
     for (long long el = blockIdx.x; el < nelem; el += gridDim.x) {
+        // L2-blocked element order: pencils along axis 2, swept over axis 0 inside blocks of `bw`
+        // pencils along axis 1, so the CSR rows an element layer leaves half-accumulated are
+        // still in L2 when the next layer adds to them (the red.add scatter then reads each
+        // row from HBM about once)
         int e[3];
         {
-            long long r = el;
-            e[2] = s.ax[2].el_lo + (int)(r % n2); r /= n2;
-            e[1] = s.ax[1].el_lo + (int)(r % n1); r /= n1;
-            e[0] = s.ax[0].el_lo + (int)r;
+            const long long r = el / n2;
+            e[2] = s.ax[2].el_lo + (int)(el - r * n2);
+            const long long blk = (long long)n0 * bw;
+            const int e1b = (int)(r / blk);
+            const int bwe = min(bw, n1 - e1b * bw);
+            const int rem = (int)(r - e1b * blk);
+            e[0] = s.ax[0].el_lo + rem / bwe;
+            e[1] = s.ax[1].el_lo + e1b * bw + rem % bwe;
         }
         auto EL = [&](int d) { return d == 0 ? e[0] : (d == 1 ? e[1] : e[2]); };   // no local-memory indexing
         // ---- 1. stage: tables, per-axis function data, position tables, and (uniform knots:
@@ -299,15 +305,9 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         }
         __syncthreads();
         {
-            for (int i = tid; i < NEN * NEN + NEN * M; i += F::NT) {
-                if (i < NEN * NEN) {
-                    const int A = i / NEN, B = i - A * NEN;
-                    const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
-                    const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
-                    sCO[i] = (sPosE[a0 * NP1 + b0] * sW[NP1 + a1] + sPosE[NP1 * NP1 + a1 * NP1 + b1]) * sW[2 * NP1 + a2]
-                             + sPosE[2 * NP1 * NP1 + a2 * NP1 + b2];
-                } else {
-                    const int k = i - NEN * NEN, A = k / M, m = k - A * M;
+            for (int i = tid; i < NEN * M; i += F::NT) {
+                {
+                    const int k = i, A = k / M, m = k - A * M;
                     const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
                     const long long node = local_node(s, sG[a0], sG[NP1 + a1], sG[2 * NP1 + a2]);
                     if (!uni_knots) {
@@ -493,9 +493,23 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         for (int A = 0; A < NEN; A++) Kc[A] = sD[A * 7 + J];
                     }
                     if (!(dbg & 2)) {
+                        // column offset of (A, B) in row A: closed form of the per-axis Alg. 3
+                        // positions, ((pos0 W1 + pos1) W2 + pos2) (in nodes)
+                        int P0[NP1], P1[NP1], P2[NP1], W1[NP1], W2[NP1];
 #pragma unroll
-                        for (int A = 0; A < NEN; A++)
-                            atomicAdd(val + sRS[A * M + I] + (long long)sCO[A * NEN + B] * M + J, Kc[A]);
+                        for (int x = 0; x < NP1; x++) {
+                            P0[x] = sPosE[x * NP1 + b0];
+                            P1[x] = sPosE[NP1 * NP1 + x * NP1 + b1];
+                            P2[x] = sPosE[2 * NP1 * NP1 + x * NP1 + b2];
+                            W1[x] = sW[NP1 + x];
+                            W2[x] = sW[2 * NP1 + x];
+                        }
+#pragma unroll
+                        for (int A = 0; A < NEN; A++) {
+                            const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
+                            const int co = (P0[a0] * W1[a1] + P1[a1]) * W2[a2] + P2[a2];
+                            atomicAdd(val + sRS[A * M + I] + (long long)co * M + J, Kc[A]);
+                        }
                     } else {
                         double sum = 0.0;
 #pragma unroll
@@ -588,8 +602,14 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
     if (F) { ProfScope ps(s, "k_zero", st); k_zero_vec(F, s->nrows_owned, st, nsm); launches++; }
     {
         ProfScope ps(s, "k_fused3d", st);
-        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg);
-        else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg);
+        // block width: ~3 element layers of a block's rows (values, m^2 (2p+1)^3 per node) in half the L2
+        const int ne1 = s->el_hi[1] - s->el_lo[1], ne2 = s->el_hi[2] - s->el_lo[2];
+        const double row_bytes = 8.0 * FF::M * FF::M * (2 * P + 1) * (2 * P + 1) * (2 * P + 1);
+        int bw = (int)(60e6 / (3.0 * (ne2 + P) * row_bytes)) - P;
+        if (s->bw_opt > 0) bw = s->bw_opt;
+        bw = std::max(1, std::min(bw, ne1));
+        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
+        else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
         launches++;
     }
     s->last_launches = launches;

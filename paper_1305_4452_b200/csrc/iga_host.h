@@ -46,6 +46,7 @@ struct iga_space_s {
     int last_launches = 0;
     int force_split = 0;
     int force_general = 0;
+    int bw_opt = 0;                      // 3D element-order block width override (0: from the L2 size)
     int last_occupancy = 0;
     int dbg = 0;                         // experiment bits (bench A/B only; results invalid when set)               // 1: never use the uniform-table fast paths
     // per axis: all elements share the same 1D tables / weights / span length (uniform knots,
