@@ -114,6 +114,12 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
             double n1[3];
 #pragma unroll
             for (int k = 0; k < 3; k++) n1[k] = TS(1, q1, k, b1);
+            // trial 2D products n0[o0] n1[o1] once per (q0, q1) (unused orders are dead code)
+            double n01[3][3];
+#pragma unroll
+            for (int o0 = 0; o0 < 3; o0++)
+#pragma unroll
+                for (int o1 = 0; o1 < 3; o1++) n01[o0][o1] = n0[o0] * n1[o1];
             double S[3][3][NP1];
 #pragma unroll
             for (int o = 0; o < 3; o++)
@@ -134,7 +140,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
                     double v = 0.0;
                     static_for<KS::nterms(c)>([&](auto TT) {
                         constexpr int s = decltype(TT)::value;
-                        v += n0[KS::ord(c, s, 0)] * n1[KS::ord(c, s, 1)] * n2[KS::ord(c, s, 2)];
+                        v += n01[KS::ord(c, s, 0)][KS::ord(c, s, 1)] * n2[KS::ord(c, s, 2)];
                     });
                     pb[kq] = v;
                 });
