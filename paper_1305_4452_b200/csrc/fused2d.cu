@@ -21,9 +21,10 @@
 namespace iga {
 
 template <int P> struct Tile2 {
-    static constexpr int TE0 = P == 3 ? 8 : 16;
+    static constexpr int TE0 = 16;
     static constexpr int TE1 = 16;
-    static constexpr int NWARP = 12;                          // 384 threads (168 regs), 1 CTA / SM
+    // p = 2 (9-lane groups, 120 regs) runs 16 warps; p = 3 (16-lane groups, NURBS) needs 168 regs -> 12
+    static constexpr int NWARP = P == 3 ? 12 : 16;
     static constexpr int NB0 = TE0 + P, NB1 = TE1 + P;      // touched node box (uniform knots)
     static constexpr int NSL = (2 * P + 1) * (2 * P + 1);   // stencil slots per row
 };
