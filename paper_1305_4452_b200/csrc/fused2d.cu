@@ -146,7 +146,8 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
     }
 }
 
-template <int P, class PH, int MODE, bool JAC, bool UNI>
+// UNI: 0 general tables, 1 uniform runs checked per element, 2 every element uniform
+template <int P, class PH, int MODE, bool JAC, int UNI>
 __global__ void __launch_bounds__(32 * Tile2<P>::NWARP, 1)
 k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1,
@@ -330,7 +331,14 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 // (3) Jacobian column B = t
                 if constexpr (JAC) {
                     double Kc[NEN];
-                    tsf_column_2d<L, KS, P, UNI>(Kc, gs, tb0, tb1, c0, c1, ut);
+                    // elements inside both axes' uniform runs take the constant-operand tables
+                    const int ge0 = e0lo + le0, ge1 = e1lo + le1;
+                    if constexpr (UNI == 2)
+                        tsf_column_2d<L, KS, P, true>(Kc, gs, tb0, tb1, c0, c1, ut);
+                    else if (UNI == 1 && ge0 >= A0.uni_lo && ge0 < A0.uni_hi && ge1 >= A1.uni_lo && ge1 < A1.uni_hi)
+                        tsf_column_2d<L, KS, P, true>(Kc, gs, tb0, tb1, c0, c1, ut);
+                    else
+                        tsf_column_2d<L, KS, P, false>(Kc, gs, tb0, tb1, c0, c1, ut);
 #pragma unroll
                     for (int A = 0; A < NEN; A++) {
                         const int a0 = A / NP1, a1 = A % NP1;
@@ -389,7 +397,7 @@ static size_t fused2d_smem(bool jac) {
     return n * sizeof(double) + (size_t)NBN * 16 + (size_t)(TL::NB0 + TL::NB1) * (2 * P + 1) * sizeof(int);
 }
 
-template <int P, class PH, int MODE, bool JAC, bool UNI>
+template <int P, class PH, int MODE, bool JAC, int UNI>
 static iga_status launch_k2(iga_space_s *s, const Prm &prm, double a, double b, const double *U, const double *Ud,
                             double *val, double *F, int nt0, int nt1, const UniTab2<P> &ut, cudaStream_t st, int nsm) {
     using TL = Tile2<P>;
@@ -420,7 +428,10 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
     const bool jac = val != nullptr;
     const int ne0 = s->el_hi[0] - s->el_lo[0], ne1 = s->el_hi[1] - s->el_lo[1];
     const int nt0 = (ne0 + TL::TE0 - 1) / TL::TE0, nt1 = (ne1 + TL::TE1 - 1) / TL::TE1;
-    const bool uni = s->tab_uniform[0] && s->tab_uniform[1] && !s->force_general;
+    // fast path whenever both axes have a uniform run (all elements on periodic knots, all but p at
+    // each end on open uniform knots); the kernel checks each element against the runs
+    const bool runs = s->dev.ax[0].uni_hi > s->dev.ax[0].uni_lo && s->dev.ax[1].uni_hi > s->dev.ax[1].uni_lo;
+    const int uni = s->force_general ? 0 : (s->tab_uniform[0] && s->tab_uniform[1]) ? 2 : runs ? 1 : 0;
     UniTab2<P> ut{};
     if (uni)
         for (int d = 0; d < 2; d++)
@@ -439,10 +450,10 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
         launches++;
     }
     iga_status r;
-    if (jac) r = uni ? launch_k2<P, PH, MODE, true, true>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
-                     : launch_k2<P, PH, MODE, true, false>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
-    else r = uni ? launch_k2<P, PH, MODE, false, true>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
-                 : launch_k2<P, PH, MODE, false, false>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
+    if (jac) r = uni == 2 ? launch_k2<P, PH, MODE, true, 2>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
+               : uni == 1 ? launch_k2<P, PH, MODE, true, 1>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
+                          : launch_k2<P, PH, MODE, true, 0>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
+    else r = launch_k2<P, PH, MODE, false, 0>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
     if (r != IGA_OK) return r;
     launches++;
     s->last_launches = launches;

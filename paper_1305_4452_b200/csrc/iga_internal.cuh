@@ -40,6 +40,7 @@ struct AxisDev {
     const int *posd;          // [nu][2p+1] position of column g+delta in row g's list, or -1
     int uniform;              // first[e+1] == first[e] + 1 for all e (simple interior knots)
     int first0;               // first[0] (uniform: first[e] = first0 + e)
+    int uni_lo, uni_hi;       // elements [uni_lo, uni_hi) share the middle element's 1D tables
     // touched box of this rank (box decomposition): local index l = g - own_lo
     // (mod nu) in [0, x_n); l < n_own are owned functions, the next x_n - n_own are the halo
     // (owned by the upper neighbour).  Single rank: own_lo = 0, n_own = x_n = nu.

@@ -503,6 +503,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             if ((st = upload(s, (int **)&ax.posd, z)) != IGA_OK) goto fail;
             if ((st = upload(s, (long long **)&ax.lS, zl)) != IGA_OK) goto fail;
             ax.n_own = 1; ax.x_n = 1; ax.Th = 0;
+            ax.uni_lo = 0; ax.uni_hi = 1;
             ax.uniform = 1;
             ax.first0 = 0;
             ax.colmax = 1; ax.T = 1; ax.own_lo = 0; ax.own_hi = 1; ax.el_lo = 0; ax.el_hi = 1;
@@ -562,24 +563,34 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         }
         ax.tab = dtab;
         {
-            // uniform-table detection (element-0 tables reused by the fused kernels' fast path)
+            // uniform-table detection: the maximal run of elements around the middle one whose 1D
+            // tables, Gauss weights and span lengths equal the middle element's (all of them on
+            // periodic / uniform knots; all but p at each end on open uniform knots).  The fused
+            // kernels' fast path uses the middle element's tables for elements of that run.
             std::vector<double> ht((size_t)nel * nq * 3 * (p + 1));
             CUDA_TRY(cudaMemcpy(ht.data(), dtab, ht.size() * sizeof(double), cudaMemcpyDeviceToHost));
             const size_t per = (size_t)nq * 3 * (p + 1);
+            const int em = nel / 2;
             double mx = 0.0;
-            for (size_t k = 0; k < per; k++) mx = std::max(mx, std::fabs(ht[k]));
-            bool uni = true;
-            for (int e = 1; e < nel && uni; e++) {
+            for (size_t k = 0; k < per; k++) mx = std::max(mx, std::fabs(ht[em * per + k]));
+            auto same = [&](int e) {
                 for (size_t k = 0; k < per; k++)
-                    if (std::fabs(ht[e * per + k] - ht[k]) > 1e-13 * mx) { uni = false; break; }
-                for (int q = 0; q < nq && uni; q++)
-                    if (std::fabs(qw[(size_t)e * nq + q] - qw[q]) > 1e-14 * std::fabs(qw[q])) uni = false;
-                if (std::fabs(hpar[e] - hpar[0]) > 1e-14 * hpar[0]) uni = false;
-            }
+                    if (std::fabs(ht[e * per + k] - ht[em * per + k]) > 1e-13 * mx) return false;
+                for (int q = 0; q < nq; q++)
+                    if (std::fabs(qw[(size_t)e * nq + q] - qw[(size_t)em * nq + q]) > 1e-14 * std::fabs(qw[(size_t)em * nq + q]))
+                        return false;
+                return std::fabs(hpar[e] - hpar[em]) <= 1e-14 * hpar[em];
+            };
+            int ilo = em, ihi = em + 1;
+            while (ilo > 0 && same(ilo - 1)) ilo--;
+            while (ihi < nel && same(ihi)) ihi++;
+            const bool uni = ilo == 0 && ihi == nel;
+            ax.uni_lo = ilo;
+            ax.uni_hi = ihi;
+            s->tab0[a].assign(ht.begin() + em * per, ht.begin() + (em + 1) * per);
+            s->qw0[a].assign(qw.begin() + (size_t)em * nq, qw.begin() + (size_t)(em + 1) * nq);
+            s->hp0[a] = hpar[em];
             s->tab_uniform[a] = uni ? 1 : 0;
-            s->tab0[a].assign(ht.begin(), ht.begin() + per);
-            s->qw0[a].assign(qw.begin(), qw.begin() + nq);
-            s->hp0[a] = hpar[0];
         }
         nnodes *= nu;
         nrows_nodes *= (own_hi - own_lo);
