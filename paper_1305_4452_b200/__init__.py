@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libiga.so")
+# IGA_LIB: an alternative build of the same library (A/B experiments); default the in-tree one
+LIB_PATH = os.environ.get("IGA_LIB", os.path.join(_HERE, "libiga.so"))
 
 PHYS_LAPLACE, PHYS_CAHN_HILLIARD, PHYS_NEOHOOKE, PHYS_NS_VMS = 0, 1, 2, 3
 GEOM_PARAMETRIC, GEOM_NURBS = 0, 1

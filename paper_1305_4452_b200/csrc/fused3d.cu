@@ -109,7 +109,9 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
             for (int x = 0; x < NP1; x++)
 #pragma unroll
                 for (int y = 0; y < NP1; y++) Tt[o][x][y] = 0.0;
-#pragma unroll
+        // VMS (m = 4) keeps the q1 loop rolled: fully unrolled it spills at 255 registers
+        constexpr int UNROLL_Q1 = F::M >= 4 ? 1 : NQ1;
+#pragma unroll UNROLL_Q1
         for (int q1 = 0; q1 < NQ1; q1++) {
             double n1[3];
 #pragma unroll
@@ -144,21 +146,17 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
                     });
                     pb[kq] = v;
                 });
+                // H[t] = sum_k D[k][t] pb[k]: block rows (trial kind k) streamed 16 bytes at a time
                 const double2 *Dq2 = reinterpret_cast<const double2 *>(Dsm + q * F::DQS + ij * DB);
-                double dd[DB];
+                double H[NTK];
+#pragma unroll
+                for (int t = 0; t < NTK; t++) H[t] = 0.0;
 #pragma unroll
                 for (int x = 0; x < DB / 2; x++) {
                     const double2 v2 = Dq2[x];
-                    dd[2 * x] = v2.x;
-                    dd[2 * x + 1] = v2.y;
-                }
-                double H[NTK];
-#pragma unroll
-                for (int t = 0; t < NTK; t++) {
-                    double h = 0.0;
-#pragma unroll
-                    for (int k = 0; k < NQK; k++) h += dd[t * NQK + k] * pb[k];
-                    H[t] = h;
+                    const int e0 = 2 * x, e1 = 2 * x + 1;
+                    if (e0 < NTK * NQK) H[e0 % NTK] += v2.x * pb[e0 / NTK];
+                    if (e1 < NTK * NQK) H[e1 % NTK] += v2.y * pb[e1 / NTK];
                 }
                 static_for<NTK>([&](auto TK) {
                     constexpr int t = decltype(TK)::value;
@@ -471,13 +469,23 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                             PH::template dcol<3>(st, k2, j, a, b, col);
 #pragma unroll
                             for (int i = 0; i < M; i++) {
-                                double *dst = sD + q * F::DQS + (i * M + j) * DB + kq;
+                                // block layout [trial kind k][test kind t]: this column's NTK entries
+                                // are contiguous (16-byte stores when NTK is even)
+                                double *dst = sD + q * F::DQS + (i * M + j) * DB + kq * NTK;
+                                double v[NTK];
                                 static_for<NTK>([&](auto TK) {
                                     constexpr int t = decltype(TK)::value;
-                                    const double v = col[L::tk(t) * M + i] * dV;
-                                    chk += v;
-                                    dst[t * NQK] = v;
+                                    v[t] = col[L::tk(t) * M + i] * dV;
+                                    chk += v[t];
                                 });
+                                if constexpr (NTK % 2 == 0 && (NTK * 8) % 16 == 0) {
+#pragma unroll
+                                    for (int t = 0; t < NTK; t += 2)
+                                        *reinterpret_cast<double2 *>(dst + t) = make_double2(v[t], v[t + 1]);
+                                } else {
+#pragma unroll
+                                    for (int t = 0; t < NTK; t++) dst[t] = v[t];
+                                }
                             }
                         }
                     });
