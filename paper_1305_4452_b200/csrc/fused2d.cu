@@ -29,14 +29,6 @@ template <int P> struct Tile2 {
     static constexpr int NSL = (2 * P + 1) * (2 * P + 1);   // stencil slots per row
 };
 
-// per axis: is function g (unique) complete in the tile's element range [elo, elo + TE) (all
-// support elements inside; the cyclic support of a wrapped periodic function never is)
-__device__ __forceinline__ bool complete_axis(const AxisDev &ax, int g, int elo, int TE) {
-    const int lo = ax.suplo[g], c = ax.supcnt[g];
-    const int hi = lo + c - 1;
-    return hi < ax.nel && lo >= elo && hi < elo + TE;
-}
-
 // element's nodes in the tile box: local function A = (a0, a1) -> box index base + a0*NB1 + a1
 template <int NP1, int NB1>
 struct SmemNodes2 {
@@ -164,19 +156,17 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     constexpr int SCR = (JAC ? NE : 0) + NR;
 
     extern __shared__ __align__(16) double sm[];
-    double *rows = sm;                                  // [NBN][NSL]
-    double *Fb = rows + (JAC ? NBN * NSL : 0);          // [NBN]
-    double *nU = Fb + NBN, *nUd = nU + NBN, *nw = nUd + NBN, *nx0 = nw + NBN, *nx1 = nx0 + NBN;
+    double *nU = sm, *nUd = nU + NBN, *nw = nUd + NBN, *nx0 = nw + NBN, *nx1 = nx0 + NBN;
     double *tb = nx1 + NBN;                             // [2][TE][NQ1][3][NP1]
     double *qwb = tb + 2 * TL::TE1 * NQ1 * 3 * NP1;      // [2][TE][NQ1]  weights
     double *qxb = qwb + 2 * TL::TE1 * NQ1;              // [2][TE][NQ1]  coordinates
     double *hpb = qxb + 2 * TL::TE1 * NQ1;              // [2][TE]
     double *scr = hpb + 2 * TL::TE1;                    // [NGRP][SCR][NQ]
-    // write-out metadata of the tile's rows (computed once per node, not per entry)
+    // scatter metadata of the tile's rows (computed once per node, not per entry)
     long long *rowOff = reinterpret_cast<long long *>(scr + (size_t)NGRP * SCR * NQ);   // [NBN] CSR row start - val
-    int *rowW1 = reinterpret_cast<int *>(rowOff + NBN);     // [NBN] Alg. 3 width along axis 1
-    int *rowSt = rowW1 + NBN;                               // [NBN] -1 outside / 0 boundary (red.add) / 1 complete
-    int *pd0 = rowSt + NBN;                                 // [NB0][W2] position of column g0+delta in row g0
+    long long *fIdx = rowOff + NBN;                         // [NBN] residual entry of the node
+    int *rowW1 = reinterpret_cast<int *>(fIdx + NBN);       // [NBN] Alg. 3 width along axis 1
+    int *pd0 = rowW1 + NBN;                                 // [NB0][W2] position of column g0+delta in row g0
     int *pd1 = pd0 + NB0 * W2;                              // [NB1][W2]
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -185,7 +175,6 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     const int grp = warp * GPW + (lane_ok ? grp_in_warp : 0);
     double *gs = scr + (size_t)grp * SCR * NQ;
     const AxisDev &A0 = s.ax[0], &A1 = s.ax[1];
-    const int TEd[2] = {TL::TE0, TL::TE1};
     int errbits = 0;
 
     for (int tile = blockIdx.x; tile < ntile0 * ntile1; tile += gridDim.x) {
@@ -194,19 +183,16 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         const int ne0 = min(TL::TE0, A0.el_hi - e0lo), ne1 = min(TL::TE1, A1.el_hi - e1lo);
         const int F00 = A0.first[e0lo], F01 = A1.first[e1lo];
         const int nb0 = ne0 + P, nb1 = ne1 + P;
-        // ---- stage the tile: zero rows/F, node data, tables ----
-        if (JAC)
-            for (int i = tid; i < NBN * NSL; i += blockDim.x) rows[i] = 0.0;
+        // ---- stage the tile: node data, scatter metadata, tables ----
         for (int i = tid; i < NBN; i += blockDim.x) {
-            Fb[i] = 0.0;
             const int l0 = i / NB1, l1 = i % NB1;
-            int st = -1;
             if (l0 < nb0 && l1 < nb1) {
                 int g0 = F00 + l0, g1 = F01 + l1;
                 if (g0 >= A0.nu) g0 -= A0.nu;
                 if (g1 >= A1.nu) g1 -= A1.nu;
                 const long long node = (long long)g0 * A1.nu + g1;             // geometry: global
                 const long long lnode = local_node(s, g0, g1, 0);               // fields: touched box
+                fIdx[i] = lnode;
                 nU[i] = U[lnode];
                 nUd[i] = Ud ? Ud[lnode] : 0.0;
                 nw[i] = s.wts ? s.wts[node] : 1.0;
@@ -224,14 +210,8 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         off += ((long long)(uintptr_t)(s.halo + s.hbase[(sg0 * 2 + sg1) * 2]) - (long long)(uintptr_t)val) / 8;
                     rowOff[i] = off;
                     rowW1[i] = A1.rowW[g1];
-                    // complete = every support element inside this tile and the row appears once in
-                    // the tile box (small periodic meshes wrap the box onto itself) -> plain store;
-                    // otherwise red.add of the partial sums
-                    const bool uniq = (l0 < A0.nu && l0 + A0.nu >= nb0) && (l1 < A1.nu && l1 + A1.nu >= nb1);
-                    st = (uniq && complete_axis(A0, g0, e0lo, TEd[0]) && complete_axis(A1, g1, e1lo, TEd[1])) ? 1 : 0;
                 }
             }
-            if (JAC) rowSt[i] = st;
         }
         if (JAC) {
             for (int i = tid; i < (NB0 + NB1) * W2; i += blockDim.x) {
@@ -326,7 +306,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                             acc += pv * Rg[rr * NQ + q];
                         });
                     }
-                    atomicAdd(Fb + nidx, sw * acc);
+                    atomicAdd(Fout + fIdx[nidx], sw * acc);           // red.global (no return value)
                 }
                 // (3) Jacobian column B = t
                 if constexpr (JAC) {
@@ -339,45 +319,20 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         tsf_column_2d<L, KS, P, true>(Kc, gs, tb0, tb1, c0, c1, ut);
                     else
                         tsf_column_2d<L, KS, P, false>(Kc, gs, tb0, tb1, c0, c1, ut);
+                    // column B of the element block straight into the CSR rows with red.global.add
+                    // (fire-and-forget; rows of a tile stay L2-resident): entry (A, B) at
+                    // rowOff(A) + pos0(a0 -> b0) W1(A) + pos1(a1 -> b1)
 #pragma unroll
                     for (int A = 0; A < NEN; A++) {
                         const int a0 = A / NP1, a1 = A % NP1;
                         const int ridx = (fo0 + a0) * NB1 + fo1 + a1;
                         const double sa = s.wts ? nw[ridx] : 1.0;
-                        const int slot = (c0 - a0 + P) * W2 + (c1 - a1 + P);
-                        atomicAdd(rows + ridx * NSL + slot, sa * sw * Kc[A]);
+                        const int p0 = pd0[(fo0 + a0) * W2 + c0 - a0 + P], p1 = pd1[(fo1 + a1) * W2 + c1 - a1 + P];
+                        atomicAdd(val + rowOff[ridx] + (long long)p0 * rowW1[ridx] + p1, sa * sw * Kc[A]);
                     }
                 }
             }
             __syncwarp();
-        }
-        __syncthreads();
-
-        // ---- write-out: complete rows with plain stores, boundary rows with red.add ----
-        if (JAC) {
-            for (int i = tid; i < NBN * NSL; i += blockDim.x) {
-                const int node = i / NSL, slot = i - node * NSL;
-                const int st = rowSt[node];
-                if (st < 0) continue;
-                const int l0 = node / NB1, l1 = node - l0 * NB1;
-                const int d0 = slot / W2, d1 = slot - d0 * W2;
-                const int p0 = pd0[l0 * W2 + d0], p1 = pd1[l1 * W2 + d1];
-                if (p0 < 0 || p1 < 0) continue;
-                double *dst = val + rowOff[node] + (long long)p0 * rowW1[node] + p1;
-                const double vv = rows[i];
-                if (st) *dst = vv;
-                else if (vv != 0.0) atomicAdd(dst, vv);
-            }
-        }
-        if (Fout) {
-            for (int i = tid; i < NBN; i += blockDim.x) {
-                const int l0 = i / NB1, l1 = i % NB1;
-                if (l0 >= nb0 || l1 >= nb1) continue;
-                int g0 = F00 + l0, g1 = F01 + l1;
-                if (g0 >= A0.nu) g0 -= A0.nu;
-                if (g1 >= A1.nu) g1 -= A1.nu;
-                if (Fb[i] != 0.0) atomicAdd(Fout + local_node(s, g0, g1, 0), Fb[i]);
-            }
         }
         __syncthreads();
     }
@@ -391,10 +346,10 @@ static size_t fused2d_smem(bool jac) {
     constexpr int NQ1 = P + 1, NP1 = P + 1, NQ = NQ1 * NQ1;
     constexpr int NGRP = TL::NWARP * (32 / (NP1 * NP1));
     const int NBN = TL::NB0 * TL::NB1;
-    size_t n = (jac ? (size_t)NBN * TL::NSL : 0) + 6 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
+    size_t n = 5 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
                + 2 * TL::TE1 + (size_t)NGRP * ((jac ? L::NE : 0) + L::NR) * NQ;
-    // row metadata: rowOff (8 B) + rowW1, rowSt (4 B each) per node, posd tables
-    return n * sizeof(double) + (size_t)NBN * 16 + (size_t)(TL::NB0 + TL::NB1) * (2 * P + 1) * sizeof(int);
+    // scatter metadata: rowOff, fIdx (8 B) + rowW1 (4 B) per node, posd tables
+    return n * sizeof(double) + (size_t)NBN * 20 + (size_t)(TL::NB0 + TL::NB1) * (2 * P + 1) * sizeof(int);
 }
 
 template <int P, class PH, int MODE, bool JAC, int UNI>
