@@ -22,9 +22,9 @@ namespace iga {
 
 template <int P> struct Tile2 {
     static constexpr int TE0 = 16;
-    static constexpr int TE1 = 16;
-    // p = 2 (9-lane groups, 120 regs) runs 16 warps; p = 3 (16-lane groups, NURBS) needs 168 regs -> 12
-    static constexpr int NWARP = P == 3 ? 12 : 16;
+    static constexpr int TE1 = P == 2 ? 36 : 16;   // 16 rounds of 36 (p = 2) element groups
+    // 12 warps (168 registers, no spills with the direct scatter; measured best for p = 2 and 3)
+    static constexpr int NWARP = 12;
     static constexpr int NB0 = TE0 + P, NB1 = TE1 + P;      // touched node box (uniform knots)
     static constexpr int NSL = (2 * P + 1) * (2 * P + 1);   // stencil slots per row
 };
