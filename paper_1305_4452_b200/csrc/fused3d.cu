@@ -19,6 +19,7 @@
 // B-splines) the test-side tables travel as a __grid_constant__ parameter: immediates in the
 // unrolled contraction.
 #include <cstdio>
+#include <type_traits>
 
 #include "iga_host.h"
 #include "pointwise.cuh"
@@ -46,6 +47,8 @@ struct F3 {
     static constexpr int DQS = NCOMBO * DB + 2;               // q stride (+2: spread smem banks)
     using State = typename PH::template State<3>;
     static constexpr int STD = (sizeof(State) + 7) / 8;      // doubles per state
+    // symmetric element Jacobian (hyperelastic tangent, major symmetry): contract blocks I <= J
+    static constexpr bool SYMJ = std::is_same<PH, PhysNeoHooke>::value;
     // shared-memory carve-up (in doubles)
     static constexpr int O_U = 0;                            // [NEN][M]
     static constexpr int O_UD = O_U + NEN * M;               // [NEN][M]
@@ -496,10 +499,27 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
             // ---- 5. test-side sum factorisation + coalesced emission, thread = (B, j) ----
             if (tid < NEN * M) {
-                const int B = tid / M, J = tid - B * M;
+                const int B = tid / M, T = tid - B * M;
                 const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
+                // Symmetric tangents (hyperelasticity: major symmetry of A_aIbJ, A-12): only the
+                // M(M+1)/2 blocks I <= J are contracted, (M+1)/2 per thread, and block (J, I) is
+                // written as the transpose.  Otherwise thread (B, J) does blocks (0..M-1, J).
+                constexpr bool SYMJ = F::SYMJ;
+                constexpr int NPAIR = SYMJ ? (M + 1) / 2 : M;
 #pragma unroll 1
-                for (int I = 0; I < M; I++) {
+                for (int pi = 0; pi < NPAIR; pi++) {
+                    int I, J;
+                    if constexpr (SYMJ) {
+                        const int k = T * NPAIR + pi;                  // k-th pair of the upper triangle
+                        I = 0;
+                        J = k;
+                        while (J >= M - I) { J -= M - I; I++; }       // row I holds pairs (I, I..M-1)
+                        J += I;
+                        if (I >= M) break;                            // odd M*(M+1)/2 remainder
+                    } else {
+                        I = pi;
+                        J = T;
+                    }
                     double Kc[NEN];
                     if (!(dbg & 1)) tsf_column_3d<F, UNI, P>(Kc, sD, I * M + J, b0, b1, b2, sTab, ut);
                     else {
@@ -523,6 +543,23 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                             const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
                             const int co = (P0[a0] * W1[a1] + P1[a1]) * W2[a2] + P2[a2];
                             atomicAdd(val + sRS[A * M + I] + (long long)co * M + J, Kc[A]);
+                        }
+                        if (SYMJ && I != J) {
+                            // transpose: row (B, J), column (A, I); positions of A in row B
+                            const int W1B = sW[NP1 + b1], W2B = sW[2 * NP1 + b2];
+#pragma unroll
+                            for (int x = 0; x < NP1; x++) {
+                                P0[x] = sPosE[b0 * NP1 + x];
+                                P1[x] = sPosE[NP1 * NP1 + b1 * NP1 + x];
+                                P2[x] = sPosE[2 * NP1 * NP1 + b2 * NP1 + x];
+                            }
+                            const long long rowB = sRS[B * M + J] + I;
+#pragma unroll
+                            for (int A = 0; A < NEN; A++) {
+                                const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
+                                const int co = (P0[a0] * W1B + P1[a1]) * W2B + P2[a2];
+                                atomicAdd(val + rowB + (long long)co * M, Kc[A]);
+                            }
                         }
                     } else {
                         double sum = 0.0;
