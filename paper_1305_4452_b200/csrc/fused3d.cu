@@ -49,6 +49,8 @@ struct F3 {
     static constexpr int STD = (sizeof(State) + 7) / 8;      // doubles per state
     // symmetric element Jacobian (hyperelastic tangent, major symmetry): contract blocks I <= J
     static constexpr bool SYMJ = std::is_same<PH, PhysNeoHooke>::value;
+    // resident CTAs per SM the register budget is sized for (m = 3: 96 threads -> 3 CTAs)
+    static constexpr int MINB = M == 3 ? 3 : 2;
     // shared-memory carve-up (in doubles)
     static constexpr int O_U = 0;                            // [NEN][M]
     static constexpr int O_UD = O_U + NEN * M;               // [NEN][M]
@@ -204,7 +206,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
 }
 
 template <int P, class PH, bool JAC, bool UNI>
-__global__ void __launch_bounds__(F3<P, PH>::NT, 2)
+__global__ void __launch_bounds__(F3<P, PH>::NT, F3<P, PH>::MINB)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
           int dbg, int bw) {
