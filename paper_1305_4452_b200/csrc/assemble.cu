@@ -256,6 +256,27 @@ __global__ void k_zero(double *__restrict__ p, long long n) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) p[k] = 0.0;
 }
 
+// two arrays in one launch (CSR values + residual): 16-byte stores where aligned
+__global__ void k_zero2(double *__restrict__ p, long long n, double *__restrict__ q, long long m) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n2 = ((reinterpret_cast<uintptr_t>(p) & 15) == 0) ? n / 2 : 0;
+    for (long long k = t0; k < n2; k += stride) reinterpret_cast<double2 *>(p)[k] = make_double2(0.0, 0.0);
+    for (long long k = 2 * n2 + t0; k < n; k += stride) p[k] = 0.0;
+    for (long long k = t0; k < m; k += stride) q[k] = 0.0;
+}
+
+void k_zero_pair(double *p, long long n, double *q, long long m, cudaStream_t st, int nsm) {
+    if (!p) { p = q; n = m; q = nullptr; m = 0; }
+    if (!q) m = 0;
+    if (n <= 0 && m <= 0) return;
+    long long blocks = (std::max(n / 2, m) + 255) / 256;
+    const long long cap = (long long)nsm * 16;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k_zero2<<<(unsigned)blocks, 256, 0, st>>>(p, n, q, m);
+}
+
 void k_zero_vec(double *p, long long n, cudaStream_t st, int nsm) {
     if (n <= 0) return;
     long long blocks = (n + 255) / 256;

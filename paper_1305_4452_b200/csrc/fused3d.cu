@@ -651,8 +651,11 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
     const long long nel = s->nel_local;
     const int grid = (int)std::min<long long>(nel, (long long)nsm * occ);
     int launches = 0;
-    if (jac) { ProfScope ps(s, "k_zero", st); k_zero_vec(val, s->nnz_owned, st, nsm); launches++; }
-    if (F) { ProfScope ps(s, "k_zero", st); k_zero_vec(F, s->nrows_owned, st, nsm); launches++; }
+    if (jac || F) {
+        ProfScope ps(s, "k_zero", st);
+        k_zero_pair(val, jac ? s->nnz_owned : 0, F, F ? s->nrows_owned : 0, st, nsm);
+        launches++;
+    }
     {
         ProfScope ps(s, "k_fused3d", st);
         // block width: ~3 element layers of a block's rows (values, m^2 (2p+1)^3 per node) in half the L2

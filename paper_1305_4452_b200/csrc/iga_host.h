@@ -78,6 +78,7 @@ void set_error(const std::string &msg);
 iga_status launch_form(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
                        const double *Udot, double *csr_val, double *F, cudaStream_t st);
 void k_zero_vec(double *p, long long n, cudaStream_t st, int nsm);
+void k_zero_pair(double *p, long long n, double *q, long long m, cudaStream_t st, int nsm);   // p and/or q may be null
 iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
