@@ -35,6 +35,7 @@ __device__ __forceinline__ void elem_coords(const SpaceDev &s, long long el, int
 // K3a: pointwise kernel
 // ============================================================================================
 struct GlobalNodes {
+    static constexpr bool PREMUL = false;
     const SpaceDev *s;
     const double *U, *Ud;
     long long node[64];      // global node (geometry: control points, weights)

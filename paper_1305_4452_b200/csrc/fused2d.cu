@@ -32,6 +32,7 @@ template <int P> struct Tile2 {
 // element's nodes in the tile box: local function A = (a0, a1) -> box index base + a0*NB1 + a1
 template <int NP1, int NB1>
 struct SmemNodes2 {
+    static constexpr bool PREMUL = true;     // tile staging stores w u, w udot, w x (NURBS)
     const double *pu, *pud, *pw, *px0, *px1;
     int base;
     bool hud;
@@ -193,12 +194,14 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 const long long node = (long long)g0 * A1.nu + g1;             // geometry: global
                 const long long lnode = local_node(s, g0, g1, 0);               // fields: touched box
                 fIdx[i] = lnode;
-                nU[i] = U[lnode];
-                nUd[i] = Ud ? Ud[lnode] : 0.0;
-                nw[i] = s.wts ? s.wts[node] : 1.0;
+                // homogeneous (weighted) node data for the rational basis, staged once per tile
+                const double wn = (MODE == MODE_NURBS && s.wts) ? s.wts[node] : 1.0;
+                nU[i] = wn * U[lnode];
+                nUd[i] = Ud ? wn * Ud[lnode] : 0.0;
+                nw[i] = wn;
                 if (s.geom == IGA_GEOM_NURBS) {
-                    nx0[i] = s.ctrl[node * 2];
-                    nx1[i] = s.ctrl[node * 2 + 1];
+                    nx0[i] = wn * s.ctrl[node * 2];
+                    nx1[i] = wn * s.ctrl[node * 2 + 1];
                 }
                 if (JAC) {
                     // closed-form CSR row start over the touched box (row_start with m = 1 and a

@@ -29,7 +29,8 @@ __device__ __forceinline__ double kind_value(const V &v, const int *aa) {
     return s;
 }
 
-// Nodes: accessor with u(A,m), ud(A,m), has_ud(), w(A), x(A,i) for the element's local functions.
+// Nodes: accessor with u(A,m), ud(A,m), has_ud(), w(A), x(A,i) for the element's local functions;
+// Nodes::PREMUL = the accessor returns w_A u, w_A udot, w_A x (homogeneous coordinates, staged once).
 // Returns error bits (1: detJ <= 0, 2: non-finite).
 template <int DIM, int P, class PH, int MODE, bool JAC, class Nodes, bool UNROLL_A = false>
 __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, double a, double b,
@@ -75,7 +76,7 @@ __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, d
             if (nurbs_geom) {
 #pragma unroll
                 for (int i = 0; i < DIM; i++) {
-                    const double xA = wA * nodes.x(A, i);
+                    const double xA = Nodes::PREMUL ? nodes.x(A, i) : wA * nodes.x(A, i);
 #pragma unroll
                     for (int c = 0; c < NC; c++) X[i][c] += xA * Pc[c];
                 }
@@ -83,10 +84,11 @@ __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, d
         }
 #pragma unroll
         for (int m = 0; m < M; m++) {
-            const double uA = wA * nodes.u(A, m);
+            const double uA = (MODE == MODE_NURBS && Nodes::PREMUL) ? nodes.u(A, m) : wA * nodes.u(A, m);
 #pragma unroll
             for (int c = 0; c < NC; c++) Phi[m][c] += uA * Pc[c];
-            if (nodes.has_ud()) Phit[m] += wA * nodes.ud(A, m) * Pc[0];
+            if (nodes.has_ud())
+                Phit[m] += ((MODE == MODE_NURBS && Nodes::PREMUL) ? nodes.ud(A, m) : wA * nodes.ud(A, m)) * Pc[0];
         }
     };
     if constexpr (UNROLL_A) {
