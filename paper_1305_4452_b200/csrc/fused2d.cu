@@ -140,11 +140,16 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
 }
 
 // UNI: 0 general tables, 1 uniform runs checked per element, 2 every element uniform
+#ifndef IGA_DBG
+#define IGA_DBG 0      // 1: honour the dbg phase-skip bits (A/B timing builds only)
+#endif
+
 template <int P, class PH, int MODE, bool JAC, int UNI>
 __global__ void __launch_bounds__(32 * Tile2<P>::NWARP, 1)
 k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
-          double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1,
+          double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1, int dbg_,
           const __grid_constant__ UniTab2<P> ut) {
+    const int dbg = IGA_DBG ? dbg_ : 0;
     using L = Lists<PH, 2, MODE>;
     using KS = typename L::KS;
     using TL = Tile2<P>;
@@ -255,7 +260,8 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             const bool act = lane_ok && el < nel_tile;
             const int le0 = act ? el / ne1 : 0, le1 = act ? el % ne1 : 0;
             // local node offsets of the element's functions within the tile box
-            const int fo0 = A0.first[e0lo + le0] - F00, fo1 = A1.first[e1lo + le1] - F01;
+            // (uniform knots, checked at launch: first[e] = first0 + e)
+            const int fo0 = le0, fo1 = le1;
             const double *tb0 = tb + (size_t)(0 * TL::TE1 + le0) * NQ1 * 3 * NP1;
             const double *tb1 = tb + (size_t)(1 * TL::TE1 + le1) * NQ1 * 3 * NP1;
             if (act) {
@@ -276,9 +282,10 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 nodes.pu = nU; nodes.pud = nUd; nodes.pw = s.wts ? nw : nullptr; nodes.px0 = nx0; nodes.px1 = nx1;
                 nodes.hud = Ud != nullptr;
                 nodes.base = fo0 * NB1 + fo1;
-                errbits |= pointwise_qp<2, P, PH, MODE, JAC, SmemNodes2<NP1, NB1>, true>(s, prm, a, b, v, wq, xq, hp, nodes,
-                                                             JAC ? gs + t : nullptr, NQ,
-                                                             Fout ? gs + (JAC ? NE * NQ : 0) + t : nullptr, NQ);
+                if (!(dbg & 4))          // dbg bits skip phases (A/B timing only; results invalid)
+                    errbits |= pointwise_qp<2, P, PH, MODE, JAC, SmemNodes2<NP1, NB1>, true>(s, prm, a, b, v, wq, xq, hp, nodes,
+                                                                 JAC ? gs + t : nullptr, NQ,
+                                                                 Fout ? gs + (JAC ? NE * NQ : 0) + t : nullptr, NQ);
             }
             __syncwarp();
             if (act) {
@@ -286,29 +293,33 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 const int nidx = (fo0 + c0) * NB1 + fo1 + c1;
                 const double sw = s.wts ? nw[nidx] : 1.0;
                 // (2) residual F_e[A], A = t
-                if (Fout) {
+                if (Fout && !(dbg & 8)) {
+                    // sum factorised per separable term: sum_q0 T0[o0](a0) sum_q1 T1[o1](a1) r(q0, q1)
                     const double *Rg = gs + (JAC ? NE * NQ : 0);
-                    double acc = 0.0;
+                    double t0[NQ1][3], t1[NQ1][3];
 #pragma unroll
-                    for (int q = 0; q < NQ; q++) {
-                        const int q0 = q / NQ1, q1 = q % NQ1;
-                        double va0[3], va1[3];
+                    for (int q = 0; q < NQ1; q++)
 #pragma unroll
                         for (int k = 0; k < 3; k++) {
-                            va0[k] = tb0[(q0 * 3 + k) * NP1 + c0];
-                            va1[k] = tb1[(q1 * 3 + k) * NP1 + c1];
+                            t0[q][k] = tb0[(q * 3 + k) * NP1 + c0];
+                            t1[q][k] = tb1[(q * 3 + k) * NP1 + c1];
                         }
-                        static_for<NR>([&](auto RR) {
-                            constexpr int rr = decltype(RR)::value;
-                            constexpr int c = L::R.c[rr];
-                            double pv = 0.0;
-                            static_for<KS::nterms(c)>([&](auto TT) {
-                                constexpr int tt = decltype(TT)::value;
-                                pv += va0[KS::ord(c, tt, 0)] * va1[KS::ord(c, tt, 1)];
-                            });
-                            acc += pv * Rg[rr * NQ + q];
+                    double acc = 0.0;
+                    static_for<NR>([&](auto RR) {
+                        constexpr int rr = decltype(RR)::value;
+                        constexpr int c = L::R.c[rr];
+                        static_for<KS::nterms(c)>([&](auto TT) {
+                            constexpr int tt = decltype(TT)::value;
+                            constexpr int o0 = KS::ord(c, tt, 0), o1 = KS::ord(c, tt, 1);
+#pragma unroll
+                            for (int q0 = 0; q0 < NQ1; q0++) {
+                                double s1 = 0.0;
+#pragma unroll
+                                for (int q1 = 0; q1 < NQ1; q1++) s1 += t1[q1][o1] * Rg[rr * NQ + q0 * NQ1 + q1];
+                                acc += t0[q0][o0] * s1;
+                            }
                         });
-                    }
+                    });
                     atomicAdd(Fout + fIdx[nidx], sw * acc);           // red.global (no return value)
                 }
                 // (3) Jacobian column B = t
@@ -316,7 +327,10 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     double Kc[NEN];
                     // elements inside both axes' uniform runs take the constant-operand tables
                     const int ge0 = e0lo + le0, ge1 = e1lo + le1;
-                    if constexpr (UNI == 2)
+                    if (dbg & 1) {
+#pragma unroll
+                        for (int A = 0; A < NEN; A++) Kc[A] = gs[A];
+                    } else if constexpr (UNI == 2)
                         tsf_column_2d<L, KS, P, true>(Kc, gs, tb0, tb1, c0, c1, ut);
                     else if (UNI == 1 && ge0 >= A0.uni_lo && ge0 < A0.uni_hi && ge1 >= A1.uni_lo && ge1 < A1.uni_hi)
                         tsf_column_2d<L, KS, P, true>(Kc, gs, tb0, tb1, c0, c1, ut);
@@ -327,6 +341,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     // rowOff(A) + pos0(a0 -> b0) W1(A) + pos1(a1 -> b1)
 #pragma unroll
                     for (int A = 0; A < NEN; A++) {
+                        if (dbg & 2) { if (Kc[A] == 1.2345e300) val[0] = 0.0; continue; }
                         const int a0 = A / NP1, a1 = A % NP1;
                         const int ridx = (fo0 + a0) * NB1 + fo1 + a1;
                         const double sa = s.wts ? nw[ridx] : 1.0;
@@ -373,7 +388,7 @@ static iga_status launch_k2(iga_space_s *s, const Prm &prm, double a, double b, 
     occ = std::max(occ, 1);
     const int grid = std::min(nt0 * nt1, nsm * occ);
     ProfScope ps(s, "k_fused2d", st);
-    k_fused2d<P, PH, MODE, JAC, UNI><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1, ut);
+    k_fused2d<P, PH, MODE, JAC, UNI><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1, s->dbg, ut);
     return IGA_OK;
 }
 
