@@ -18,6 +18,8 @@ ROOT = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+# experiment builds only (tools/variant.sh), e.g. IGA_NVCC_EXTRA=-DIGA_DBG=1
+FLAGS += os.environ.get("IGA_NVCC_EXTRA", "").split()
 
 
 def _sources():

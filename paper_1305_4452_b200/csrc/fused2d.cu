@@ -190,7 +190,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         const int F00 = A0.first[e0lo], F01 = A1.first[e1lo];
         const int nb0 = ne0 + P, nb1 = ne1 + P;
         // ---- stage the tile: node data, scatter metadata, tables ----
-        for (int i = tid; i < NBN; i += blockDim.x) {
+        for (int i = (dbg & 16) ? NBN : tid; i < NBN; i += blockDim.x) {
             const int l0 = i / NB1, l1 = i % NB1;
             if (l0 < nb0 && l1 < nb1) {
                 int g0 = F00 + l0, g1 = F01 + l1;
@@ -231,13 +231,13 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 pd0[i] = (l < (d ? nb1 : nb0)) ? ax.posd[g * W2 + dl] : -1;
             }
         }
-        for (int i = tid; i < 2 * TL::TE1 * NQ1 * 3 * NP1; i += blockDim.x) {
+        for (int i = (dbg & 16) ? 1 << 30 : tid; i < 2 * TL::TE1 * NQ1 * 3 * NP1; i += blockDim.x) {
             const int d = i / (TL::TE1 * NQ1 * 3 * NP1), r = i % (TL::TE1 * NQ1 * 3 * NP1);
             const int el = r / (NQ1 * 3 * NP1);
             const int elo = d == 0 ? e0lo : e1lo, ne = d == 0 ? ne0 : ne1;
             if (el < ne) tb[i] = s.ax[d].tab[(size_t)(elo + el) * NQ1 * 3 * NP1 + r % (NQ1 * 3 * NP1)];
         }
-        for (int i = tid; i < 2 * TL::TE1 * NQ1; i += blockDim.x) {
+        for (int i = (dbg & 16) ? 1 << 30 : tid; i < 2 * TL::TE1 * NQ1; i += blockDim.x) {
             const int d = i / (TL::TE1 * NQ1), r = i % (TL::TE1 * NQ1);
             const int el = r / NQ1;
             const int elo = d == 0 ? e0lo : e1lo, ne = d == 0 ? ne0 : ne1;
@@ -246,7 +246,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 qxb[i] = s.ax[d].qx[(size_t)(elo + el) * NQ1 + r % NQ1];
             }
         }
-        for (int i = tid; i < 2 * TL::TE1; i += blockDim.x) {
+        for (int i = (dbg & 16) ? 1 << 30 : tid; i < 2 * TL::TE1; i += blockDim.x) {
             const int d = i / TL::TE1, el = i % TL::TE1;
             const int elo = d == 0 ? e0lo : e1lo, ne = d == 0 ? ne0 : ne1;
             if (el < ne) hpb[i] = s.ax[d].hpar[elo + el];
