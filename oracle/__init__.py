@@ -51,6 +51,8 @@ def lib():
         L.orc_pattern_rows.argtypes = [P, C.c_int64, lp, lp, C.POINTER(C.c_int32)]
         L.orc_eval_point.restype = C.c_int
         L.orc_eval_point.argtypes = [P, ip, dp, dp, dp, dp, lp, dp, dp]
+        L.orc_eval_point3.restype = C.c_int
+        L.orc_eval_point3.argtypes = [P, ip, dp, dp, dp, dp, dp, lp, dp, dp]
         L.orc_element.restype = C.c_int
         L.orc_element.argtypes = [P, C.c_int, dp, C.c_double, C.c_double, dp, dp, dp, ip, dp, dp, lp]
         L.orc_assemble_dense.restype = C.c_int
@@ -188,6 +190,24 @@ class Space:
             raise ValueError("oracle: detJ <= 0")
         return dict(R=R[:n], dR=dR[:3 * n].reshape(n, 3), ddR=ddR[:9 * n].reshape(n, 3, 3), node=node[:n],
                     x=x, detJ=det.value)
+
+    def eval_point3(self, e, xi):
+        """All spatial derivatives of R_A up to third order (orc_eval_point3)."""
+        nen_max = 125
+        R = np.zeros(nen_max)
+        d1 = np.zeros(nen_max * 3)
+        d2 = np.zeros(nen_max * 9)
+        d3 = np.zeros(nen_max * 27)
+        node = np.zeros(nen_max, np.int64)
+        x = np.zeros(3)
+        det = C.c_double()
+        ee = np.array(list(e) + [0] * (3 - len(e)), np.int32)
+        xx = np.array(list(xi) + [0.0] * (3 - len(xi)), np.float64)
+        n = lib().orc_eval_point3(self.h, _i(ee), _d(xx), _d(R), _d(d1), _d(d2), _d(d3), _l(node), _d(x), C.byref(det))
+        if n < 0:
+            raise ValueError("oracle: detJ <= 0")
+        return dict(R=R[:n], dR=d1[:3 * n].reshape(n, 3), ddR=d2[:9 * n].reshape(n, 3, 3),
+                    dddR=d3[:27 * n].reshape(n, 3, 3, 3), node=node[:n], x=x, detJ=det.value)
 
     def element(self, kind, params, a, b, U, Udot=None, e=(0, 0, 0), Utau=None, want_K=True):
         prm = np.zeros(8)

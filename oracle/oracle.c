@@ -513,6 +513,171 @@ int orc_eval_point(const orc_space *s, const int *e, const double *xi, double *R
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* Third-order basis: every spatial derivative of R_A up to order 3 at */
+/* one point, written out in the paper's order and notation:                               */
+/*   N and its first three derivatives by the derivative recursion (A5), tensor product     */
+/*   M_{A,abg}; w, w_{,a}, w_{,ab}, w_{,abg}; R_A ... R_{A,abg} by  */
+/*   (rational) P:211, (drational) P:234, (ddrational) P:245, (dddrational) P:248-255;      */
+/*   x_{m,a}, x_{m,ab}, x_{m,abg} = sum_B x_B R_{B,...} (isoparametric map P:265-278);        */
+/*   xi_{a,i} (A-5), xi_{n,nl}, xi_{n,nlo};                  */
+/*   R_{A,i}, R_{A,ij}, R_{A,ijk} by (dspatial), (ddspatial), (dddspatial) P:309-315.        */
+/* Output per local function A: R[A], d1[A][3], d2[A][3][3], d3[A][3][3][3] (unused dims 0). */
+/* ------------------------------------------------------------------------------------ */
+int orc_eval_point3(const orc_space *s, const int *e_in, const double *xi_in, double *R, double *d1, double *d2,
+                    double *d3, int64_t *node, double *x, double *detJ)
+{
+    int dim = s->dim;
+    int e[3] = {0, 0, 0};
+    double xi[3] = {0, 0, 0};
+    for (int d = 0; d < dim; d++) { e[d] = e_in[d]; xi[d] = xi_in[d]; }
+    double Nv[3][ORC_MAXP + 1][4];
+    int first[3];
+    for (int d = 0; d < 3; d++) {
+        if (d >= dim) { Nv[d][0][0] = 1.0; Nv[d][0][1] = Nv[d][0][2] = Nv[d][0][3] = 0.0; first[d] = 0; continue; }
+        int sp = s->span[d][e[d]];
+        first[d] = sp - s->p[d];
+        for (int a = 0; a <= s->p[d]; a++)
+            for (int k = 0; k < 4; k++) Nv[d][a][k] = orc_coxdeboor_deriv(first[d] + a, s->p[d], s->U[d], xi[d], k);
+    }
+    int n0 = s->p[0] + 1, n1 = dim > 1 ? s->p[1] + 1 : 1, n2 = dim > 2 ? s->p[2] + 1 : 1;
+    int nen = n0 * n1 * n2;
+    static __thread double M[ORC_MAXEN], M1[ORC_MAXEN][3], M2[ORC_MAXEN][3][3], M3[ORC_MAXEN][3][3][3], wA[ORC_MAXEN];
+    for (int A = 0; A < nen; A++) {
+        int aa[3] = {A / (n1 * n2), (A / n2) % n1, A % n2};
+        int g[3];
+        for (int d = 0; d < 3; d++) g[d] = (first[d] + aa[d]) % s->nu[d];
+        node[A] = ((int64_t)g[0] * s->nu[1] + g[1]) * s->nu[2] + g[2];
+        wA[A] = s->wts ? s->wts[node[A]] : 1.0;
+        M[A] = Nv[0][aa[0]][0] * Nv[1][aa[1]][0] * Nv[2][aa[2]][0];
+        for (int al = 0; al < 3; al++)
+            for (int be = 0; be < 3; be++)
+                for (int ga = 0; ga < 3; ga++) {
+                    double v1 = 1.0, v2 = 1.0, v3 = 1.0;
+                    for (int d = 0; d < 3; d++) {
+                        int k1 = (d == al), k2 = k1 + (d == be), k3 = k2 + (d == ga);
+                        v1 *= (k1 < 4) ? Nv[d][aa[d]][k1] : 0.0;
+                        v2 *= (k2 < 4) ? Nv[d][aa[d]][k2] : 0.0;
+                        v3 *= (k3 < 4) ? Nv[d][aa[d]][k3] : 0.0;
+                    }
+                    M1[A][al] = v1;
+                    M2[A][al][be] = v2;
+                    M3[A][al][be][ga] = v3;
+                }
+    }
+    /* weight function and its derivatives */
+    double w = 0.0, w1[3] = {0}, w2[3][3] = {{0}}, w3[3][3][3] = {{{0}}};
+    for (int A = 0; A < nen; A++) {
+        w += wA[A] * M[A];
+        for (int al = 0; al < 3; al++) {
+            w1[al] += wA[A] * M1[A][al];
+            for (int be = 0; be < 3; be++) {
+                w2[al][be] += wA[A] * M2[A][al][be];
+                for (int ga = 0; ga < 3; ga++) w3[al][be][ga] += wA[A] * M3[A][al][be][ga];
+            }
+        }
+    }
+    /* rational basis and parametric derivatives */
+    static __thread double Rp1[ORC_MAXEN][3], Rp2[ORC_MAXEN][3][3], Rp3[ORC_MAXEN][3][3][3];
+    for (int A = 0; A < nen; A++) {
+        R[A] = wA[A] * M[A] / w;
+        for (int al = 0; al < dim; al++) Rp1[A][al] = (wA[A] * M1[A][al] - R[A] * w1[al]) / w;
+        for (int al = 0; al < dim; al++)
+            for (int be = 0; be < dim; be++)
+                Rp2[A][al][be] = (wA[A] * M2[A][al][be] - R[A] * w2[al][be] - Rp1[A][be] * w1[al] - Rp1[A][al] * w1[be]) / w;
+        for (int al = 0; al < dim; al++)
+            for (int be = 0; be < dim; be++)
+                for (int ga = 0; ga < dim; ga++)
+                    Rp3[A][al][be][ga] = (wA[A] * M3[A][al][be][ga] - R[A] * w3[al][be][ga]) / w
+                                         - (Rp1[A][al] * w2[be][ga] + Rp1[A][be] * w2[al][ga] + Rp1[A][ga] * w2[al][be]) / w
+                                         - (Rp2[A][be][ga] * w1[al] + Rp2[A][al][ga] * w1[be] + Rp2[A][al][be] * w1[ga]) / w;
+    }
+    /* isoparametric map and its parametric derivatives up to third order */
+    double X[3] = {0}, X1[3][3] = {{0}}, X2[3][3][3] = {{{0}}}, X3[3][3][3][3] = {{{{0}}}};
+    if (s->geom == ORC_NURBS) {
+        for (int B = 0; B < nen; B++)
+            for (int m = 0; m < dim; m++) {
+                double xb = s->ctrl[node[B] * dim + m];
+                X[m] += xb * R[B];
+                for (int al = 0; al < dim; al++) {
+                    X1[m][al] += xb * Rp1[B][al];
+                    for (int be = 0; be < dim; be++) {
+                        X2[m][al][be] += xb * Rp2[B][al][be];
+                        for (int ga = 0; ga < dim; ga++) X3[m][al][be][ga] += xb * Rp3[B][al][be][ga];
+                    }
+                }
+            }
+    } else {
+        for (int m = 0; m < dim; m++) { X[m] = xi[m]; X1[m][m] = 1.0; }
+    }
+    double Xi[3][3] = {{0}};
+    double det = inverse(dim, X1, Xi);
+    if (!(det > 0.0)) return -1;
+    /* xi_{nu,nl} = - x_{m,eps mu} xi_{eps,n} xi_{mu,l} xi_{nu,m} */
+    double Xi2[3][3][3] = {{{0}}};
+    for (int nu_ = 0; nu_ < dim; nu_++)
+        for (int n = 0; n < dim; n++)
+            for (int l = 0; l < dim; l++) {
+                double v = 0.0;
+                for (int m = 0; m < dim; m++)
+                    for (int ep = 0; ep < dim; ep++)
+                        for (int mu = 0; mu < dim; mu++) v -= X2[m][ep][mu] * Xi[ep][n] * Xi[mu][l] * Xi[nu_][m];
+                Xi2[nu_][n][l] = v;
+            }
+    /* xi_{nu,nlo} = - x_{m,eps mu om} xi_{eps,n} xi_{mu,l} xi_{nu,m} xi_{om,o}
+     *              - x_{m,eps mu} (xi_{eps,no} xi_{mu,l} xi_{nu,m} + xi_{eps,n} xi_{mu,lo} xi_{nu,m}
+     *                              + xi_{eps,n} xi_{mu,l} xi_{nu,mo}) */
+    double Xi3[3][3][3][3] = {{{{0}}}};
+    for (int nu_ = 0; nu_ < dim; nu_++)
+        for (int n = 0; n < dim; n++)
+            for (int l = 0; l < dim; l++)
+                for (int o = 0; o < dim; o++) {
+                    double v = 0.0;
+                    for (int m = 0; m < dim; m++)
+                        for (int ep = 0; ep < dim; ep++)
+                            for (int mu = 0; mu < dim; mu++) {
+                                for (int om = 0; om < dim; om++)
+                                    v -= X3[m][ep][mu][om] * Xi[ep][n] * Xi[mu][l] * Xi[nu_][m] * Xi[om][o];
+                                v -= X2[m][ep][mu] * (Xi2[ep][n][o] * Xi[mu][l] * Xi[nu_][m] + Xi[ep][n] * Xi2[mu][l][o] * Xi[nu_][m]
+                                                      + Xi[ep][n] * Xi[mu][l] * Xi2[nu_][m][o]);
+                            }
+                    Xi3[nu_][n][l][o] = v;
+                }
+    /* push-forward (dspatial) P:309, (ddspatial) P:310, (dddspatial) P:311-315 */
+    for (int A = 0; A < nen; A++) {
+        for (int i = 0; i < 3; i++) {
+            double v1 = 0.0;
+            if (i < dim)
+                for (int al = 0; al < dim; al++) v1 += Rp1[A][al] * Xi[al][i];
+            d1[A * 3 + i] = v1;
+            for (int j = 0; j < 3; j++) {
+                double v2 = 0.0;
+                if (i < dim && j < dim) {
+                    for (int al = 0; al < dim; al++)
+                        for (int be = 0; be < dim; be++) v2 += Rp2[A][al][be] * Xi[al][i] * Xi[be][j];
+                    for (int al = 0; al < dim; al++) v2 += Rp1[A][al] * Xi2[al][i][j];
+                }
+                d2[(A * 3 + i) * 3 + j] = v2;
+                for (int k = 0; k < 3; k++) {
+                    double v3 = 0.0;
+                    if (i < dim && j < dim && k < dim) {
+                        for (int al = 0; al < dim; al++)
+                            for (int be = 0; be < dim; be++) {
+                                for (int ga = 0; ga < dim; ga++) v3 += Rp3[A][al][be][ga] * Xi[al][i] * Xi[be][j] * Xi[ga][k];
+                                v3 += Rp2[A][al][be] * (Xi[al][i] * Xi2[be][j][k] + Xi[be][j] * Xi2[al][i][k] + Xi[be][k] * Xi2[al][i][j]);
+                            }
+                        for (int al = 0; al < dim; al++) v3 += Rp1[A][al] * Xi3[al][i][j][k];
+                    }
+                    d3[((A * 3 + i) * 3 + j) * 3 + k] = v3;
+                }
+            }
+        }
+    }
+    for (int i = 0; i < 3; i++) x[i] = X[i];
+    *detJ = det;
+    return nen;
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* Fields at the quadrature point from U_e (Alg. 4).                      */
 /* ------------------------------------------------------------------------------------ */
 typedef struct {
