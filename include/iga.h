@@ -179,6 +179,18 @@ iga_status iga_form_residual_group(int n, const iga_space *spaces, const iga_phy
                                    const double *const *U, const double *const *Udot,
                                    double *const *F, void *stream);
 
+/* Basis evaluation at the quadrature points -- Alg. 4's "Basis(G_e, x_q)" extended to
+ * the third spatial derivatives the paper derives for higher-order PDEs on mapped geometry:
+ * (dddrational) P:248-255, the inverse-map derivatives P:316-340, (dspatial)-(dddspatial)
+ * P:309-315.  For every element of this rank (element box, C order, last axis fastest), every
+ * local function A of the element (C order) and every Gauss point q of the element (C order):
+ *   out[((e * nen + A) * ncomp + c) * nq + q],  nen = prod(p_d+1), nq = prod(quad_d),
+ *   components c: R_A; R_{A,i} (order >= 1); R_{A,ij} (order >= 2, i-major); R_{A,ijk} (order 3),
+ *   ncomp = 1 + d + d^2 + d^3 (truncated at `order`).
+ * out: device fp64, caller-allocated.  order in [0, 3]; IGA_ERR_PARAM otherwise.  A point with
+ * detJ <= 0 sets the device flag (iga_space_check -> IGA_ERR_SINGULAR_MAP). */
+iga_status iga_basis_eval(iga_space s, int order, double *out, void *stream);
+
 /* Synchronises `stream` and reports (then clears) the device error flag of the last form
  * call: IGA_OK, IGA_ERR_SINGULAR_MAP or IGA_ERR_NONFINITE. */
 iga_status iga_space_check(iga_space s, void *stream);

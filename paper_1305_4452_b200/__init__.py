@@ -62,7 +62,7 @@ EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_p
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
            "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
            "iga_microbench", "iga_space_set_option", "iga_form_jacobian_group", "iga_form_residual_group",
-           "iga_dist_plan", "iga_nccl_unique_id"]
+           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval"]
 
 
 def lib():
@@ -101,12 +101,13 @@ def lib():
         L.iga_dist_plan.argtypes = [C.POINTER(_Desc), C.POINTER(_Dist), lp, lp, lp, lp, lp, C.c_int,
                                     C.POINTER(_Msg), C.POINTER(C.c_int), C.POINTER(_Msg), C.POINTER(C.c_int)]
         L.iga_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte * 128)]
+        L.iga_basis_eval.argtypes = [vp, C.c_int, vp, vp]
         L.iga_last_error.restype = C.c_char_p
         L.iga_version.restype = C.c_char_p
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
                   "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
                   "iga_profile_reset", "iga_form_jacobian_group", "iga_form_residual_group", "iga_dist_plan",
-                  "iga_nccl_unique_id"):
+                  "iga_nccl_unique_id", "iga_basis_eval"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -286,6 +287,8 @@ class Space:
         _check(L.iga_space_create(C.byref(d), C.byref(dd) if dd is not None else None, device, C.byref(h)))
         self.h = h
         self.dim, self.dof, self.device = dim, dof, device
+        self.degree = [int(degree[a]) for a in range(dim)]
+        self.quad = [int(quad[a]) if quad is not None and quad[a] else int(degree[a]) + 1 for a in range(dim)]
         v = [C.c_int64() for _ in range(4)]
         lo, hi, elo, ehi = [(C.c_int64 * 3)() for _ in range(4)]
         _check(L.iga_space_info(h, *[C.byref(x) for x in v], lo, hi, elo, ehi))
@@ -341,6 +344,19 @@ class Space:
         _check(lib().iga_form_jacobian_host(self.h, C.byref(phys), float(a), float(b), _ptr(U_host),
                                             _ptr(Udot_host), _ptr(vals_host), _ptr(F_host), _stream(stream)))
         return vals_host, F_host
+
+    def basis_eval(self, order=3, out=None, stream=None):
+        """Spatial derivatives of every local basis function up to `order` at every Gauss point
+        (iga_basis_eval); returns a tensor [nelem_local, nen, ncomp, nq]."""
+        import torch
+        nen = int(np.prod([p + 1 for p in self.degree]))
+        nq = int(np.prod(self.quad))
+        ncomp = sum(self.dim ** k for k in range(order + 1))
+        nel = int(np.prod([self.elem_hi[a] - self.elem_lo[a] for a in range(self.dim)]))
+        if out is None:
+            out = torch.empty((nel, nen, ncomp, nq), dtype=torch.float64, device=torch.device("cuda", self.device))
+        _check(lib().iga_basis_eval(self.h, int(order), _ptr(out), _stream(stream)))
+        return out
 
     def check(self, stream=None):
         _check(lib().iga_space_check(self.h, _stream(stream)))

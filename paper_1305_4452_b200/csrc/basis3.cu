@@ -1,0 +1,335 @@
+// basis3.cu -- third-order basis evaluation at the quadrature points (the
+// paper's "higher-order spatial derivatives" for higher-order PDEs on mapped geometry):
+// for every element of this rank and every Gauss point, all spatial derivatives of every local
+// rational basis function up to order 3:
+//   univariate N..N''' by the in-span triangular scheme extended to third order (the "more
+//   efficient algorithm" P:191-193), tensor product, weight function derivatives
+//   (P:218-224), rational derivatives (rational)-(dddrational), the isoparametric map
+//   and its parametric derivatives, its inverse and the inverse-map
+//   derivatives, and the push-forward (dspatial)-(dddspatial).
+// One thread per (element, quadrature point); three passes over the element's functions (weight
+// sums; geometry sums; push-forward and output) keep the per-thread state to the point's tensors.
+// Output layout [element][A][component][q]: consecutive threads (q) write consecutive doubles.
+#include "iga_host.h"
+
+namespace iga {
+
+constexpr int B3P = MAXP + 1;
+
+// N^(k)_{span-p+a}(xi), k = 0..3, a = 0..p (triangular scheme; derivatives via the a[][] recurrence)
+__device__ void span_ders3(int span, double xi, int p, const double *__restrict__ U, double out[4][B3P]) {
+    double ndu[B3P][B3P], left[B3P], right[B3P];
+    ndu[0][0] = 1.0;
+    for (int j = 1; j <= p; j++) {
+        left[j] = xi - U[span + 1 - j];
+        right[j] = U[span + j] - xi;
+        double saved = 0.0;
+        for (int r = 0; r < j; r++) {
+            ndu[j][r] = right[r + 1] + left[j - r];
+            const double tmp = ndu[r][j - 1] / ndu[j][r];
+            ndu[r][j] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        ndu[j][j] = saved;
+    }
+    for (int r = 0; r <= p; r++) {
+        out[0][r] = ndu[r][p];
+        for (int k = 1; k < 4; k++) out[k][r] = 0.0;
+    }
+    const int nd = p < 3 ? p : 3;
+    double a[2][B3P];
+    for (int r = 0; r <= p; r++) {
+        int s1 = 0, s2 = 1;
+        a[0][0] = 1.0;
+        for (int k = 1; k <= nd; k++) {
+            double d = 0.0;
+            const int rk = r - k, pk = p - k;
+            if (r >= k) {
+                a[s2][0] = a[s1][0] / ndu[pk + 1][rk];
+                d = a[s2][0] * ndu[rk][pk];
+            }
+            const int j1 = (rk >= -1) ? 1 : -rk;
+            const int j2 = (r - 1 <= pk) ? k - 1 : p - r;
+            for (int j = j1; j <= j2; j++) {
+                a[s2][j] = (a[s1][j] - a[s1][j - 1]) / ndu[pk + 1][rk + j];
+                d += a[s2][j] * ndu[rk + j][pk];
+            }
+            if (r <= pk) {
+                a[s2][k] = -a[s1][k - 1] / ndu[pk + 1][r];
+                d += a[s2][k] * ndu[r][pk];
+            }
+            out[k][r] = d;
+            const int t = s1; s1 = s2; s2 = t;
+        }
+    }
+    double f = p;
+    for (int k = 1; k <= nd; k++) {
+        for (int r = 0; r <= p; r++) out[k][r] *= f;
+        f *= (p - k);
+    }
+}
+
+template <int DIM>
+struct Pt3 {
+    double v[DIM][4][B3P];   // univariate N..N''' per axis
+    int g[DIM], nen, np1[DIM];
+};
+
+// parametric derivatives of the tensor-product B-spline M_A up to third order
+template <int DIM>
+__device__ __forceinline__ void tensor3(const Pt3<DIM> &P, const int aa[3], double &m0, double m1[DIM],
+                                        double m2[DIM][DIM], double m3[DIM][DIM][DIM]) {
+    auto val = [&](int c0, int c1, int c2) {
+        double r = 1.0;
+        const int c[3] = {c0, c1, c2};
+#pragma unroll
+        for (int d = 0; d < DIM; d++) r *= P.v[d][c[d]][aa[d]];
+        return r;
+    };
+    m0 = val(0, 0, 0);
+#pragma unroll
+    for (int al = 0; al < DIM; al++) {
+        int c[3] = {0, 0, 0};
+        c[al]++;
+        m1[al] = val(c[0], c[1], c[2]);
+#pragma unroll
+        for (int be = 0; be < DIM; be++) {
+            int c2[3] = {c[0], c[1], c[2]};
+            c2[be]++;
+            m2[al][be] = val(c2[0], c2[1], c2[2]);
+#pragma unroll
+            for (int ga = 0; ga < DIM; ga++) {
+                int c3[3] = {c2[0], c2[1], c2[2]};
+                c3[ga]++;
+                m3[al][be][ga] = val(c3[0], c3[1], c3[2]);
+            }
+        }
+    }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long nelem, int nq_el, int ncomp,
+                                                double *__restrict__ out) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nelem * nq_el) return;
+    const long long el = t / nq_el;
+    const int q = (int)(t - el * nq_el);
+    int e[3] = {0, 0, 0}, qd[3] = {0, 0, 0};
+    {
+        long long r = el;
+        int rq = q;
+        for (int d = DIM - 1; d >= 0; d--) {
+            const int n = s.ax[d].el_hi - s.ax[d].el_lo;
+            e[d] = s.ax[d].el_lo + (int)(r % n);
+            r /= n;
+            qd[d] = rq % s.ax[d].nq;
+            rq /= s.ax[d].nq;
+        }
+    }
+    Pt3<DIM> P;
+    P.nen = 1;
+    for (int d = 0; d < DIM; d++) {
+        const AxisDev &ax = s.ax[d];
+        const int first = ax.first[e[d]];
+        P.g[d] = first;
+        P.np1[d] = ax.p + 1;
+        P.nen *= ax.p + 1;
+        span_ders3(first + ax.p, ax.qx[(size_t)e[d] * ax.nq + qd[d]], ax.p, ax.knots, P.v[d]);
+    }
+    const bool rational = s.mode == MODE_NURBS;
+    const bool geom = s.geom == IGA_GEOM_NURBS;
+    auto decode = [&](int A, int aa[3], long long &node) {
+        int r = A;
+        int g[3] = {0, 0, 0};
+        for (int d = DIM - 1; d >= 0; d--) {
+            aa[d] = r % P.np1[d];
+            r /= P.np1[d];
+            g[d] = P.g[d] + aa[d];
+            if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
+        }
+        node = node_index(s, g[0], g[1], g[2]);
+    };
+    // ---- pass 1: w and its parametric derivatives ----
+    double w0 = 0.0, w1[DIM] = {}, w2[DIM][DIM] = {}, w3[DIM][DIM][DIM] = {};
+    for (int A = 0; A < P.nen; A++) {
+        int aa[3] = {0, 0, 0};
+        long long node;
+        decode(A, aa, node);
+        const double wA = (rational && s.wts) ? s.wts[node] : 1.0;
+        double m0, m1[DIM], m2[DIM][DIM], m3[DIM][DIM][DIM];
+        tensor3<DIM>(P, aa, m0, m1, m2, m3);
+        w0 += wA * m0;
+        for (int al = 0; al < DIM; al++) {
+            w1[al] += wA * m1[al];
+            for (int be = 0; be < DIM; be++) {
+                w2[al][be] += wA * m2[al][be];
+                for (int ga = 0; ga < DIM; ga++) w3[al][be][ga] += wA * m3[al][be][ga];
+            }
+        }
+    }
+    const double iw = 1.0 / w0;
+    // rational parametric derivatives of one function
+    auto rational3 = [&](int A, double &r0, double r1[DIM], double r2[DIM][DIM], double r3[DIM][DIM][DIM], long long &node) {
+        int aa[3] = {0, 0, 0};
+        decode(A, aa, node);
+        const double wA = (rational && s.wts) ? s.wts[node] : 1.0;
+        double m0, m1[DIM], m2[DIM][DIM], m3[DIM][DIM][DIM];
+        tensor3<DIM>(P, aa, m0, m1, m2, m3);
+        r0 = wA * m0 * iw;
+        for (int al = 0; al < DIM; al++) r1[al] = (wA * m1[al] - r0 * w1[al]) * iw;
+        for (int al = 0; al < DIM; al++)
+            for (int be = 0; be < DIM; be++)
+                r2[al][be] = (wA * m2[al][be] - r0 * w2[al][be] - r1[be] * w1[al] - r1[al] * w1[be]) * iw;
+        for (int al = 0; al < DIM; al++)
+            for (int be = 0; be < DIM; be++)
+                for (int ga = 0; ga < DIM; ga++)
+                    r3[al][be][ga] = (wA * m3[al][be][ga] - r0 * w3[al][be][ga]
+                                      - r1[al] * w2[be][ga] - r1[be] * w2[al][ga] - r1[ga] * w2[al][be]
+                                      - r2[be][ga] * w1[al] - r2[al][ga] * w1[be] - r2[al][be] * w1[ga]) * iw;
+    };
+    // ---- pass 2: the map x and its parametric derivatives ----
+    double X1[DIM][DIM] = {}, X2[DIM][DIM][DIM] = {}, X3[DIM][DIM][DIM][DIM] = {};
+    if (geom) {
+        for (int A = 0; A < P.nen; A++) {
+            double r0, r1[DIM], r2[DIM][DIM], r3[DIM][DIM][DIM];
+            long long node;
+            rational3(A, r0, r1, r2, r3, node);
+            for (int m = 0; m < DIM; m++) {
+                const double xb = s.ctrl[node * DIM + m];
+                for (int al = 0; al < DIM; al++) {
+                    X1[m][al] += xb * r1[al];
+                    for (int be = 0; be < DIM; be++) {
+                        X2[m][al][be] += xb * r2[al][be];
+                        for (int ga = 0; ga < DIM; ga++) X3[m][al][be][ga] += xb * r3[al][be][ga];
+                    }
+                }
+            }
+        }
+    } else {
+        for (int m = 0; m < DIM; m++) X1[m][m] = 1.0;
+    }
+    // inverse map G[al][i] = xi_{al,i}, by cofactors
+    double G[DIM][DIM], det;
+    if constexpr (DIM == 2) {
+        det = X1[0][0] * X1[1][1] - X1[0][1] * X1[1][0];
+        G[0][0] = X1[1][1] / det; G[0][1] = -X1[0][1] / det;
+        G[1][0] = -X1[1][0] / det; G[1][1] = X1[0][0] / det;
+    } else {
+        const double c00 = X1[1][1] * X1[2][2] - X1[1][2] * X1[2][1];
+        const double c01 = X1[1][2] * X1[2][0] - X1[1][0] * X1[2][2];
+        const double c02 = X1[1][0] * X1[2][1] - X1[1][1] * X1[2][0];
+        det = X1[0][0] * c00 + X1[0][1] * c01 + X1[0][2] * c02;
+        G[0][0] = c00 / det; G[1][0] = c01 / det; G[2][0] = c02 / det;
+        G[0][1] = (X1[0][2] * X1[2][1] - X1[0][1] * X1[2][2]) / det;
+        G[1][1] = (X1[0][0] * X1[2][2] - X1[0][2] * X1[2][0]) / det;
+        G[2][1] = (X1[0][1] * X1[2][0] - X1[0][0] * X1[2][1]) / det;
+        G[0][2] = (X1[0][1] * X1[1][2] - X1[0][2] * X1[1][1]) / det;
+        G[1][2] = (X1[0][2] * X1[1][0] - X1[0][0] * X1[1][2]) / det;
+        G[2][2] = (X1[0][0] * X1[1][1] - X1[0][1] * X1[1][0]) / det;
+    }
+    if (!(det > 0.0)) atomicOr(s.errflag, 1);
+    // second and third derivatives of the inverse map:
+    //   G2[nu][n][l]   = - x_{m,em} G[e][n] G[mu][l] G[nu][m]
+    //   G3[nu][n][l][o] = - x_{m,emw} G[e][n] G[mu][l] G[nu][m] G[w][o]
+    //                     - x_{m,em} (G2[e][n][o] G[mu][l] G[nu][m] + G[e][n] G2[mu][l][o] G[nu][m] + G[e][n] G[mu][l] G2[nu][m][o])
+    // evaluated with the spatial-index tensors H2 = x_{m,em} G G and H3 = x_{m,emw} G G G first
+    double H2[DIM][DIM][DIM] = {}, G2[DIM][DIM][DIM] = {};
+    for (int m = 0; m < DIM; m++)
+        for (int n = 0; n < DIM; n++)
+            for (int l = 0; l < DIM; l++) {
+                double v = 0.0;
+                for (int ep = 0; ep < DIM; ep++)
+                    for (int mu = 0; mu < DIM; mu++) v += X2[m][ep][mu] * G[ep][n] * G[mu][l];
+                H2[m][n][l] = v;
+            }
+    for (int nu = 0; nu < DIM; nu++)
+        for (int n = 0; n < DIM; n++)
+            for (int l = 0; l < DIM; l++) {
+                double v = 0.0;
+                for (int m = 0; m < DIM; m++) v -= G[nu][m] * H2[m][n][l];
+                G2[nu][n][l] = v;
+            }
+    double G3[DIM][DIM][DIM][DIM] = {};
+    if (order >= 3) {
+        for (int nu = 0; nu < DIM; nu++)
+            for (int n = 0; n < DIM; n++)
+                for (int l = 0; l < DIM; l++)
+                    for (int o = 0; o < DIM; o++) {
+                        double v = 0.0;
+                        for (int m = 0; m < DIM; m++) {
+                            double h3 = 0.0, mix = 0.0;
+                            for (int ep = 0; ep < DIM; ep++)
+                                for (int mu = 0; mu < DIM; mu++) {
+                                    double x3 = 0.0;
+                                    for (int om = 0; om < DIM; om++) x3 += X3[m][ep][mu][om] * G[om][o];
+                                    h3 += x3 * G[ep][n] * G[mu][l];
+                                    mix += X2[m][ep][mu] * (G2[ep][n][o] * G[mu][l] + G[ep][n] * G2[mu][l][o]);
+                                }
+                            v -= G[nu][m] * (h3 + mix) + G2[nu][m][o] * H2[m][n][l];
+                        }
+                        G3[nu][n][l][o] = v;
+                    }
+    }
+    // ---- pass 3: push-forward (dspatial) P:309, (ddspatial) P:310, (dddspatial) P:311-315 ----
+    const int nq_el_ = nq_el;
+    double *base = out + (size_t)el * P.nen * ncomp * nq_el_ + q;
+    for (int A = 0; A < P.nen; A++) {
+        double r0, r1[DIM], r2[DIM][DIM], r3[DIM][DIM][DIM];
+        long long node;
+        rational3(A, r0, r1, r2, r3, node);
+        double *o = base + (size_t)A * ncomp * nq_el_;
+        int c = 0;
+        o[(c++) * nq_el_] = r0;
+        if (order >= 1)
+            for (int i = 0; i < DIM; i++) {
+                double v = 0.0;
+                for (int al = 0; al < DIM; al++) v += r1[al] * G[al][i];
+                o[(c++) * nq_el_] = v;
+            }
+        if (order >= 2)
+            for (int i = 0; i < DIM; i++)
+                for (int j = 0; j < DIM; j++) {
+                    double v = 0.0;
+                    for (int al = 0; al < DIM; al++) {
+                        for (int be = 0; be < DIM; be++) v += r2[al][be] * G[al][i] * G[be][j];
+                        v += r1[al] * G2[al][i][j];
+                    }
+                    o[(c++) * nq_el_] = v;
+                }
+        if (order >= 3)
+            for (int i = 0; i < DIM; i++)
+                for (int j = 0; j < DIM; j++)
+                    for (int k = 0; k < DIM; k++) {
+                        double v = 0.0;
+                        for (int al = 0; al < DIM; al++) {
+                            for (int be = 0; be < DIM; be++) {
+                                for (int ga = 0; ga < DIM; ga++) v += r3[al][be][ga] * G[al][i] * G[be][j] * G[ga][k];
+                                v += r2[al][be] * (G[al][i] * G2[be][j][k] + G[be][j] * G2[al][i][k] + G[be][k] * G2[al][i][j]);
+                            }
+                            v += r1[al] * G3[al][i][j][k];
+                        }
+                        o[(c++) * nq_el_] = v;
+                    }
+    }
+}
+
+iga_status launch_basis3(iga_space_s *s, int order, double *out, cudaStream_t st) {
+    if (order < 0 || order > 3) { set_error("order must be 0..3"); return IGA_ERR_PARAM; }
+    int nq_el = 1, ncomp = 0;
+    for (int d = 0; d < s->dim; d++) nq_el *= s->nq[d];
+    for (int k = 0, t = 1; k <= order; k++, t *= s->dim) ncomp += t;
+    const long long n = s->nel_local * nq_el;
+    if (n == 0) return IGA_OK;
+    {
+        ProfScope ps(s, "k_basis3", st);
+        const unsigned blocks = (unsigned)((n + 127) / 128);
+        if (s->dim == 2) k_basis3<2><<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out);
+        else k_basis3<3><<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out);
+    }
+    s->last_launches = 1;
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) { set_error(std::string("basis3: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return IGA_OK;
+}
+
+}  // namespace iga

@@ -84,6 +84,7 @@ iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b
 iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st);
+iga_status launch_basis3(iga_space_s *s, int order, double *out, cudaStream_t st);   // basis3.cu
 // dist.cu
 iga_status dist_setup(iga_space_s *s, const iga_dist *dist);
 void dist_destroy(iga_space_s *s);

@@ -502,6 +502,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             if ((st = upload(s, (int **)&ax.supcnt, one_i)) != IGA_OK) goto fail;
             if ((st = upload(s, (int **)&ax.posd, z)) != IGA_OK) goto fail;
             if ((st = upload(s, (long long **)&ax.lS, zl)) != IGA_OK) goto fail;
+            if ((st = upload(s, (double **)&ax.knots, x0)) != IGA_OK) goto fail;
             ax.n_own = 1; ax.x_n = 1; ax.Th = 0;
             ax.uni_lo = 0; ax.uni_hi = 1;
             ax.uniform = 1;
@@ -539,6 +540,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         double *dU = nullptr;
         double *dtab = nullptr;
         if ((st = upload(s, &dU, U)) != IGA_OK) goto fail;
+        ax.knots = dU;
         if ((st = upload(s, (double **)&ax.qw, qw)) != IGA_OK) goto fail;
         if ((st = upload(s, (double **)&ax.qx, qx)) != IGA_OK) goto fail;
         if ((st = upload(s, (double **)&ax.hpar, hpar)) != IGA_OK) goto fail;
@@ -843,6 +845,16 @@ iga_status iga_dist_plan(const iga_space_desc *desc, const iga_dist *dist, int64
                          int64_t el_lo[3], int64_t el_hi[3], int64_t ext_n[3], int max_msgs, iga_msg *send, int *nsend,
                          iga_msg *recv, int *nrecv) {
     return dist_plan_host(desc, dist, own_lo, own_hi, el_lo, el_hi, ext_n, max_msgs, send, nsend, recv, nrecv);
+}
+
+iga_status iga_basis_eval(iga_space s, int order, double *out, void *stream) {
+    if (!s || !out) { set_error("null argument"); return IGA_ERR_PARAM; }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    iga_status st = launch_basis3(s, order, out, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
 }
 
 iga_status iga_nccl_unique_id(unsigned char out[128]) {
