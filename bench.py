@@ -413,8 +413,52 @@ def run_iga(args, w, ws, rank, local):
     return 0
 
 
+def run_basis3(args, w, local):
+    """Secondary measurement: iga_basis_eval, all spatial derivatives up to
+    third order of every local basis function at every Gauss point.  HBM-write-bound: the
+    algorithmic bytes are the output tensor (8 B x nen x ncomp x nqp)."""
+    import torch
+    import paper_1305_4452_b200 as iga
+    torch.cuda.set_device(local)
+    sp = iga.Space.from_workload(w, device=local)
+    out = sp.basis_eval(3)
+    sp.check()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=out.device)
+    for _ in range(args.warmup):
+        sp.basis_eval(3, out=out)
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sp.basis_eval(3, out=out)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+    sp.check()
+    t = statistics.mean(ms)
+    nbytes = out.numel() * 8
+    peaks = load_peaks()
+    bw = peaks.get("hbm_gbs", 6650.0)
+    achieved = nbytes / (t * 1e-3) / 1e9
+    print(json.dumps({
+        "metric": "third-order basis evaluation quadrature points/sec (fp64)", "value": sp.nqp / (t * 1e-3),
+        "unit": "qpts/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t,
+        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "op": "iga_basis_eval(order=3)", "out_shape": list(out.shape),
+                   "l2": "flushed (512 MiB write) between steps"},
+        "roofline": {"bound": "hbm", "kernel": "k_basis3", "achieved": achieved, "peak": bw, "unit": "GB/s",
+                     "frac": achieved / bw, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "clocks": clk.summary()}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--op", default="jacobian", choices=["jacobian", "basis3"],
+                    help="jacobian: the headline assembly step; basis3: third-order basis evaluation")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
@@ -429,6 +473,8 @@ def main():
     w = workloads.make(args.config, n=args.n)
     if args.impl == "reference":
         return run_reference(args, w, ws, rank)
+    if args.op == "basis3":
+        return run_basis3(args, w, local)
     return run_iga(args, w, ws, rank, local)
 
 

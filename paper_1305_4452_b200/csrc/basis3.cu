@@ -72,18 +72,17 @@ __device__ void span_ders3(int span, double xi, int p, const double *__restrict_
 template <int DIM>
 struct Pt3 {
     double v[DIM][4][B3P];   // univariate N..N''' per axis
-    int g[DIM], nen, np1[DIM];
+    int g[DIM];
 };
 
-// parametric derivatives of the tensor-product B-spline M_A up to third order
+// parametric derivatives of the tensor-product B-spline M_A up to third order from the function's
+// univariate values f[d][k] = N^(k) along axis d
 template <int DIM>
-__device__ __forceinline__ void tensor3(const Pt3<DIM> &P, const int aa[3], double &m0, double m1[DIM],
-                                        double m2[DIM][DIM], double m3[DIM][DIM][DIM]) {
+__device__ __forceinline__ void tensor3(const double (&f)[DIM][4], double &m0, double m1[DIM], double m2[DIM][DIM],
+                                        double m3[DIM][DIM][DIM]) {
     auto val = [&](int c0, int c1, int c2) {
-        double r = 1.0;
-        const int c[3] = {c0, c1, c2};
-#pragma unroll
-        for (int d = 0; d < DIM; d++) r *= P.v[d][c[d]][aa[d]];
+        double r = f[0][c0] * f[1][c1];
+        if constexpr (DIM == 3) r *= f[2][c2];
         return r;
     };
     m0 = val(0, 0, 0);
@@ -107,9 +106,10 @@ __device__ __forceinline__ void tensor3(const Pt3<DIM> &P, const int aa[3], doub
     }
 }
 
-template <int DIM>
+template <int DIM, int PP>
 __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long nelem, int nq_el, int ncomp,
                                                 double *__restrict__ out) {
+    constexpr int NP1 = PP + 1, NEN = DIM == 2 ? NP1 * NP1 : NP1 * NP1 * NP1;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nelem * nq_el) return;
     const long long el = t / nq_el;
@@ -127,42 +127,55 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
         }
     }
     Pt3<DIM> P;
-    P.nen = 1;
+#pragma unroll
     for (int d = 0; d < DIM; d++) {
         const AxisDev &ax = s.ax[d];
         const int first = ax.first[e[d]];
         P.g[d] = first;
-        P.np1[d] = ax.p + 1;
-        P.nen *= ax.p + 1;
-        span_ders3(first + ax.p, ax.qx[(size_t)e[d] * ax.nq + qd[d]], ax.p, ax.knots, P.v[d]);
+        span_ders3(first + PP, ax.qx[(size_t)e[d] * ax.nq + qd[d]], PP, ax.knots, P.v[d]);
     }
     const bool rational = s.mode == MODE_NURBS;
     const bool geom = s.geom == IGA_GEOM_NURBS;
     auto decode = [&](int A, int aa[3], long long &node) {
         int r = A;
         int g[3] = {0, 0, 0};
+#pragma unroll
         for (int d = DIM - 1; d >= 0; d--) {
-            aa[d] = r % P.np1[d];
-            r /= P.np1[d];
+            aa[d] = r % NP1;
+            r /= NP1;
             g[d] = P.g[d] + aa[d];
             if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
         }
         node = node_index(s, g[0], g[1], g[2]);
     };
+    auto fvals = [&](const int aa[3], double (&f)[DIM][4]) {     // select, no dynamic indexing
+#pragma unroll
+        for (int d = 0; d < DIM; d++)
+#pragma unroll
+            for (int a = 0; a < NP1; a++)
+                if (a == aa[d])
+#pragma unroll
+                    for (int k = 0; k < 4; k++) f[d][k] = P.v[d][k][a];
+    };
     // ---- pass 1: w and its parametric derivatives ----
     double w0 = 0.0, w1[DIM] = {}, w2[DIM][DIM] = {}, w3[DIM][DIM][DIM] = {};
-    for (int A = 0; A < P.nen; A++) {
+#pragma unroll 1
+    for (int A = 0; A < NEN; A++) {
         int aa[3] = {0, 0, 0};
         long long node;
         decode(A, aa, node);
         const double wA = (rational && s.wts) ? s.wts[node] : 1.0;
-        double m0, m1[DIM], m2[DIM][DIM], m3[DIM][DIM][DIM];
-        tensor3<DIM>(P, aa, m0, m1, m2, m3);
+        double m0, m1[DIM], m2[DIM][DIM], m3[DIM][DIM][DIM], f[DIM][4];
+        fvals(aa, f);
+        tensor3<DIM>(f, m0, m1, m2, m3);
         w0 += wA * m0;
+        #pragma unroll
         for (int al = 0; al < DIM; al++) {
             w1[al] += wA * m1[al];
+            #pragma unroll
             for (int be = 0; be < DIM; be++) {
                 w2[al][be] += wA * m2[al][be];
+                #pragma unroll
                 for (int ga = 0; ga < DIM; ga++) w3[al][be][ga] += wA * m3[al][be][ga];
             }
         }
@@ -173,15 +186,22 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
         int aa[3] = {0, 0, 0};
         decode(A, aa, node);
         const double wA = (rational && s.wts) ? s.wts[node] : 1.0;
-        double m0, m1[DIM], m2[DIM][DIM], m3[DIM][DIM][DIM];
-        tensor3<DIM>(P, aa, m0, m1, m2, m3);
+        double m0, m1[DIM], m2[DIM][DIM], m3[DIM][DIM][DIM], f[DIM][4];
+        fvals(aa, f);
+        tensor3<DIM>(f, m0, m1, m2, m3);
         r0 = wA * m0 * iw;
+        #pragma unroll
         for (int al = 0; al < DIM; al++) r1[al] = (wA * m1[al] - r0 * w1[al]) * iw;
+        #pragma unroll
         for (int al = 0; al < DIM; al++)
+            #pragma unroll
             for (int be = 0; be < DIM; be++)
                 r2[al][be] = (wA * m2[al][be] - r0 * w2[al][be] - r1[be] * w1[al] - r1[al] * w1[be]) * iw;
+        #pragma unroll
         for (int al = 0; al < DIM; al++)
+            #pragma unroll
             for (int be = 0; be < DIM; be++)
+                #pragma unroll
                 for (int ga = 0; ga < DIM; ga++)
                     r3[al][be][ga] = (wA * m3[al][be][ga] - r0 * w3[al][be][ga]
                                       - r1[al] * w2[be][ga] - r1[be] * w2[al][ga] - r1[ga] * w2[al][be]
@@ -190,22 +210,28 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
     // ---- pass 2: the map x and its parametric derivatives ----
     double X1[DIM][DIM] = {}, X2[DIM][DIM][DIM] = {}, X3[DIM][DIM][DIM][DIM] = {};
     if (geom) {
-        for (int A = 0; A < P.nen; A++) {
+#pragma unroll 1
+        for (int A = 0; A < NEN; A++) {
             double r0, r1[DIM], r2[DIM][DIM], r3[DIM][DIM][DIM];
             long long node;
             rational3(A, r0, r1, r2, r3, node);
+            #pragma unroll
             for (int m = 0; m < DIM; m++) {
                 const double xb = s.ctrl[node * DIM + m];
+                #pragma unroll
                 for (int al = 0; al < DIM; al++) {
                     X1[m][al] += xb * r1[al];
+                    #pragma unroll
                     for (int be = 0; be < DIM; be++) {
                         X2[m][al][be] += xb * r2[al][be];
+                        #pragma unroll
                         for (int ga = 0; ga < DIM; ga++) X3[m][al][be][ga] += xb * r3[al][be][ga];
                     }
                 }
             }
         }
     } else {
+        #pragma unroll
         for (int m = 0; m < DIM; m++) X1[m][m] = 1.0;
     }
     // inverse map G[al][i] = xi_{al,i}, by cofactors
@@ -234,33 +260,50 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
     //                     - x_{m,em} (G2[e][n][o] G[mu][l] G[nu][m] + G[e][n] G2[mu][l][o] G[nu][m] + G[e][n] G[mu][l] G2[nu][m][o])
     // evaluated with the spatial-index tensors H2 = x_{m,em} G G and H3 = x_{m,emw} G G G first
     double H2[DIM][DIM][DIM] = {}, G2[DIM][DIM][DIM] = {};
+    #pragma unroll
     for (int m = 0; m < DIM; m++)
+        #pragma unroll
         for (int n = 0; n < DIM; n++)
+            #pragma unroll
             for (int l = 0; l < DIM; l++) {
                 double v = 0.0;
+                #pragma unroll
                 for (int ep = 0; ep < DIM; ep++)
+                    #pragma unroll
                     for (int mu = 0; mu < DIM; mu++) v += X2[m][ep][mu] * G[ep][n] * G[mu][l];
                 H2[m][n][l] = v;
             }
+    #pragma unroll
     for (int nu = 0; nu < DIM; nu++)
+        #pragma unroll
         for (int n = 0; n < DIM; n++)
+            #pragma unroll
             for (int l = 0; l < DIM; l++) {
                 double v = 0.0;
+                #pragma unroll
                 for (int m = 0; m < DIM; m++) v -= G[nu][m] * H2[m][n][l];
                 G2[nu][n][l] = v;
             }
     double G3[DIM][DIM][DIM][DIM] = {};
     if (order >= 3) {
+        #pragma unroll
         for (int nu = 0; nu < DIM; nu++)
+            #pragma unroll
             for (int n = 0; n < DIM; n++)
+                #pragma unroll
                 for (int l = 0; l < DIM; l++)
+                    #pragma unroll
                     for (int o = 0; o < DIM; o++) {
                         double v = 0.0;
+                        #pragma unroll
                         for (int m = 0; m < DIM; m++) {
                             double h3 = 0.0, mix = 0.0;
+                            #pragma unroll
                             for (int ep = 0; ep < DIM; ep++)
+                                #pragma unroll
                                 for (int mu = 0; mu < DIM; mu++) {
                                     double x3 = 0.0;
+                                    #pragma unroll
                                     for (int om = 0; om < DIM; om++) x3 += X3[m][ep][mu][om] * G[om][o];
                                     h3 += x3 * G[ep][n] * G[mu][l];
                                     mix += X2[m][ep][mu] * (G2[ep][n][o] * G[mu][l] + G[ep][n] * G2[mu][l][o]);
@@ -272,8 +315,9 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
     }
     // ---- pass 3: push-forward (dspatial) P:309, (ddspatial) P:310, (dddspatial) P:311-315 ----
     const int nq_el_ = nq_el;
-    double *base = out + (size_t)el * P.nen * ncomp * nq_el_ + q;
-    for (int A = 0; A < P.nen; A++) {
+    double *base = out + (size_t)el * NEN * ncomp * nq_el_ + q;
+#pragma unroll 1
+    for (int A = 0; A < NEN; A++) {
         double r0, r1[DIM], r2[DIM][DIM], r3[DIM][DIM][DIM];
         long long node;
         rational3(A, r0, r1, r2, r3, node);
@@ -281,28 +325,40 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
         int c = 0;
         o[(c++) * nq_el_] = r0;
         if (order >= 1)
+            #pragma unroll
             for (int i = 0; i < DIM; i++) {
                 double v = 0.0;
+                #pragma unroll
                 for (int al = 0; al < DIM; al++) v += r1[al] * G[al][i];
                 o[(c++) * nq_el_] = v;
             }
         if (order >= 2)
+            #pragma unroll
             for (int i = 0; i < DIM; i++)
+                #pragma unroll
                 for (int j = 0; j < DIM; j++) {
                     double v = 0.0;
+                    #pragma unroll
                     for (int al = 0; al < DIM; al++) {
+                        #pragma unroll
                         for (int be = 0; be < DIM; be++) v += r2[al][be] * G[al][i] * G[be][j];
                         v += r1[al] * G2[al][i][j];
                     }
                     o[(c++) * nq_el_] = v;
                 }
         if (order >= 3)
+            #pragma unroll
             for (int i = 0; i < DIM; i++)
+                #pragma unroll
                 for (int j = 0; j < DIM; j++)
+                    #pragma unroll
                     for (int k = 0; k < DIM; k++) {
                         double v = 0.0;
+                        #pragma unroll
                         for (int al = 0; al < DIM; al++) {
+                            #pragma unroll
                             for (int be = 0; be < DIM; be++) {
+                                #pragma unroll
                                 for (int ga = 0; ga < DIM; ga++) v += r3[al][be][ga] * G[al][i] * G[be][j] * G[ga][k];
                                 v += r2[al][be] * (G[al][i] * G2[be][j][k] + G[be][j] * G2[al][i][k] + G[be][k] * G2[al][i][j]);
                             }
@@ -323,8 +379,16 @@ iga_status launch_basis3(iga_space_s *s, int order, double *out, cudaStream_t st
     {
         ProfScope ps(s, "k_basis3", st);
         const unsigned blocks = (unsigned)((n + 127) / 128);
-        if (s->dim == 2) k_basis3<2><<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out);
-        else k_basis3<3><<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out);
+        const int p = s->p[0];
+        for (int d = 1; d < s->dim; d++)
+            if (s->p[d] != p) { set_error("basis3: equal degrees per axis in this build"); return IGA_ERR_PARAM; }
+        if (p < 1 || p > 3) { set_error("basis3: degree 1..3"); return IGA_ERR_PARAM; }
+        auto go = [&](auto kern) { kern<<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out); };
+        if (s->dim == 2) {
+            if (p == 1) go(k_basis3<2, 1>); else if (p == 2) go(k_basis3<2, 2>); else go(k_basis3<2, 3>);
+        } else {
+            if (p == 1) go(k_basis3<3, 1>); else if (p == 2) go(k_basis3<3, 2>); else go(k_basis3<3, 3>);
+        }
     }
     s->last_launches = 1;
     cudaError_t ce = cudaGetLastError();
