@@ -108,7 +108,8 @@ __device__ __forceinline__ void tensor3(const double (&f)[DIM][4], double &m0, d
 
 template <int DIM, int PP>
 __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long nelem, int nq_el, int ncomp,
-                                                double *__restrict__ out) {
+                                                double *__restrict__ out, const double *__restrict__ kn0,
+                                                const double *__restrict__ kn1, const double *__restrict__ kn2) {
     constexpr int NP1 = PP + 1, NEN = DIM == 2 ? NP1 * NP1 : NP1 * NP1 * NP1;
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nelem * nq_el) return;
@@ -132,7 +133,7 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
         const AxisDev &ax = s.ax[d];
         const int first = ax.first[e[d]];
         P.g[d] = first;
-        span_ders3(first + PP, ax.qx[(size_t)e[d] * ax.nq + qd[d]], PP, ax.knots, P.v[d]);
+        span_ders3(first + PP, ax.qx[(size_t)e[d] * ax.nq + qd[d]], PP, d == 0 ? kn0 : d == 1 ? kn1 : kn2, P.v[d]);
     }
     const bool rational = s.mode == MODE_NURBS;
     const bool geom = s.geom == IGA_GEOM_NURBS;
@@ -383,7 +384,9 @@ iga_status launch_basis3(iga_space_s *s, int order, double *out, cudaStream_t st
         for (int d = 1; d < s->dim; d++)
             if (s->p[d] != p) { set_error("basis3: equal degrees per axis in this build"); return IGA_ERR_PARAM; }
         if (p < 1 || p > 3) { set_error("basis3: degree 1..3"); return IGA_ERR_PARAM; }
-        auto go = [&](auto kern) { kern<<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out); };
+        auto go = [&](auto kern) {
+            kern<<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out, s->dknots[0], s->dknots[1], s->dknots[2]);
+        };
         if (s->dim == 2) {
             if (p == 1) go(k_basis3<2, 1>); else if (p == 2) go(k_basis3<2, 2>); else go(k_basis3<2, 3>);
         } else {

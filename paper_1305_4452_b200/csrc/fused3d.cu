@@ -373,8 +373,10 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         s2[a0][a1][o] = t;
                     }
                     double t = 0.0;
+                    if constexpr (PH::UDOT) {
 #pragma unroll
-                    for (int a2 = 0; a2 < NP1; a2++) t += v2[0][a2] * sUd[((a0 * NP1 + a1) * NP1 + a2) * M + m];
+                        for (int a2 = 0; a2 < NP1; a2++) t += v2[0][a2] * sUd[((a0 * NP1 + a1) * NP1 + a2) * M + m];
+                    }
                     d2[a0][a1] = t;
                 }
             // stage a1: s1[a0][o1][o2] (unused order pairs are dead code)

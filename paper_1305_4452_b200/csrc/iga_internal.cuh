@@ -23,7 +23,6 @@ struct AxisDev {
     int nu;           // unique functions (periodic identification, SURVEY A-8)
     int nq;           // Gauss points per element
     const double *tab;        // [nel][nq][3][p+1]  N, N', N'' of the span's p+1 functions
-    const double *knots;      // unclamped knot vector (third-order basis evaluation)
     const double *qw;         // [nel][nq]  Gauss weight * (h_e / 2)
     const double *qx;         // [nel][nq]  parametric coordinate of the Gauss point
     const double *hpar;       // [nel]      span length h_e

@@ -36,6 +36,7 @@ struct Fields {
 struct PhysLaplace {
     static constexpr int M = 1;
     static constexpr bool HESS = false;
+    static constexpr bool UDOT = false;       // residual depends on the time derivative
     template <int DIM> static constexpr int NK() { return 1 + DIM; }
     template <int DIM> static constexpr bool dmask(int k, int i, int k2, int j) { return k == k2 && i == 0 && j == 0; }
     static constexpr bool rmask(int k, int i) { return i == 0; }
@@ -76,6 +77,7 @@ struct PhysLaplace {
 struct PhysCahnHilliard {
     static constexpr int M = 1;
     static constexpr bool HESS = true;
+    static constexpr bool UDOT = true;       // residual depends on the time derivative
     template <int DIM> static constexpr int NK() { return 2 + DIM; }
     // structural D for DIM up to 3 (kinds: 0 N, 1..3 grad, last lap); lap index passed as L
     static constexpr bool dmask_d(int k, int k2, int L) {
@@ -141,6 +143,7 @@ struct PhysCahnHilliard {
 struct PhysNeoHooke {
     static constexpr int M = 3;
     static constexpr bool HESS = false;
+    static constexpr bool UDOT = false;       // residual depends on the time derivative
     template <int DIM> static constexpr int NK() { return 1 + DIM; }
     template <int DIM> static constexpr bool dmask(int k, int i, int k2, int j) { return k >= 1 && k2 >= 1; }
     static constexpr bool rmask(int k, int i) { return k >= 1; }
@@ -227,6 +230,7 @@ struct PhysNeoHooke {
 struct PhysNSVMS {
     static constexpr int M = 4;
     static constexpr bool HESS = true;
+    static constexpr bool UDOT = true;       // residual depends on the time derivative
     template <int DIM> static constexpr int NK() { return 5; }
     // exact structural pattern (derived in DESIGN.md; 192 entries)
     template <int DIM> static constexpr bool dmask(int k, int i, int k2, int j) {

@@ -87,7 +87,7 @@ __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, d
             const double uA = (MODE == MODE_NURBS && Nodes::PREMUL) ? nodes.u(A, m) : wA * nodes.u(A, m);
 #pragma unroll
             for (int c = 0; c < NC; c++) Phi[m][c] += uA * Pc[c];
-            if (nodes.has_ud())
+            if (PH::UDOT && nodes.has_ud())
                 Phit[m] += ((MODE == MODE_NURBS && Nodes::PREMUL) ? nodes.ud(A, m) : wA * nodes.ud(A, m)) * Pc[0];
         }
     };

@@ -502,7 +502,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             if ((st = upload(s, (int **)&ax.supcnt, one_i)) != IGA_OK) goto fail;
             if ((st = upload(s, (int **)&ax.posd, z)) != IGA_OK) goto fail;
             if ((st = upload(s, (long long **)&ax.lS, zl)) != IGA_OK) goto fail;
-            if ((st = upload(s, (double **)&ax.knots, x0)) != IGA_OK) goto fail;
+            if ((st = upload(s, (double **)&s->dknots[a], x0)) != IGA_OK) goto fail;
             ax.n_own = 1; ax.x_n = 1; ax.Th = 0;
             ax.uni_lo = 0; ax.uni_hi = 1;
             ax.uniform = 1;
@@ -540,7 +540,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         double *dU = nullptr;
         double *dtab = nullptr;
         if ((st = upload(s, &dU, U)) != IGA_OK) goto fail;
-        ax.knots = dU;
+        s->dknots[a] = dU;
         if ((st = upload(s, (double **)&ax.qw, qw)) != IGA_OK) goto fail;
         if ((st = upload(s, (double **)&ax.qx, qx)) != IGA_OK) goto fail;
         if ((st = upload(s, (double **)&ax.hpar, hpar)) != IGA_OK) goto fail;
