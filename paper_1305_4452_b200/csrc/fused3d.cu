@@ -114,9 +114,9 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
             for (int x = 0; x < NP1; x++)
 #pragma unroll
                 for (int y = 0; y < NP1; y++) Tt[o][x][y] = 0.0;
-        // VMS (m = 4) keeps the q1 loop rolled: fully unrolled it spills at 255 registers
-        constexpr int UNROLL_Q1 = F::M >= 4 ? 1 : NQ1;
-#pragma unroll UNROLL_Q1
+        // q1 loop rolled: unrolled, VMS spills at 255 registers and Neo-Hooke (168-register cap of
+        // 3 CTAs/SM) misses in the instruction cache (A/B: 208 vs 216 ms, 10.1 vs 10.6 ms)
+#pragma unroll 1
         for (int q1 = 0; q1 < NQ1; q1++) {
             double n1[3];
 #pragma unroll
