@@ -197,7 +197,7 @@ def run_reference(args, w, ws, rank):
               f"{r['nvisited']} elements x {nq} qpts per step, single-threaded C oracle")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": w.name, "nqp_per_step": int(qp[0]), "l2": "host"},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -387,7 +387,8 @@ def run_iga(args, w, ws, rank, local):
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "nqp": sp.nqp, "nelem": w.nelem, "ndof": sp.ndof, "nnz": sp.nnz,
                    "degree": w.degree[0], "dof_per_node": w.dof, "l2": "flushed (512 MiB write) between steps",
@@ -467,10 +468,18 @@ def main():
     ap.add_argument("--impl", default="iga", choices=["iga", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="libiga option key=value (experiments)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="--gpus N > 1: weak = every GPU keeps the named config's element count (the global "
+                         "mesh grows with the box decomposition); strong = the named mesh is split N ways")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "iga" else args.warmup
     ws, rank, local = dist_env()
-    w = workloads.make(args.config, n=args.n)
+    n = args.n
+    if ws > 1 and args.scaling == "weak":
+        dim = 2 if args.config <= 3 else 3
+        base = n if n is not None else workloads.FULL_N[args.config]
+        n = [base * f for f in box_procs(ws, dim)]
+    w = workloads.make(args.config, n=n)
     if args.impl == "reference":
         return run_reference(args, w, ws, rank)
     if args.op == "basis3":

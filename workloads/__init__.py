@@ -129,16 +129,27 @@ def annulus_geometry(U0: np.ndarray, U1: np.ndarray, p: int = 3):
     return ctrl, weights
 
 
-def make(cid: int, n: int | None = None, seed: int | None = None) -> Workload:
-    """Build config `cid` (1..5) with n elements per axis (default: the full BASELINE size)."""
+def make(cid: int, n=None, seed: int | None = None) -> Workload:
+    """Build config `cid` (1..5) with n elements per axis (default: the full BASELINE size); n may
+    be a list with one count per axis (weak-scaling meshes of bench.py --gpus N)."""
+    dims = {1: 2, 2: 2, 3: 2, 4: 3, 5: 3}[cid] if cid in (1, 2, 3, 4, 5) else 0
     if n is None:
         n = FULL_N[cid]
+    nn = list(n) if isinstance(n, (list, tuple)) else [int(n)] * dims
+    w = _make(cid, nn, seed)
+    if any(x != nn[0] for x in nn) or nn[0] != FULL_N.get(cid):
+        w.name = NAMES[cid].rsplit("_", 1)[0] + "_" + "x".join(str(x) for x in nn)
+    return w
+
+
+def _make(cid: int, nn: list, seed: int | None = None) -> Workload:
+    n = nn[0]
     if seed is None:
         seed = cid
     rng = np.random.default_rng(seed)
     if cid == 1:
         p, d = 2, 2
-        U = [open_uniform_knots(p, n) for _ in range(d)]
+        U = [open_uniform_knots(p, nn[a]) for a in range(d)]
         g = [_greville(u, p) for u in U]
         nf = [len(x) for x in g]
         ctrl = np.zeros((nf[0], nf[1], 2))
@@ -146,29 +157,29 @@ def make(cid: int, n: int | None = None, seed: int | None = None) -> Workload:
         ctrl[:, :, 1] = g[1][None, :]
         w = Workload(1, NAMES[1], d, [p] * d, U, [0] * d, [p - 1] * d, 1, [p + 1] * d, GEOM_NURBS,
                      ctrl, np.ones(nf), PHYS_LAPLACE, [1.0, 0.0, 1.0], 0.0, 1.0,
-                     np.zeros(nf[0] * nf[1]), np.zeros(nf[0] * nf[1]), [n] * d, nf)
+                     np.zeros(nf[0] * nf[1]), np.zeros(nf[0] * nf[1]), list(nn), nf)
     elif cid == 2:
         p, d = 3, 2
-        U = [open_uniform_knots(p, n) for _ in range(d)]
+        U = [open_uniform_knots(p, nn[a]) for a in range(d)]
         ctrl, weights = annulus_geometry(U[0], U[1], p)
         nf = [ctrl.shape[0], ctrl.shape[1]]
         nd = nf[0] * nf[1]
         w = Workload(2, NAMES[2], d, [p] * d, U, [0] * d, [p - 1] * d, 1, [p + 1] * d, GEOM_NURBS,
                      ctrl, weights, PHYS_LAPLACE, [1.0, 1.0, 0.0], 0.0, 1.0,
-                     rng.uniform(-1.0, 1.0, nd), np.zeros(nd), [n] * d, nf)
+                     rng.uniform(-1.0, 1.0, nd), np.zeros(nd), list(nn), nf)
     elif cid == 3:
         p, d = 2, 2
-        U = [open_uniform_knots(p, n) for _ in range(d)]
-        nf = [n, n]
-        nd = n * n
+        U = [open_uniform_knots(p, nn[a]) for a in range(d)]
+        nf = [nn[0], nn[1]]
+        nd = nf[0] * nf[1]
         c = 0.63 + rng.uniform(-0.05, 0.05, nd)
         dt = 1e-6
         w = Workload(3, NAMES[3], d, [p] * d, U, [1] * d, [p - 1] * d, 1, [p + 1] * d, GEOM_PARAMETRIC,
                      None, None, PHYS_CAHN_HILLIARD, [1.5, 3000.0], 5.0 / 6.0, (4.0 / 9.0) * dt,
-                     c, np.zeros(nd), [n] * d, nf)
+                     c, np.zeros(nd), list(nn), nf)
     elif cid == 4:
         p, d = 2, 3
-        U = [open_uniform_knots(p, n) for _ in range(d)]
+        U = [open_uniform_knots(p, nn[a]) for a in range(d)]
         g = [_greville(u, p) for u in U]
         nf = [len(x) for x in g]
         # A-22: idx, phi, amplitude drawn in this order from default_rng(4)
@@ -188,13 +199,13 @@ def make(cid: int, n: int | None = None, seed: int | None = None) -> Workload:
         mu = E / (2 * (1 + nu))
         w = Workload(4, NAMES[4], d, [p] * d, U, [0] * d, [p - 1] * d, 3, [p + 1] * d, GEOM_PARAMETRIC,
                      None, None, PHYS_NEOHOOKE, [lam, mu], 0.0, 1.0,
-                     disp.reshape(-1).copy(), np.zeros(disp.size), [n] * d, nf)
+                     disp.reshape(-1).copy(), np.zeros(disp.size), list(nn), nf)
     elif cid == 5:
         p, d = 2, 3
         L = 2.0 * math.pi
-        U = [open_uniform_knots(p, n, 0.0, L) for _ in range(d)]
-        g = _periodic_greville(0.0, L, n, p)
-        x, y, z = np.meshgrid(g, g, g, indexing="ij")
+        U = [open_uniform_knots(p, nn[a], 0.0, L) for a in range(d)]
+        gs = [_periodic_greville(0.0, L, nn[a], p) for a in range(d)]
+        x, y, z = np.meshgrid(gs[0], gs[1], gs[2], indexing="ij")
         vel = np.stack([np.sin(x) * np.cos(y) * np.cos(z),
                         -np.cos(x) * np.sin(y) * np.cos(z),
                         np.zeros_like(x)], axis=-1)
@@ -204,7 +215,7 @@ def make(cid: int, n: int | None = None, seed: int | None = None) -> Workload:
         dt = 1e-2
         w = Workload(5, NAMES[5], d, [p] * d, U, [1] * d, [p - 1] * d, 4, [p + 1] * d, GEOM_PARAMETRIC,
                      None, None, PHYS_NS_VMS, [1.0 / 1600.0, dt, 4.0, 36.0], 5.0 / 6.0, (4.0 / 9.0) * dt,
-                     Uarr, np.zeros(Uarr.size), [n] * d, [n] * d)
+                     Uarr, np.zeros(Uarr.size), list(nn), list(nn))
     else:
         raise ValueError(f"unknown config {cid}")
     return w
