@@ -307,8 +307,8 @@ static iga_status run_form(iga_space_s *s, const iga_phys *phys, double a, doubl
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
     int launches = 0;
-    if (jac) launches += zero_launch(s, val, s->nnz_owned, st, nsm);
-    if (F) launches += zero_launch(s, F, s->nrows_owned, st, nsm);
+    if (jac && !s->skip_zero) launches += zero_launch(s, val, s->nnz_owned, st, nsm);
+    if (F && !s->skip_zero) launches += zero_launch(s, F, s->nrows_owned, st, nsm);
     const size_t per_el = (size_t)NQ * ((jac ? L::NE : 0) + (F ? L::NR : 0)) * sizeof(double);
     long long nb_max = per_el ? (long long)(s->work_bytes / per_el) : s->nel_local;
     if (nb_max < 1) { set_error("workspace too small"); return IGA_ERR_NOMEM; }
@@ -411,6 +411,40 @@ iga_status launch_form(iga_space_s *s, const iga_phys *ph, double a, double b, c
     }
     set_error("physics / dim / dof combination not supported");
     return IGA_ERR_PARAM;
+}
+
+// Element sub-box launch (multi-rank schedule, dist.cu): the kernels take their element range
+// from the space (SpaceDev axes, el_lo/el_hi, nel_local), so the sub-box is swapped in for the
+// launch and restored; the outputs are not zeroed (the caller zeroes them once per form).
+iga_status launch_form_box(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                           const double *Ud, double *val, double *F, cudaStream_t st, const int lo[3],
+                           const int hi[3]) {
+    long long nel = 1, nqp = 1;
+    for (int d = 0; d < 3; d++) {
+        if (hi[d] <= lo[d]) return IGA_OK;            // empty box
+        nel *= hi[d] - lo[d];
+        nqp *= (long long)(hi[d] - lo[d]) * s->nq[d];
+    }
+    int sl[3], sh[3];
+    const long long snel = s->nel_local, snqp = s->nqp_local;
+    for (int d = 0; d < 3; d++) {
+        sl[d] = s->el_lo[d]; sh[d] = s->el_hi[d];
+        s->el_lo[d] = s->dev.ax[d].el_lo = lo[d];
+        s->el_hi[d] = s->dev.ax[d].el_hi = hi[d];
+    }
+    s->nel_local = nel;
+    s->nqp_local = nqp;
+    const int skip = s->skip_zero;
+    s->skip_zero = 1;
+    iga_status r = launch_form(s, ph, a, b, U, Ud, val, F, st);
+    s->skip_zero = skip;
+    s->nel_local = snel;
+    s->nqp_local = snqp;
+    for (int d = 0; d < 3; d++) {
+        s->el_lo[d] = s->dev.ax[d].el_lo = sl[d];
+        s->el_hi[d] = s->dev.ax[d].el_hi = sh[d];
+    }
+    return r;
 }
 
 }  // namespace iga

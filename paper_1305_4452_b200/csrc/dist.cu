@@ -83,6 +83,12 @@ struct Msg {
 struct DistState {
     int transport = 0;
     ncclComm_t comm = nullptr;
+    // element sub-boxes: blo[a] = first element of the rank's box touching a halo function along
+    // axis a (= el_hi without a halo); the upper slabs are computed first, the interior overlaps
+    // the halo-row exchange (which runs on `side`)
+    int blo[3] = {0, 0, 0};
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_pack = nullptr, ev_xchg = nullptr;
     std::vector<Msg> up, down;
     long long ext_nodes = 0, halo_vals = 0, recv_vals = 0, up_vec = 0, down_vec = 0;
     double *Uext = nullptr, *Udext = nullptr, *Fext = nullptr;
@@ -280,6 +286,9 @@ void dist_destroy(iga_space_s *s) {
     if (!s->dist) return;
     DistState *D = s->dist;
     if (D->comm && nccl().ok) nccl().CommDestroy(D->comm);
+    if (D->ev_pack) cudaEventDestroy(D->ev_pack);
+    if (D->ev_xchg) cudaEventDestroy(D->ev_xchg);
+    if (D->side) cudaStreamDestroy(D->side);
     for (void *p : D->allocs) cudaFree(p);
     delete D;
     s->dist = nullptr;
@@ -305,6 +314,31 @@ iga_status dist_setup(iga_space_s *s, const iga_dist *dist) {
     if ((st = dmalloc(D, &D->fh_send, D->up_vec)) != IGA_OK) return st;
     if ((st = dmalloc(D, &D->fh_recv, D->down_vec)) != IGA_OK) return st;
     s->dev.halo = D->halo;
+    for (int a = 0; a < 3; a++) {
+        const AxisHost &H = s->part[a];
+        int b = s->el_hi[a];
+        if (a < s->dim && s->halo[a] > 0) {
+            const int n_own = s->own_hi[a] - s->own_lo[a];
+            for (int e = s->el_hi[a] - 1; e >= s->el_lo[a]; e--) {
+                bool touches = false;
+                for (int al = 0; al <= H.p; al++) {
+                    int l = (H.first[e] + al) % H.nu - s->own_lo[a];
+                    if (l < 0) l += H.nu;
+                    if (l >= n_own) touches = true;
+                }
+                if (!touches) break;
+                b = e;
+            }
+        }
+        D->blo[a] = b;
+    }
+    if (cudaStreamCreateWithFlags(&D->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D->ev_pack, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&D->ev_xchg, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("multi-rank stream / event creation failed");
+        return IGA_ERR_CUDA;
+    }
     if (D->transport == IGA_XPORT_NCCL) {
         NcclApi &api = nccl();
         if (!api.ok) { set_error("libnccl.so.2 not loadable (multi-rank needs NCCL)"); return IGA_ERR_COMM; }
@@ -463,34 +497,78 @@ static iga_status exchange(iga_space_s **sp, int n, int which, bool has_ud, bool
 }
 
 // ---- the multi-rank form call ---------------------------------------------------------------------
+// Schedule per rank (caller's stream st; NCCL halo exchange on the rank's side stream):
+//   zero outputs | pack ghost U -> ghost exchange -> unpack | upper slabs (elements touching halo
+//   rows) -> pack halo residual -> [halo-row exchange on `side` || interior elements on st] ->
+//   K5 adds.  The interior never touches halo rows or ghost functions, so the largest message
+//   (full halo rows) travels while most of the elements are integrated.
 // sp[k], U[k], ... for the n ranks this call drives: n = 1 with NCCL (one process per GPU), or all
-// ranks of an in-process group.  val[k] == nullptr => residual only.
+// ranks of an in-process group (exchanges = device copies, everything on st).  val[k] == nullptr
+// => residual only.
+static void sub_boxes(const iga_space_s *s, int lo[4][3], int hi[4][3]) {
+    const int *L = s->el_lo, *H = s->el_hi, *B = s->dist->blo;
+    // 0..2: upper slabs along axes 0, 1, 2 (disjoint); 3: interior
+    for (int k = 0; k < 4; k++)
+        for (int d = 0; d < 3; d++) { lo[k][d] = L[d]; hi[k][d] = H[d]; }
+    lo[0][0] = B[0];
+    hi[1][0] = B[0]; lo[1][1] = B[1];
+    hi[2][0] = B[0]; hi[2][1] = B[1]; lo[2][2] = B[2];
+    hi[3][0] = B[0]; hi[3][1] = B[1]; hi[3][2] = B[2];
+}
+
 iga_status dist_form(iga_space_s **sp, int n, const iga_phys *ph, double a, double b, const double *const *U,
                      const double *const *Ud, double *const *val, double *const *F, cudaStream_t st) {
     const bool has_ud = Ud[0] != nullptr, has_val = val[0] != nullptr, has_F = F[0] != nullptr;
+    const bool nccl_x = sp[0]->dist->transport == IGA_XPORT_NCCL;
     int launches[64] = {0};
-    for (int k = 0; k < n; k++) phase_ghost_pack(sp[k], U[k], Ud[k], st);
+    for (int k = 0; k < n; k++) {
+        iga_space_s *s = sp[k];
+        DistState *D = s->dist;
+        {
+            ProfScope ps(s, "k_zero", st);
+            k_zero_pair(has_val ? val[k] : nullptr, has_val ? s->nnz_owned : 0, has_F ? D->Fext : nullptr,
+                        has_F ? D->ext_nodes * s->dof : 0, st, 148);
+            if (has_val && D->halo_vals) k_zero_vec(D->halo, D->halo_vals, st, 148);
+        }
+        phase_ghost_pack(s, U[k], Ud[k], st);
+    }
     iga_status r = exchange(sp, n, XCHG_GHOST, has_ud, has_val, has_F, st);
     if (r != IGA_OK) return r;
+    int lo[64][4][3], hi[64][4][3];
     for (int k = 0; k < n; k++) {
         iga_space_s *s = sp[k];
         DistState *D = s->dist;
         phase_ghost_unpack(s, has_ud, st);
-        if (has_F) {
-            ProfScope ps(s, "k_zero", st);
-            k_zero_vec(D->Fext, D->ext_nodes * s->dof, st, 148);
+        sub_boxes(s, lo[k % 64], hi[k % 64]);
+        for (int j = 0; j < 3; j++) {
+            r = launch_form_box(s, ph, a, b, D->Uext, has_ud ? D->Udext : nullptr, val[k], has_F ? D->Fext : nullptr, st,
+                                lo[k % 64][j], hi[k % 64][j]);
+            if (r != IGA_OK) return r;
+            launches[k % 64] += s->last_launches;
         }
-        if (has_val && D->halo_vals) {
-            ProfScope ps(s, "k_zero", st);
-            k_zero_vec(D->halo, D->halo_vals, st, 148);
-        }
-        r = launch_form(s, ph, a, b, D->Uext, has_ud ? D->Udext : nullptr, val[k], has_F ? D->Fext : nullptr, st);
-        if (r != IGA_OK) return r;
-        launches[k % 64] = s->last_launches;
         phase_halo_pack(s, has_F, st);
     }
-    r = exchange(sp, n, XCHG_HALO, has_ud, has_val, has_F, st);
-    if (r != IGA_OK) return r;
+    if (nccl_x) {
+        // halo rows leave on the side stream while the interior is integrated on st
+        DistState *D = sp[0]->dist;
+        cudaEventRecord(D->ev_pack, st);
+        cudaStreamWaitEvent(D->side, D->ev_pack, 0);
+        r = exchange(sp, n, XCHG_HALO, has_ud, has_val, has_F, D->side);
+        if (r != IGA_OK) return r;
+        cudaEventRecord(D->ev_xchg, D->side);
+    } else {
+        r = exchange(sp, n, XCHG_HALO, has_ud, has_val, has_F, st);
+        if (r != IGA_OK) return r;
+    }
+    for (int k = 0; k < n; k++) {
+        iga_space_s *s = sp[k];
+        DistState *D = s->dist;
+        r = launch_form_box(s, ph, a, b, D->Uext, has_ud ? D->Udext : nullptr, val[k], has_F ? D->Fext : nullptr, st,
+                            lo[k % 64][3], hi[k % 64][3]);
+        if (r != IGA_OK) return r;
+        launches[k % 64] += s->last_launches;
+    }
+    if (nccl_x) cudaStreamWaitEvent(st, sp[0]->dist->ev_xchg, 0);
     for (int k = 0; k < n; k++) {
         phase_halo_add(sp[k], val[k], F[k], st);
         sp[k]->last_launches = launches[k % 64];

@@ -410,7 +410,7 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
         for (int d = 0; d < 2; d++)
             for (int i = 0; i < (P + 1) * 3 * (P + 1); i++) (&ut.t[d][0][0][0])[i] = s->tab0[d][i];
     int launches = 0;
-    if (F || jac) {
+    if ((F || jac) && !s->skip_zero) {
         // CSR values (rows not complete inside one element receive red.add) and residual, one launch
         ProfScope ps(s, "k_zero", st);
         k_zero_pair(val, jac ? s->nnz_owned : 0, F, F ? s->nrows_owned : 0, st, nsm);

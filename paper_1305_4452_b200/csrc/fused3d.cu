@@ -653,7 +653,7 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
     const long long nel = s->nel_local;
     const int grid = (int)std::min<long long>(nel, (long long)nsm * occ);
     int launches = 0;
-    if (jac || F) {
+    if ((jac || F) && !s->skip_zero) {
         ProfScope ps(s, "k_zero", st);
         k_zero_pair(val, jac ? s->nnz_owned : 0, F, F ? s->nrows_owned : 0, st, nsm);
         launches++;

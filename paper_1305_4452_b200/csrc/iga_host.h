@@ -50,6 +50,7 @@ struct iga_space_s {
     int force_split = 0;
     int force_general = 0;
     int bw_opt = 0;                      // 3D element-order block width override (0: from the L2 size)
+    int skip_zero = 0;                   // dist.cu: the caller zeroed the outputs (sub-box launches)
     int last_occupancy = 0;
     int dbg = 0;                         // experiment bits (bench A/B only; results invalid when set)               // 1: never use the uniform-table fast paths
     // per axis: all elements share the same 1D tables / weights / span length (uniform knots,
@@ -80,6 +81,10 @@ struct ProfScope {
 void set_error(const std::string &msg);
 iga_status launch_form(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
                        const double *Udot, double *csr_val, double *F, cudaStream_t st);
+// launch_form over the element sub-box [lo, hi) of this rank's element box, outputs not zeroed
+iga_status launch_form_box(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
+                           const double *Udot, double *csr_val, double *F, cudaStream_t st, const int lo[3],
+                           const int hi[3]);
 void k_zero_vec(double *p, long long n, cudaStream_t st, int nsm);
 void k_zero_pair(double *p, long long n, double *q, long long m, cudaStream_t st, int nsm);   // p and/or q may be null
 iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
