@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _SO = os.path.join(_HERE, "liboracle.so")
 
-LAPLACE, CAHN_HILLIARD, NEOHOOKE, NS_VMS = 0, 1, 2, 3
+LAPLACE, CAHN_HILLIARD, NEOHOOKE, NS_VMS, NSK = 0, 1, 2, 3, 4
 PARAMETRIC, NURBS = 0, 1
 
 

@@ -38,7 +38,7 @@
 #define ORC_MAXEN 125 /* (ORC_MAXP+1)^3 */
 #define ORC_MAXM 4
 
-enum { ORC_LAPLACE = 0, ORC_CAHN_HILLIARD = 1, ORC_NEOHOOKE = 2, ORC_NS_VMS = 3 };
+enum { ORC_LAPLACE = 0, ORC_CAHN_HILLIARD = 1, ORC_NEOHOOKE = 2, ORC_NS_VMS = 3, ORC_NSK = 4 };
 enum { ORC_PARAMETRIC = 0, ORC_NURBS = 1 };
 
 /* ------------------------------------------------------------------------------------ */
@@ -716,6 +716,8 @@ typedef struct {
     double F[3][3], S[3][3], P[3][3], Ci[3][3], J, AA[3][3][3][3];
     /* VMS */
     double tauM, tauC, rM[3], rC, up[3], pp;
+    /* NSK */
+    double pv, dpv;
 } orc_pt;
 
 /* LAPLACE: R_A = int kappa grad N_A . grad u + sigma N_A u - N_A f; J_AB = b int (...)  */
@@ -835,6 +837,50 @@ static void vms_setup(orc_pt *P, const orc_fields *f)
     P->pp = -P->tauC * P->rC;
 }
 
+/* Navier-Stokes-Korteweg, readings A-25..A-27:
+ * unknowns (rho, u_1..u_d) per node; prm = [a, b, R, theta, mu_bar, lambda_bar, lambda].
+ * van der Waals pressure p = R b rho theta / (b - rho) - a rho^2, p' = R b^2 theta/(b-rho)^2 - 2 a rho.
+ * Weak form of the strong form P:780-782 on a periodic domain (boundary terms vanish):
+ *   R^C_A    = N_A rho_t - N_{A,j} rho u_j
+ *   R^M_{Ai} = N_A (rho_t u_i + rho u_{i,t}) + N_{A,j} (-rho u_i u_j - p delta_ij + tau_ij + zeta_ij)
+ *   tau  = mu_bar (grad u + grad u^T) + lambda_bar (div u) I
+ *   zeta = lambda (rho lap rho + |grad rho|^2 / 2) I - lambda grad rho (x) grad rho */
+static void nsk_setup(orc_pt *P, const orc_fields *f)
+{
+    const double av = P->prm[0], bv = P->prm[1], Rg = P->prm[2], th = P->prm[3];
+    double rho = f->u[0];
+    P->pv = Rg * bv * rho * th / (bv - rho) - av * rho * rho;
+    P->dpv = Rg * bv * bv * th / ((bv - rho) * (bv - rho)) - 2.0 * av * rho;
+}
+
+/* NSK residual at a point for test function values (N, dN): r[0..dim] */
+static void nsk_residual(const orc_pt *P, const orc_fields *f, double N, const double *dN, double *r)
+{
+    int dim = P->dim;
+    const double mub = P->prm[4], lamb = P->prm[5], lam = P->prm[6];
+    double rho = f->u[0], rhot = f->ut[0];
+    double div = 0.0, g2 = 0.0;
+    for (int k = 0; k < dim; k++) { div += f->du[1 + k][k]; g2 += f->du[0][k] * f->du[0][k]; }
+    double v = N * rhot;
+    for (int j = 0; j < dim; j++) v -= dN[j] * rho * f->u[1 + j];
+    r[0] = v;
+    for (int i = 0; i < dim; i++) {
+        double w = N * (rhot * f->u[1 + i] + rho * f->ut[1 + i]);
+        for (int j = 0; j < dim; j++) {
+            double sig = -rho * f->u[1 + i] * f->u[1 + j];
+            double tau = mub * (f->du[1 + i][j] + f->du[1 + j][i]);
+            double zeta = -lam * f->du[0][i] * f->du[0][j];
+            if (i == j) {
+                sig -= P->pv;
+                tau += lamb * div;
+                zeta += lam * (rho * f->lap[0] + 0.5 * g2);
+            }
+            w += dN[j] * (sig + tau + zeta);
+        }
+        r[1 + i] = w;
+    }
+}
+
 static void residual_at(const orc_pt *P, const orc_qp *Q, const orc_fields *f, int A, double *r)
 {
     int dim = P->dim;
@@ -865,6 +911,9 @@ static void residual_at(const orc_pt *P, const orc_qp *Q, const orc_fields *f, i
         }
         break;
     }
+    case ORC_NSK:
+        nsk_residual(P, f, N, dN, r);
+        break;
     case ORC_NS_VMS: {
         double nu = P->prm[0];
         /* momentum (Appendix A) */
@@ -934,6 +983,52 @@ static void jacobian_at(const orc_pt *P, const orc_qp *Q, const orc_fields *f, i
             }
         break;
     }
+    case ORC_NSK: {
+        const double mub = P->prm[4], lamb = P->prm[5], lam = P->prm[6];
+        double rho = f->u[0], rhot = f->ut[0];
+        double g2 = 0.0;
+        for (int k = 0; k < dim; k++) g2 += f->du[0][k] * f->du[0][k];
+        for (int j = 0; j < m; j++) {
+            double res[2][ORC_MAXM];
+            for (int part = 0; part < 2; part++) {
+                /* perturbation of the fields in the direction N_B e_j */
+                double drho = 0.0, drhot = 0.0, dgrho[3] = {0, 0, 0}, dlrho = 0.0;
+                double du[3] = {0, 0, 0}, dut[3] = {0, 0, 0}, dgu[3][3] = {{0}};
+                if (part == 0) {
+                    if (j == 0) drhot = NB; else dut[j - 1] = NB;
+                } else if (j == 0) {
+                    drho = NB;
+                    for (int k = 0; k < dim; k++) dgrho[k] = dNB[k];
+                    dlrho = lapB;
+                } else {
+                    du[j - 1] = NB;
+                    for (int k = 0; k < dim; k++) dgu[j - 1][k] = dNB[k];
+                }
+                double ddiv = 0.0, dg2 = 0.0;
+                for (int k = 0; k < dim; k++) { ddiv += dgu[k][k]; dg2 += 2.0 * f->du[0][k] * dgrho[k]; }
+                double v = NA * drhot;
+                for (int l = 0; l < dim; l++) v -= dNA[l] * (drho * f->u[1 + l] + rho * du[l]);
+                res[part][0] = v;
+                for (int i = 0; i < dim; i++) {
+                    double w = NA * (drhot * f->u[1 + i] + rhot * du[i] + drho * f->ut[1 + i] + rho * dut[i]);
+                    for (int l = 0; l < dim; l++) {
+                        double dsig = -(drho * f->u[1 + i] * f->u[1 + l] + rho * du[i] * f->u[1 + l] + rho * f->u[1 + i] * du[l]);
+                        double dtau = mub * (dgu[i][l] + dgu[l][i]);
+                        double dzeta = -lam * (dgrho[i] * f->du[0][l] + f->du[0][i] * dgrho[l]);
+                        if (i == l) {
+                            dsig -= P->dpv * drho;
+                            dtau += lamb * ddiv;
+                            dzeta += lam * (drho * f->lap[0] + rho * dlrho + 0.5 * dg2);
+                        }
+                        w += dNA[l] * (dsig + dtau + dzeta);
+                    }
+                    res[part][1 + i] = w;
+                }
+            }
+            for (int i = 0; i < m; i++) K[i * m + j] = P->a * res[0][i] + P->b * res[1][i];
+        }
+        break;
+    }
     case ORC_NS_VMS: {
         double nu = P->prm[0];
         for (int j = 0; j < 4; j++) {
@@ -999,6 +1094,8 @@ static int phys_dof(int kind)
     return -1;
 }
 
+static int phys_dof_dim(int kind, int dim) { return kind == ORC_NSK ? 1 + dim : phys_dof(kind); }
+
 /* ------------------------------------------------------------------------------------ */
 /* Element integration (Alg. 4 lines P:599-604): dense K_e and F_e.                       */
 /* Ke is (nen*m)^2 row-major with row = A*m+i, col = B*m+j.  Utau: state for the frozen   */
@@ -1036,6 +1133,7 @@ static int element_integrate(const orc_space *s, int kind, const double *prm, do
                 memset(&P, 0, sizeof(P));
                 P.kind = kind; P.dim = dim; P.m = m; P.prm = prm; P.a = a; P.b = b;
                 if (kind == ORC_CAHN_HILLIARD) ch_setup(&P, &f);
+                if (kind == ORC_NSK) nsk_setup(&P, &f);
                 if (kind == ORC_NEOHOOKE) { nh_setup(&P, &f); if (want_K) nh_tangent(&P); }
                 if (kind == ORC_NS_VMS) {
                     if (Utau) { eval_fields(s, &Q, Utau, Udot, &ftau); vms_tau(&P, &Q, &ftau); }
@@ -1069,7 +1167,7 @@ int orc_element(const orc_space *s, int kind, const double *prm, double a, doubl
                 const double *U, const double *Udot, const double *Utau, const int *e,
                 double *Ke, double *Fe, int64_t *nodes)
 {
-    if (phys_dof(kind) != s->dof) return -3;
+    if (phys_dof_dim(kind, s->dim) != s->dof) return -3;
     int ee[3] = {0, 0, 0};
     for (int d = 0; d < s->dim; d++) ee[d] = e[d];
     orc_qp Q;
@@ -1087,7 +1185,7 @@ int orc_assemble_dense(const orc_space *s, int kind, const double *prm, double a
                        const double *U, const double *Udot, const double *Utau,
                        double *K, unsigned char *touched, double *F)
 {
-    if (phys_dof(kind) != s->dof) return -3;
+    if (phys_dof_dim(kind, s->dim) != s->dof) return -3;
     int m = s->dof;
     int64_t nd = orc_ndof(s);
     if (K) memset(K, 0, sizeof(double) * (size_t)nd * nd);
@@ -1156,7 +1254,7 @@ int64_t orc_assemble_rows(const orc_space *s, int kind, const double *prm, doubl
                           int64_t nrows, const int64_t *rows, const int64_t *rowptr,
                           const int32_t *cols, double *vals, double *F, unsigned char *touched)
 {
-    if (phys_dof(kind) != s->dof) return -3;
+    if (phys_dof_dim(kind, s->dim) != s->dof) return -3;
     int m = s->dof;
     int dim = s->dim;
     /* elements touching each global function, per axis */

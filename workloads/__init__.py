@@ -33,13 +33,13 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-PHYS_LAPLACE, PHYS_CAHN_HILLIARD, PHYS_NEOHOOKE, PHYS_NS_VMS = 0, 1, 2, 3
+PHYS_LAPLACE, PHYS_CAHN_HILLIARD, PHYS_NEOHOOKE, PHYS_NS_VMS, PHYS_NSK = 0, 1, 2, 3, 4
 GEOM_PARAMETRIC, GEOM_NURBS = 0, 1
 
 # full-size element counts per axis (BASELINE.json configs[0..4])
-FULL_N = {1: 16, 2: 256, 3: 1024, 4: 64, 5: 128}
+FULL_N = {1: 16, 2: 256, 3: 1024, 4: 64, 5: 128, 6: 256}
 NAMES = {1: "poisson2d_p2_16x16", 2: "annulus_lapmass_p3_256x256", 3: "cahn_hilliard2d_p2_1024x1024",
-         4: "neohooke3d_p2_64x64x64", 5: "ns_vms3d_p2_128x128x128"}
+         4: "neohooke3d_p2_64x64x64", 5: "ns_vms3d_p2_128x128x128", 6: "nsk2d_p2_256x256"}
 
 
 @dataclass
@@ -132,7 +132,7 @@ def annulus_geometry(U0: np.ndarray, U1: np.ndarray, p: int = 3):
 def make(cid: int, n=None, seed: int | None = None) -> Workload:
     """Build config `cid` (1..5) with n elements per axis (default: the full BASELINE size); n may
     be a list with one count per axis (weak-scaling meshes of bench.py --gpus N)."""
-    dims = {1: 2, 2: 2, 3: 2, 4: 3, 5: 3}[cid] if cid in (1, 2, 3, 4, 5) else 0
+    dims = {1: 2, 2: 2, 3: 2, 4: 3, 5: 3, 6: 2}[cid] if cid in (1, 2, 3, 4, 5, 6) else 0
     if n is None:
         n = FULL_N[cid]
     nn = list(n) if isinstance(n, (list, tuple)) else [int(n)] * dims
@@ -216,6 +216,29 @@ def _make(cid: int, nn: list, seed: int | None = None) -> Workload:
         w = Workload(5, NAMES[5], d, [p] * d, U, [1] * d, [p - 1] * d, 4, [p + 1] * d, GEOM_PARAMETRIC,
                      None, None, PHYS_NS_VMS, [1.0 / 1600.0, dt, 4.0, 36.0], 5.0 / 6.0, (4.0 / 9.0) * dt,
                      Uarr, np.zeros(Uarr.size), list(nn), list(nn))
+    elif cid == 6:
+        # Navier-Stokes-Korteweg (not a BASELINE config): [0,1]^2 periodic C^1
+        # quadratic, parametric, unknowns (rho, u1, u2); three vapour bubbles in liquid (the paper's
+        # three-bubble test) as a smooth density field at the Greville points, small
+        # seeded velocity and time derivatives; van der Waals a = 3, b = 1, R = 8/27, theta = 0.85
+        # (sub-critical), mu_bar = 1/512, lambda_bar = -2/3 mu_bar, capillarity lambda = 1/512^2
+        # (readings A-25..A-27); generalized-alpha (a, b) with dt = 1e-3.
+        p, d = 2, 2
+        U = [open_uniform_knots(p, nn[a]) for a in range(d)]
+        gs = [_periodic_greville(0.0, 1.0, nn[a], p) for a in range(d)]
+        x, y = np.meshgrid(gs[0], gs[1], indexing="ij")
+        rho = np.full(x.shape, 0.6)
+        for (cx, cy, r) in ((0.30, 0.30, 0.10), (0.62, 0.60, 0.15), (0.25, 0.72, 0.08)):
+            dist = np.hypot(x - cx, y - cy)
+            rho -= 0.25 * (1.0 + np.tanh((r - dist) / 0.04))
+        vel = 0.01 * rng.uniform(-1.0, 1.0, x.shape + (2,))
+        Uarr = np.concatenate([rho[..., None], vel], axis=-1).reshape(-1).copy()
+        Udot = 0.01 * rng.uniform(-1.0, 1.0, Uarr.size)
+        dt = 1e-3
+        mub = 1.0 / 512.0
+        w = Workload(6, NAMES[6], d, [p] * d, U, [1] * d, [p - 1] * d, 3, [p + 1] * d, GEOM_PARAMETRIC,
+                     None, None, PHYS_NSK, [3.0, 1.0, 8.0 / 27.0, 0.85, mub, -2.0 / 3.0 * mub, 1.0 / 512.0 ** 2],
+                     5.0 / 6.0, (4.0 / 9.0) * dt, Uarr, Udot, list(nn), list(nn))
     else:
         raise ValueError(f"unknown config {cid}")
     return w
