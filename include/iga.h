@@ -140,7 +140,9 @@ typedef enum {
     IGA_PHYS_LAPLACE = 0,        /* p = [kappa, sigma, source_id]; m = 1                      */
     IGA_PHYS_CAHN_HILLIARD = 1,  /* p = [theta, alpha]; m = 1; needs Hessians      */
     IGA_PHYS_NEOHOOKE = 2,       /* p = [lambda, mu]; m = 3, dim 3                 */
-    IGA_PHYS_NS_VMS = 3          /* p = [nu, dt, C_t, C_I]; m = 4, dim 3, parametric*/
+    IGA_PHYS_NS_VMS = 3,         /* p = [nu, dt, C_t, C_I]; m = 4, dim 3, parametric*/
+    IGA_PHYS_NSK = 4             /* p = [a, b, R, theta, mu_bar, lambda_bar, lambda]; m = 3 (rho, u),
+                                    dim 2, Navier-Stokes-Korteweg */
 } iga_phys_kind;
 
 typedef struct {

@@ -353,8 +353,8 @@ template <int DIM, int P, class PH>
 static iga_status dispatch_mode(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                                 const double *Ud, double *val, double *F, cudaStream_t st) {
     if (s->mode == MODE_PARAM) return run_form<DIM, P, PH, MODE_PARAM>(s, ph, a, b, U, Ud, val, F, st);
-    if constexpr (std::is_same<PH, PhysNSVMS>::value) {
-        set_error("NS_VMS supports parametric geometry with unit weights only");
+    if constexpr (std::is_same<PH, PhysNSVMS>::value || std::is_same<PH, PhysNSK>::value) {
+        set_error("NS_VMS / NSK support parametric geometry with unit weights only");
         return IGA_ERR_PARAM;
     } else {
         return run_form<DIM, P, PH, MODE_NURBS>(s, ph, a, b, U, Ud, val, F, st);
@@ -405,6 +405,9 @@ iga_status launch_form(iga_space_s *s, const iga_phys *ph, double a, double b, c
     case IGA_PHYS_NS_VMS:
         if (s->dof != 4 || s->dim != 3) break;
         return dispatch_p<3, PhysNSVMS>(s, ph, a, b, U, Ud, val, F, st);
+    case IGA_PHYS_NSK:
+        if (s->dof != 3 || s->dim != 2) break;
+        return dispatch_p<2, PhysNSK>(s, ph, a, b, U, Ud, val, F, st);
     default:
         set_error("unknown physics kind");
         return IGA_ERR_PARAM;

@@ -380,4 +380,145 @@ struct PhysNSVMS {
     }
 };
 
+// ------------------------------------------------------------------------------------------
+// NAVIER-STOKES-KORTEWEG (P:774-801 strong form, readings A-25..A-27):
+// unknowns (rho, u_1, u_2) per node, 2D.  p = [a, b, R, theta, mu_bar, lambda_bar, lambda].
+//   r_(N,0)   = rho_t                         r_(d_l,0)   = -rho u_l
+//   r_(N,1+i) = rho_t u_i + rho u_{i,t}       r_(d_l,1+i) = -rho u_i u_l - p d_il + tau_il + zeta_il
+//   tau  = mu_bar (grad u + grad u^T) + lambda_bar div u I,
+//   zeta = lambda (rho lap rho + |grad rho|^2/2) I - lambda grad rho (x) grad rho,
+//   p = R b rho theta/(b - rho) - a rho^2 (van der Waals)
+// kinds: 0 = N, 1..2 = d/dx_l, 3 = lap
+// ------------------------------------------------------------------------------------------
+struct PhysNSK {
+    static constexpr int M = 3;
+    static constexpr bool HESS = true;
+    static constexpr bool UDOT = true;       // residual depends on the time derivative
+    template <int DIM> static constexpr int NK() { return 2 + DIM; }
+    template <int DIM> static constexpr bool dmask(int k, int i, int k2, int j) {
+        const int L = 1 + DIM;                       // Laplacian kind
+        if (k == L) return false;                    // no Laplacian test kind
+        if (k == 0) return i == 0 ? (k2 == 0 && j == 0) : (k2 == 0 && (j == 0 || j == i));
+        const int l = k - 1;                         // test direction
+        if (i == 0) return k2 == 0 && (j == 0 || j == 1 + l);
+        const int ii = i - 1;
+        if (j == 0) {                                // density trial: value, gradient, Laplacian
+            if (k2 == 0) return true;
+            if (k2 == L) return ii == l;
+            const int m = k2 - 1;
+            return ii == l || m == ii || m == l;
+        }
+        const int n = j - 1;                         // velocity trial
+        if (k2 == 0) return n == ii || n == l;
+        if (k2 == L) return false;
+        const int m = k2 - 1;
+        return (n == ii && m == l) || (n == l && m == ii) || (n == m && ii == l);
+    }
+    static constexpr bool rmask(int k, int i) { return k < 3; }
+    template <int DIM>
+    struct State { double rho, rt, u[2], ut[2], gr[2], gu[2][2], lr, p, dp, mub, lamb, lam; };
+    template <int DIM>
+    __device__ static inline void prepare(const double *p, const Fields<DIM, 3> &F, State<DIM> &s) {
+        static_assert(DIM == 2, "NSK is 2D in this build");
+        const double av = p[0], bv = p[1], Rg = p[2], th = p[3];
+        s.mub = p[4];
+        s.lamb = p[5];
+        s.lam = p[6];
+        s.rho = F.u[0];
+        s.rt = F.ut[0];
+        s.lr = F.lu[0];
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            s.u[i] = F.u[1 + i];
+            s.ut[i] = F.ut[1 + i];
+            s.gr[i] = F.gu[0][i];
+#pragma unroll
+            for (int l = 0; l < 2; l++) s.gu[i][l] = F.gu[1 + i][l];
+        }
+        const double ib = 1.0 / (bv - s.rho);
+        s.p = Rg * bv * th * s.rho * ib - av * s.rho * s.rho;
+        s.dp = Rg * bv * bv * th * ib * ib - 2.0 * av * s.rho;
+    }
+    template <int DIM>
+    __device__ static inline void residual(const State<DIM> &s, double *r) {
+        // r[kind * 3 + component]
+        r[0] = s.rt;
+#pragma unroll
+        for (int i = 0; i < 2; i++) r[1 + i] = s.rt * s.u[i] + s.rho * s.ut[i];
+        const double div = s.gu[0][0] + s.gu[1][1];
+        const double iso = s.lam * (s.rho * s.lr + 0.5 * (s.gr[0] * s.gr[0] + s.gr[1] * s.gr[1])) - s.p + s.lamb * div;
+#pragma unroll
+        for (int l = 0; l < 2; l++) {
+            r[(1 + l) * 3] = -s.rho * s.u[l];
+#pragma unroll
+            for (int i = 0; i < 2; i++)
+                r[(1 + l) * 3 + 1 + i] = -s.rho * s.u[i] * s.u[l] + s.mub * (s.gu[i][l] + s.gu[l][i])
+                                         - s.lam * s.gr[i] * s.gr[l] + (i == l ? iso : 0.0);
+        }
+#pragma unroll
+        for (int i = 0; i < 3; i++) r[9 + i] = 0.0;
+    }
+    // column D_(:,:),(k2,j) = a d r/d(trial_t) + b d r/d(trial); trial kind k2, component j
+    template <int DIM>
+    __device__ static inline void dcol(const State<DIM> &s, int k2, int j, double a, double b, double *col) {
+#pragma unroll
+        for (int k = 0; k < 12; k++) col[k] = 0.0;
+        if (j == 0) {                                          // density
+            if (k2 == 0) {
+                col[0] = a;                                    // d rho_t
+#pragma unroll
+                for (int i = 0; i < 2; i++) col[1 + i] = a * s.u[i] + b * s.ut[i];
+#pragma unroll
+                for (int l = 0; l < 2; l++) {
+                    col[(1 + l) * 3] = -b * s.u[l];
+#pragma unroll
+                    for (int i = 0; i < 2; i++)
+                        col[(1 + l) * 3 + 1 + i] = b * (-s.u[i] * s.u[l] + (i == l ? s.lam * s.lr - s.dp : 0.0));
+                }
+            } else if (k2 <= 2) {                              // d grad rho, direction m
+                const int m = k2 - 1;
+#pragma unroll
+                for (int l = 0; l < 2; l++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        double v = -s.lam * ((i == m ? s.gr[l] : 0.0) + (l == m ? s.gr[i] : 0.0));
+                        if (i == l) v += s.lam * s.gr[m];
+                        col[(1 + l) * 3 + 1 + i] = b * v;
+                    }
+            } else {                                           // d lap rho
+#pragma unroll
+                for (int l = 0; l < 2; l++) col[(1 + l) * 3 + 1 + l] = b * s.lam * s.rho;
+            }
+        } else {                                               // velocity component n
+            const int n = j - 1;
+            if (k2 == 0) {
+                col[1 + n] = a * s.rho + b * s.rt;
+#pragma unroll
+                for (int l = 0; l < 2; l++) {
+                    if (l == n) col[(1 + l) * 3] = -b * s.rho;
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        double v = 0.0;
+                        if (i == n) v -= s.rho * s.u[l];
+                        if (l == n) v -= s.rho * s.u[i];
+                        col[(1 + l) * 3 + 1 + i] = b * v;
+                    }
+                }
+            } else if (k2 <= 2) {                              // d (u_n)_{,m}
+                const int m = k2 - 1;
+#pragma unroll
+                for (int l = 0; l < 2; l++)
+#pragma unroll
+                    for (int i = 0; i < 2; i++) {
+                        double v = 0.0;
+                        if (i == n && l == m) v += s.mub;
+                        if (l == n && i == m) v += s.mub;
+                        if (i == l && n == m) v += s.lamb;
+                        col[(1 + l) * 3 + 1 + i] = b * v;
+                    }
+            }
+        }
+    }
+};
+
 }  // namespace iga

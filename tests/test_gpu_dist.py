@@ -37,7 +37,7 @@ def _owned_rows(w, sp):
 
 LAYOUTS = [
     (1, 16, [2, 2]), (2, 12, [2, 3]), (3, 12, [2, 1]), (3, 16, [2, 2]), (3, 33, [3, 2]),
-    (4, 6, [2, 2, 1]), (4, 5, [1, 2, 2]), (5, 8, [2, 2, 2]), (5, 7, [2, 1, 3]),
+    (4, 6, [2, 2, 1]), (4, 5, [1, 2, 2]), (5, 8, [2, 2, 2]), (5, 7, [2, 1, 3]), (6, 8, [2, 2]),
 ]
 
 
@@ -48,7 +48,7 @@ def test_group_parity(cid, n, procs):
     nr = int(np.prod(procs))
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(11 + cid)
-    Ud_full = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3) else w.Udot
+    Ud_full = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3, 4) else w.Udot
     spaces = [iga.Space.from_workload(w, dist={"rank": r, "nranks": nr, "procs": procs,
                                                "transport": iga.XPORT_LOCAL}) for r in range(nr)]
     rows = [_owned_rows(w, sp) for sp in spaces]

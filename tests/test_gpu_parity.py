@@ -40,7 +40,7 @@ def _gpu_assemble(iga, w, a=None, b=None, params=None, Udot=None, want_F=True, s
         Fr.cpu().numpy()
 
 
-SMALL = [(1, 16), (1, 5), (2, 3), (2, 16), (3, 5), (3, 12), (4, 2), (4, 5), (5, 5), (5, 7)]
+SMALL = [(1, 16), (1, 5), (2, 3), (2, 16), (3, 5), (3, 12), (4, 2), (4, 5), (5, 5), (5, 7), (6, 5), (6, 9)]
 
 
 SMALL_2D_TILES = [(1, 17), (2, 9), (2, 21), (3, 16), (3, 33), (3, 40)]   # several tiles + ragged tails
@@ -54,7 +54,7 @@ def test_small_full_parity(cid, n, split):
     iga = _gpu()
     w = workloads.make(cid, n=n)
     rng = np.random.default_rng(100 + cid)
-    Ud = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3) else w.Udot
+    Ud = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3, 4) else w.Udot
     sp, rp, ci, vals, F, Fr = _gpu_assemble(iga, w, Udot=Ud, split=split)
     osp = oracle.Space.from_workload(w)
     K, T, Fo = osp.assemble_dense(w.phys, w.params, w.a, w.b, w.U, Ud)
@@ -71,13 +71,17 @@ def test_small_full_parity(cid, n, split):
     (3, 9, [dict(a=1.0, b=0.0), dict(a=0.0, b=1.0)]),                               # mass | d/dc
     (5, 5, [dict(a=1.0, b=0.0), dict(a=0.0, b=1.0)]),                               # d/dUdot | d/dU
     (1, 6, [dict(params=[1.0, 0.0, 1.0]), dict(params=[0.0, 1.0, 1.0])]),
+    # NSK: d/dUdot | d/dU, and a capillarity-dominated state (Korteweg terms on their own scale)
+    (6, 6, [dict(a=1.0, b=0.0), dict(a=0.0, b=1.0),
+            dict(params=[3.0, 1.0, 8.0 / 27.0, 0.85, 0.0, 0.0, 1e-2]),
+            dict(params=[0.0, 1.0, 0.0, 0.85, 1.0 / 512, -2.0 / 3.0 / 512, 0.0])]),
 ])
 def test_term_groups(cid, n, groups):
     """A-17: the 1e-11 row-max rule hides small terms; check each term group on its own scale."""
     iga = _gpu()
     w = workloads.make(cid, n=n)
     rng = np.random.default_rng(7)
-    Ud = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3) else w.Udot
+    Ud = rng.uniform(-0.1, 0.1, w.U.size) if w.phys in (1, 3, 4) else w.Udot
     osp = oracle.Space.from_workload(w)
     for g in groups:
         a, b, prm = g.get("a", w.a), g.get("b", w.b), g.get("params", w.params)
