@@ -39,6 +39,7 @@ struct iga_space_s {
     // unclamped knot vectors on the device (third-order basis evaluation only; deliberately not in
     // SpaceDev, whose size the fused kernels' register allocation turned out to be sensitive to)
     const double *dknots[3] = {nullptr, nullptr, nullptr};
+    double *hb_U = nullptr, *hb_Ud = nullptr, *hb_val = nullptr, *hb_F = nullptr;   // host-buffer path staging
     int el_lo[3] = {0, 0, 0}, el_hi[3] = {1, 1, 1};
     long long ndof_global = 0, nrows_owned = 0, nnz_owned = 0, nqp_local = 0, nel_local = 0;
     // device allocations owned by the space

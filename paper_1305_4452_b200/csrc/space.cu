@@ -771,14 +771,20 @@ iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, d
     cudaSetDevice(s->device);
     cudaStream_t cs = (cudaStream_t)stream;
     const size_t nU = (size_t)s->ndof_global, nF = (size_t)s->nrows_owned, nz = (size_t)s->nnz_owned;
-    // staging buffers live inside the workspace's tail is not safe (the workspace is in use);
-    // allocate transient device buffers with the stream-ordered allocator.
-    double *dU = nullptr, *dUd = nullptr, *dV = nullptr, *dF = nullptr;
-    cudaError_t ce = cudaMallocAsync(&dU, nU * sizeof(double), cs);
-    if (ce == cudaSuccess && Udot_host) ce = cudaMallocAsync(&dUd, nU * sizeof(double), cs);
-    if (ce == cudaSuccess) ce = cudaMallocAsync(&dV, nz * sizeof(double), cs);
-    if (ce == cudaSuccess && F_host) ce = cudaMallocAsync(&dF, nF * sizeof(double), cs);
-    if (ce == cudaSuccess) ce = cudaMemcpyAsync(dU, U_host, nU * sizeof(double), cudaMemcpyHostToDevice, cs);
+    // device staging buffers of the host-buffer path: allocated on first use, kept by the space
+    cudaError_t ce = cudaSuccess;
+    if (!s->hb_U) {
+        double *p4[4] = {nullptr, nullptr, nullptr, nullptr};
+        const size_t sz[4] = {nU, nU, nz, nF};
+        for (int k = 0; k < 4 && ce == cudaSuccess; k++) {
+            ce = cudaMalloc(&p4[k], std::max<size_t>(sz[k], 1) * sizeof(double));
+            if (ce == cudaSuccess) s->allocs.push_back(p4[k]);
+        }
+        if (ce != cudaSuccess) { cudaGetLastError(); cudaSetDevice(prev); set_error("host-path staging allocation failed"); return IGA_ERR_NOMEM; }
+        s->hb_U = p4[0]; s->hb_Ud = p4[1]; s->hb_val = p4[2]; s->hb_F = p4[3];
+    }
+    double *dU = s->hb_U, *dUd = Udot_host ? s->hb_Ud : nullptr, *dV = s->hb_val, *dF = F_host ? s->hb_F : nullptr;
+    ce = cudaMemcpyAsync(dU, U_host, nU * sizeof(double), cudaMemcpyHostToDevice, cs);
     if (ce == cudaSuccess && Udot_host) ce = cudaMemcpyAsync(dUd, Udot_host, nU * sizeof(double), cudaMemcpyHostToDevice, cs);
     if (ce == cudaSuccess) {
         st = launch_form(s, phys, a, b, dU, dUd, dV, dF, cs);
@@ -788,10 +794,6 @@ iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, d
             ce = cudaMemcpyAsync(F_host, dF, nF * sizeof(double), cudaMemcpyDeviceToHost, cs);
         s->last_launches = nl;
     }
-    if (dU) cudaFreeAsync(dU, cs);
-    if (dUd) cudaFreeAsync(dUd, cs);
-    if (dV) cudaFreeAsync(dV, cs);
-    if (dF) cudaFreeAsync(dF, cs);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(cs);
     cudaSetDevice(prev);
     if (ce != cudaSuccess) { set_error(cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
