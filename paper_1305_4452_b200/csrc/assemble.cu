@@ -383,6 +383,8 @@ iga_status launch_form(iga_space_s *s, const iga_phys *ph, double a, double b, c
         if (fs != IGA_ERR_STATE) return fs;
         fs = launch_fused3d(s, ph, a, b, U, Ud, val, F, st, nsm);
         if (fs != IGA_ERR_STATE) return fs;
+        fs = launch_fused2dm(s, ph, a, b, U, Ud, val, F, st, nsm);
+        if (fs != IGA_ERR_STATE) return fs;
     }
     for (int d = 1; d < s->dim; d++)
         if (s->p[d] != s->p[0]) { set_error("degree must be equal on all axes in this build"); return IGA_ERR_PARAM; }

@@ -90,6 +90,8 @@ void k_zero_vec(double *p, long long n, cudaStream_t st, int nsm);
 void k_zero_pair(double *p, long long n, double *q, long long m, cudaStream_t st, int nsm);   // p and/or q may be null
 iga_status launch_fused2d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
+iga_status launch_fused2dm(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
+                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b, const double *U,
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st);
