@@ -93,7 +93,7 @@ def test_term_groups(cid, n, groups):
         assert vec_rel_err(Fo, F) <= ROW_TOL
 
 
-@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5, 6])
 def test_full_size_probe_rows(cid):
     """BASELINE full sizes, the launch bench.py times: complete probe rows vs the oracle's
     row-subset assembly (SURVEY O-10), pattern of those rows bit-exact, row lengths of ALL rows.
