@@ -456,10 +456,52 @@ def run_basis3(args, w, local):
     return 0
 
 
+def run_residual(args, w, local):
+    """Secondary measurement: the residual call alone, iga_form_residual."""
+    import torch
+    import paper_1305_4452_b200 as iga
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    sp = iga.Space.from_workload(w, device=local)
+    U, Ud = torch.from_numpy(w.U).to(dev), torch.from_numpy(w.Udot).to(dev)
+    F = torch.empty(sp.nrows, dtype=torch.float64, device=dev)
+    ph = iga.make_phys(w.phys, w.params)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        sp.form_residual(ph, U, Ud, F=F)
+    sp.check()
+    ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            sp.form_residual(ph, U, Ud, F=F)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+    sp.check()
+    t = statistics.mean(ms)
+    cid = w.cid
+    t_roof = max(F_R[cid] * sp.nqp / (P64_NOMINAL_TFLOPS * 1e12),
+                 (3 * 8.0 * sp.nrows) / (load_peaks().get("hbm_gbs", 6650.0) * 1e9))
+    print(json.dumps({
+        "metric": "Residual assembly quadrature points/sec (fp64)", "value": sp.nqp / (t * 1e-3), "unit": "qpts/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "op": "iga_form_residual", "l2": "flushed (512 MiB write) between steps"},
+        "roofline": {"bound": "alu", "achieved": F_R[cid] * sp.nqp / (t * 1e-3) / 1e12, "peak": P64_NOMINAL_TFLOPS,
+                     "unit": "TFLOP/s", "frac": t_roof / (t * 1e-3), "model": "F_R rank-form flops/qpt (SURVEY §8(d))"},
+        "clocks": clk.summary()}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--op", default="jacobian", choices=["jacobian", "basis3"],
-                    help="jacobian: the headline assembly step; basis3: third-order basis evaluation")
+    ap.add_argument("--op", default="jacobian", choices=["jacobian", "residual", "basis3"],
+                    help="jacobian: the headline assembly step; residual: the residual call alone; "
+                         "basis3: third-order basis evaluation")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
@@ -484,6 +526,8 @@ def main():
         return run_reference(args, w, ws, rank)
     if args.op == "basis3":
         return run_basis3(args, w, local)
+    if args.op == "residual":
+        return run_residual(args, w, local)
     return run_iga(args, w, ws, rank, local)
 
 
