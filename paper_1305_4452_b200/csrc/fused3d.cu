@@ -66,6 +66,10 @@ struct F3 {
     static constexpr int O_RS = O_D + NQ * DQS;              // long long [NEN*M] row starts
     static constexpr int O_ND = O_RS + NEN * M;              // long long [NEN] nodes
     static constexpr size_t SMEM = (size_t)(O_ND + NEN) * sizeof(double);
+    // residual only: no coefficient blocks -- row starts (unused) and node numbers right after Phi
+    static constexpr int O_RS_RES = O_PHI + NQ * M * (NKS + 1);
+    static constexpr int O_ND_RES = O_RS_RES + NEN * M;
+    static constexpr size_t SMEM_RES = (size_t)(O_ND_RES + NEN) * sizeof(double);
     static_assert(NQ * M * (NKS + 1) <= NQ * DQS, "Phi must fit in the D region");
 };
 
@@ -206,7 +210,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
 }
 
 template <int P, class PH, bool JAC, bool UNI>
-__global__ void __launch_bounds__(F3<P, PH>::NT, F3<P, PH>::MINB)
+__global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3<P, PH>::MINB : 4)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
           int dbg, int bw) {
@@ -223,8 +227,8 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     // [NEN*M] CSR row (A, i): offset of its first value from `val`, in doubles.  Halo rows live in
     // the halo buffer; their offsets are taken in the flat 64-bit address space (both arrays are
     // 8-byte aligned) so the scatter below addresses everything from the uniform `val` register.
-    long long *sRS = reinterpret_cast<long long *>(sm + F::O_RS);
-    long long *sNode = reinterpret_cast<long long *>(sm + F::O_ND); // [NEN] touched-box node of A
+    long long *sRS = reinterpret_cast<long long *>(sm + (JAC ? F::O_RS : F::O_RS_RES));
+    long long *sNode = reinterpret_cast<long long *>(sm + (JAC ? F::O_ND : F::O_ND_RES)); // [NEN] touched-box node
     __shared__ int sG[3 * NP1], sW[3 * NP1], sPosE[3 * NP1 * NP1], sSeg[3 * NP1];
     __shared__ long long sS[3 * NP1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -638,7 +642,8 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
             ut.hp[d] = s->hp0[d];
         }
     const bool jac = val != nullptr;
-    const size_t smem = FF::SMEM;
+    const bool jac_ = val != nullptr;
+    const size_t smem = jac_ ? FF::SMEM : FF::SMEM_RES;
     static bool attr[2] = {false, false};
     if (!attr[jac]) {
         cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused3d<P, PH, true, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
