@@ -21,7 +21,8 @@
  *  - CSR: row_ptr int64 [nrows+1] (config 5 has 4.19e9 nonzeros > 2^31), col_idx int32 [nnz]
  *    global dof indices, ascending within each row; csr_val fp64 [nnz].
  *  - Every call that takes a cudaStream_t (passed as void*) is asynchronous on that stream
- *    and allocates no device memory.  Buffers must stay alive until the stream reaches them.
+ *    and allocates no device memory (iga_gmres excepted, see there).  Buffers must stay alive
+ *    until the stream reaches them.
  *  - Errors: every call returns an iga_status; iga_last_error() gives a thread-local message.
  *    Argument / knot / continuity validation is synchronous.  Device-side conditions
  *    (detJ <= 0, SURVEY A-7; non-finite integrand) set a device flag that
@@ -192,6 +193,34 @@ iga_status iga_form_residual_group(int n, const iga_space *spaces, const iga_phy
  * out: device fp64, caller-allocated.  order in [0, 3]; IGA_ERR_PARAM otherwise.  A point with
  * detJ <= 0 sets the device flag (iga_space_check -> IGA_ERR_SINGULAR_MAP). */
 iga_status iga_basis_eval(iga_space s, int order, double *out, void *stream);
+
+/* Linear solve with the assembled Jacobian -- the Newton step's J dU = -F of the paper's
+ * solver protocol (§5: "30 GMRES iterations per Newton iteration", "block Jacobi
+ * ... ILU(0) ... in each block").  Right-preconditioned restarted GMRES(restart) (Saad-Schultz,
+ * cited P:872), classical Gram-Schmidt applied twice, Givens rotations; stops when the
+ * preconditioned-Krylov residual estimate |g_{j+1}| <= rtol * ||b|| or after maxit total
+ * iterations.  Preconditioner `precond`: 0 none, 1 point Jacobi (diag), 2 block Jacobi with ILU(0)
+ * (Saad's IKJ ILU(0), no fill) in each diagonal block of `block_rows` consecutive rows (0 -> 64;
+ * reading A-28: the GPU's blocks are row runs, not one per process).  Entries outside the block
+ * are not part of the preconditioner.
+ * row_ptr/col_idx/val: this space's CSR (iga_csr_pattern + iga_form_jacobian), device, sorted
+ * columns, every row holding its diagonal.  b (rhs) and x (initial guess in, solution out):
+ * device fp64 of nrows_owned.  Workspace ((2 restart + 3) n doubles + the packed preconditioner,
+ * or nnz doubles for blocks > 64 rows) is allocated on first use, kept with the space for later
+ * calls and freed by iga_space_destroy; the call synchronises `stream`.
+ * iters (total iterations) / relres (TRUE ||b - A x|| / ||b|| of the returned x) may be NULL.
+ * Single-rank spaces only (IGA_ERR_STATE otherwise); IGA_ERR_NOMEM if the workspace does not
+ * fit. */
+typedef struct {
+    int restart;    /* m, Krylov dimension per cycle (paper: 30) */
+    int maxit;      /* total iteration cap (paper: 30 per Newton step) */
+    double rtol;    /* relative tolerance on ||b - A x|| / ||b|| */
+    int precond;    /* 0 none, 1 Jacobi, 2 block-Jacobi ILU(0) */
+    int block_rows; /* rows per block-Jacobi block (precond 2); 0 -> 64 */
+} iga_krylov;
+iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
+                     const double *b, double *x, const iga_krylov *opt, int *iters, double *relres,
+                     void *stream);
 
 /* Synchronises `stream` and reports (then clears) the device error flag of the last form
  * call: IGA_OK, IGA_ERR_SINGULAR_MAP or IGA_ERR_NONFINITE. */

@@ -52,6 +52,14 @@ class _Msg(C.Structure):
 XPORT_NCCL, XPORT_LOCAL = 0, 1
 
 
+class _Krylov(C.Structure):
+    _fields_ = [("restart", C.c_int), ("maxit", C.c_int), ("rtol", C.c_double), ("precond", C.c_int),
+                ("block_rows", C.c_int)]
+
+
+PC_NONE, PC_JACOBI, PC_BJACOBI_ILU0 = 0, 1, 2
+
+
 class _Phys(C.Structure):
     _fields_ = [("kind", C.c_int), ("p", C.c_double * 8)]
 
@@ -62,7 +70,7 @@ EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_p
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
            "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
            "iga_microbench", "iga_space_set_option", "iga_form_jacobian_group", "iga_form_residual_group",
-           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval"]
+           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres"]
 
 
 def lib():
@@ -102,12 +110,13 @@ def lib():
                                     C.POINTER(_Msg), C.POINTER(C.c_int), C.POINTER(_Msg), C.POINTER(C.c_int)]
         L.iga_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte * 128)]
         L.iga_basis_eval.argtypes = [vp, C.c_int, vp, vp]
+        L.iga_gmres.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
         L.iga_last_error.restype = C.c_char_p
         L.iga_version.restype = C.c_char_p
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
                   "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
                   "iga_profile_reset", "iga_form_jacobian_group", "iga_form_residual_group", "iga_dist_plan",
-                  "iga_nccl_unique_id", "iga_basis_eval"):
+                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -357,6 +366,21 @@ class Space:
             out = torch.empty((nel, nen, ncomp, nq), dtype=torch.float64, device=torch.device("cuda", self.device))
         _check(lib().iga_basis_eval(self.h, int(order), _ptr(out), _stream(stream)))
         return out
+
+    def gmres(self, row_ptr, col_idx, val, b, x=None, restart=30, maxit=30, rtol=1e-8, precond=PC_BJACOBI_ILU0,
+              block_rows=64, stream=None):
+        """Solve J x = b with this space's assembled CSR (iga_gmres: right-preconditioned GMRES,
+        block-Jacobi ILU(0)); x (device fp64) is the initial guess (zeros if None) and is
+        overwritten.  Returns (x, iterations, true relative residual)."""
+        import torch
+        if x is None:
+            x = torch.zeros_like(b)
+        opt = _Krylov(int(restart), int(maxit), float(rtol), int(precond), int(block_rows))
+        it = C.c_int(0)
+        rr = C.c_double(0.0)
+        _check(lib().iga_gmres(self.h, _ptr(row_ptr), _ptr(col_idx), _ptr(val), _ptr(b), _ptr(x), C.byref(opt),
+                               C.byref(it), C.byref(rr), _stream(stream)))
+        return x, int(it.value), float(rr.value)
 
     def check(self, stream=None):
         _check(lib().iga_space_check(self.h, _stream(stream)))

@@ -53,12 +53,15 @@ struct iga_space_s {
     int bw_opt = 0;                      // 3D element-order block width override (0: from the L2 size)
     int skip_zero = 0;                   // dist.cu: the caller zeroed the outputs (sub-box launches)
     int last_occupancy = 0;
-    int dbg = 0;                         // experiment bits (bench A/B only; results invalid when set)               // 1: never use the uniform-table fast paths
+    int dbg = 0;                         // experiment bits (bench A/B only; results invalid when set)
     // per axis: all elements share the same 1D tables / weights / span length (uniform knots,
     // translation invariance; equal to 1e-13 relative) -> element-0 copies (host)
     int tab_uniform[3] = {0, 0, 0};
     std::vector<double> tab0[3], qw0[3];
-    double hp0[3] = {1.0, 1.0, 1.0};                 // 1: use the generic split kernels (tests / A-B checks)
+    double hp0[3] = {1.0, 1.0, 1.0};
+    // iga_gmres workspace (solver.cu): [0] Krylov vectors, [1] preconditioner; kept until destroy
+    void *gm_buf[2] = {nullptr, nullptr};
+    size_t gm_cap[2] = {0, 0};
     // kernel timing hook (iga_profile_*)
     struct ProfRec { const char *name; cudaEvent_t a, b; };
     bool prof_on = false;
@@ -96,6 +99,8 @@ iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b
                           const double *Ud, double *val, double *F, cudaStream_t st, int nsm);
 iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cudaStream_t st);
 iga_status launch_basis3(iga_space_s *s, int order, double *out, cudaStream_t st);   // basis3.cu
+iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, const double *a, const double *b, double *x,
+                       const iga_krylov *opt, int *iters, double *relres, cudaStream_t st);        // solver.cu
 // dist.cu
 iga_status dist_setup(iga_space_s *s, const iga_dist *dist);
 void dist_destroy(iga_space_s *s);

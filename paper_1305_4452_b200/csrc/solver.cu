@@ -1,0 +1,638 @@
+// solver.cu -- Newton-Krylov linear solve around the assembly (the paper's
+// §5 protocol: "30 GMRES iterations per Newton iteration", "block Jacobi ... ILU(0)
+// ... in each block").  Right-preconditioned restarted GMRES(m) (Saad 1986, cited P:872) with
+// classical Gram-Schmidt and DGKS selective reorthogonalisation (one multi-dot and one fused
+// multi-axpy + normalise kernel per pass instead of j dependent dot products), Givens rotations
+// on the host.  Preconditioner: block
+// Jacobi with ILU(0) in each block.  Reading A-28: on one GPU "one block per process"
+// would serialise the triangular solves, so the blocks are contiguous runs of `block_rows` rows
+// (default 64): one thread each over packed in-block entries for blocks <= 64 rows, one warp each
+// over the CSR otherwise (the factor and the solves are sequential over a block's rows).  All vector work runs in the kernels below; the host only does the (m+1) x m
+// Hessenberg least-squares update.
+#include <cmath>
+#include <vector>
+
+#include "iga_host.h"
+
+namespace iga {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// out[k] += sum_i V[k][i] w[i] for k < nk (V rows of length ld); block partial sums + fp64 atomics
+__global__ void k_multidot(long long n, int nk, const double *__restrict__ V, long long ld, const double *__restrict__ w,
+                           double *__restrict__ out) {
+    __shared__ double part[32][9];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int k0 = 0; k0 < nk; k0 += 8) {
+        const int kc = min(8, nk - k0);
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+            const double wi = w[i];
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (k < kc) acc[k] += V[(k0 + k) * ld + i] * wi;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const double v = warp_sum(acc[k]);
+            if (lane == 0) part[wid][k] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < kc) {
+            double s = 0.0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); q++) s += part[q][threadIdx.x];
+            atomicAdd(out + k0 + threadIdx.x, s);
+        }
+        __syncthreads();
+    }
+}
+
+// w = (w - sum_k V[k] h[k]) * scale
+__global__ void k_multiaxpy(long long n, int nk, const double *__restrict__ V, long long ld, const double *__restrict__ h,
+                            double *w, double scale) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double s = w[i];
+        for (int k = 0; k < nk; k++) s -= h[k] * V[k * ld + i];
+        w[i] = s * scale;
+    }
+}
+
+// y = alpha x + beta y
+__global__ void k_axpby(long long n, double alpha, const double *__restrict__ x, double beta, double *__restrict__ y) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = alpha * x[i] + beta * y[i];
+}
+
+// position of the diagonal entry of every row (-1 if absent)
+__global__ void k_diagpos(long long n, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci, int64_t *__restrict__ dp) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long lo = rp[i], hi = rp[i + 1] - 1, pos = -1;
+    while (lo <= hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (ci[mid] == i) { pos = mid; break; }
+        if (ci[mid] < i) lo = mid + 1; else hi = mid - 1;
+    }
+    dp[i] = pos;
+}
+
+__device__ __forceinline__ long long find_col(const int64_t *rp, const int32_t *ci, long long row, int col) {
+    long long lo = rp[row], hi = rp[row + 1] - 1;
+    while (lo <= hi) {
+        const long long mid = (lo + hi) >> 1;
+        const int c = ci[mid];
+        if (c == col) return mid;
+        if (c < col) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+// ILU(0) of each diagonal block [r0, r0+B) (IKJ variant, Saad's ILU(0)): warp per block, rows in
+// order, for each lower entry k of the row (ascending): l_ik = a_ik / u_kk, then a_ij -= l_ik u_kj
+// for the row's entries j > k (lanes), u_kj found by binary search in row k.  Entries whose column
+// leaves the block are not part of the preconditioner.
+__global__ void k_ilu0(long long n, int B, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                       const int64_t *__restrict__ dp, double *__restrict__ lu) {
+    const long long blk = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long r0 = blk * B;
+    if (r0 >= n) return;
+    const long long r1 = min(n, r0 + B);
+    for (long long i = r0; i < r1; i++) {
+        const long long pb = rp[i], pe = rp[i + 1];
+        for (long long p = pb; p < pe; p++) {
+            const int k = ci[p];
+            if (k >= i) break;
+            if (k < r0) continue;
+            double lik = 0.0;
+            if (lane == 0) lik = lu[p] / lu[dp[k]];
+            lik = __shfl_sync(0xffffffffu, lik, 0);
+            __syncwarp();
+            if (lane == 0) lu[p] = lik;
+            for (long long q = p + 1 + lane; q < pe; q += 32) {
+                const int j = ci[q];
+                if (j >= r1) continue;
+                const long long kq = find_col(rp, ci, k, j);
+                if (kq >= 0) lu[q] -= lik * lu[kq];
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// z = (LU)^{-1} r per block: forward (unit L) then backward (U), warp per block
+__global__ void k_ilu0_solve(long long n, int B, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                             const int64_t *__restrict__ dp, const double *__restrict__ lu, const double *__restrict__ r,
+                             double *__restrict__ z) {
+    const long long blk = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long r0 = blk * B;
+    if (r0 >= n) return;
+    const long long r1 = min(n, r0 + B);
+    for (long long i = r0; i < r1; i++) {
+        double s = 0.0;
+        for (long long p = rp[i] + lane; p < dp[i]; p += 32) {
+            const int k = ci[p];
+            if (k >= r0) s += lu[p] * z[k];
+        }
+        s = warp_sum(s);
+        if (lane == 0) z[i] = r[i] - s;
+        __syncwarp();
+    }
+    for (long long i = r1 - 1; i >= r0; i--) {
+        double s = 0.0;
+        for (long long p = dp[i] + 1 + lane; p < rp[i + 1]; p += 32) {
+            const int j = ci[p];
+            if (j < r1) s += lu[p] * z[j];
+        }
+        s = warp_sum(s);
+        if (lane == 0) z[i] = (z[i] - s) / lu[dp[i]];
+        __syncwarp();
+    }
+}
+
+// Same solve for blocks of <= 1024 rows, latency-hidden: the block's z lives in shared memory and
+// the rows are taken in groups of G whose (independent) row-pointer / first-chunk / rhs loads are
+// all issued before the group's sequential dependency chain runs out of shared memory.
+constexpr int ILU_G = 8;
+__global__ void __launch_bounds__(128) k_ilu0_solve_g(long long n, int B, const int64_t *__restrict__ rp,
+                                                      const int32_t *__restrict__ ci, const int64_t *__restrict__ dp,
+                                                      const double *__restrict__ lu, const double *__restrict__ r,
+                                                      double *__restrict__ z) {
+    extern __shared__ double zsm[];
+    const long long blk = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    double *zs = zsm + (threadIdx.x >> 5) * B;
+    const long long r0 = blk * B;
+    if (r0 >= n) return;
+    const int nb = (int)min((long long)B, n - r0);
+    for (int i0 = 0; i0 < nb; i0 += ILU_G) {
+        long long pb[ILU_G], pd[ILU_G];
+        double rr[ILU_G], lc[ILU_G];
+        int kc[ILU_G];
+#pragma unroll
+        for (int g = 0; g < ILU_G; g++) {
+            const long long i = r0 + min(i0 + g, nb - 1);
+            pb[g] = rp[i];
+            pd[g] = dp[i];
+            rr[g] = r[i];
+        }
+#pragma unroll
+        for (int g = 0; g < ILU_G; g++) {
+            const long long p = pb[g] + lane;
+            kc[g] = -1;
+            lc[g] = 0.0;
+            if (p < pd[g]) { kc[g] = (int)(ci[p] - r0); lc[g] = lu[p]; }
+        }
+#pragma unroll
+        for (int g = 0; g < ILU_G; g++) {
+            if (i0 + g < nb) {
+                double s = kc[g] >= 0 ? lc[g] * zs[kc[g]] : 0.0;
+                for (long long p = pb[g] + 32 + lane; p < pd[g]; p += 32) {
+                    const long long k = ci[p] - r0;
+                    if (k >= 0) s += lu[p] * zs[k];
+                }
+                s = warp_sum(s);
+                if (lane == 0) zs[i0 + g] = rr[g] - s;
+                __syncwarp();
+            }
+        }
+    }
+    for (int i0 = nb - 1; i0 >= 0; i0 -= ILU_G) {
+        long long pd[ILU_G], pe[ILU_G];
+        double dv[ILU_G], lc[ILU_G];
+        int jc[ILU_G];
+#pragma unroll
+        for (int g = 0; g < ILU_G; g++) {
+            const long long i = r0 + max(i0 - g, 0);
+            pd[g] = dp[i];
+            pe[g] = rp[i + 1];
+        }
+#pragma unroll
+        for (int g = 0; g < ILU_G; g++) {
+            const long long p = pd[g] + 1 + lane;
+            dv[g] = lu[pd[g]];
+            jc[g] = -1;
+            lc[g] = 0.0;
+            if (p < pe[g]) {
+                const long long j = ci[p] - r0;
+                if (j < nb) { jc[g] = (int)j; lc[g] = lu[p]; }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < ILU_G; g++) {
+            if (i0 - g >= 0) {
+                double s = jc[g] >= 0 ? lc[g] * zs[jc[g]] : 0.0;
+                for (long long p = pd[g] + 33 + lane; p < pe[g]; p += 32) {
+                    const long long j = ci[p] - r0;
+                    if (j < nb) s += lu[p] * zs[j];
+                }
+                s = warp_sum(s);
+                if (lane == 0) zs[i0 - g] = (zs[i0 - g] - s) / dv[g];
+                __syncwarp();
+            }
+        }
+    }
+    for (int i = lane; i < nb; i += 32) z[r0 + i] = zs[i];
+}
+
+// ---- small-block path (block_rows <= 64, the default): one THREAD per block ------------------
+// The preconditioner only ever uses a block's in-block entries, so after the pattern is known they
+// are packed once per solve into slot-major arrays -- value, 8-bit column offset inside the block --
+// indexed ((il * W + slot) * nblk + blk): consecutive lanes (= consecutive blocks) read consecutive
+// words, and no load of the solve depends on data (no row_ptr / diag-position chains).  Padding
+// slots hold value 0 and offset 0.  The factor (IKJ ILU(0), as k_ilu0) and the triangular solves
+// then run as one sequential chain per thread, the block's z in a padded shared-memory row.
+constexpr int TPB_MAXB = 64, TPB_MAXW = 16, TPB_CTA = 64;
+
+__device__ __forceinline__ long long ell_at(int il, int s, int W, long long nblk, long long blk) {
+    return ((long long)il * W + s) * nblk + blk;
+}
+
+// in-block lower / upper entry counts of every row -> maxima (wmax[0], wmax[1])
+__global__ void k_ell_count(long long n, int B, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                            const int64_t *__restrict__ dp, int *__restrict__ wmax) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int nl = 0, nu = 0;
+    if (i < n) {
+        const long long r0 = (i / B) * B, r1 = min(n, r0 + B);
+        for (long long p = rp[i]; p < dp[i]; p++) nl += ci[p] >= r0;
+        for (long long p = dp[i] + 1; p < rp[i + 1]; p++) nu += ci[p] < r1;
+    }
+    nl = __reduce_max_sync(0xffffffffu, nl);
+    nu = __reduce_max_sync(0xffffffffu, nu);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(wmax, nl);
+        atomicMax(wmax + 1, nu);
+    }
+}
+
+// pack the in-block entries of A (rows >= n of the ragged last block: empty, D = 1)
+__global__ void k_ell_pack(long long n, int B, long long nblk, const int64_t *__restrict__ rp,
+                           const int32_t *__restrict__ ci, const int64_t *__restrict__ dp, const double *__restrict__ a,
+                           int WL, int WU, double *__restrict__ Lv, uint8_t *__restrict__ Lc, double *__restrict__ Uv,
+                           uint8_t *__restrict__ Uc, double *__restrict__ D) {
+    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nblk * B) return;
+    const long long blk = g / B;
+    const int il = (int)(g % B);
+    const long long r0 = blk * B, r1 = min(n, r0 + B);
+    int sl = 0, su = 0;
+    if (g < n) {
+        for (long long p = rp[g]; p < dp[g]; p++)
+            if (ci[p] >= r0) {
+                Lv[ell_at(il, sl, WL, nblk, blk)] = a[p];
+                Lc[ell_at(il, sl, WL, nblk, blk)] = (uint8_t)(ci[p] - r0);
+                sl++;
+            }
+        for (long long p = dp[g] + 1; p < rp[g + 1]; p++)
+            if (ci[p] < r1) {
+                Uv[ell_at(il, su, WU, nblk, blk)] = a[p];
+                Uc[ell_at(il, su, WU, nblk, blk)] = (uint8_t)(ci[p] - r0);
+                su++;
+            }
+        D[(long long)il * nblk + blk] = a[dp[g]];
+    } else {
+        D[(long long)il * nblk + blk] = 1.0;
+    }
+    for (; sl < WL; sl++) { Lv[ell_at(il, sl, WL, nblk, blk)] = 0.0; Lc[ell_at(il, sl, WL, nblk, blk)] = 0; }
+    for (; su < WU; su++) { Uv[ell_at(il, su, WU, nblk, blk)] = 0.0; Uc[ell_at(il, su, WU, nblk, blk)] = 0; }
+}
+
+// ILU(0) in place on the packed block, thread per block, row il held in local arrays.  Padding
+// lower slots act as k = 0 with a_ik = 0, so l = 0 and they change nothing; padding upper slots
+// (offset 0) never match a column j > k >= 0.
+__global__ void k_ell_ilu0(long long nblk, int B, int WL, int WU, double *__restrict__ Lv, const uint8_t *__restrict__ Lc,
+                           double *__restrict__ Uv, const uint8_t *__restrict__ Uc, double *__restrict__ D) {
+    const long long blk = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (blk >= nblk) return;
+    double lv[TPB_MAXW], uv[TPB_MAXW];
+    int lc[TPB_MAXW], uc[TPB_MAXW];
+    for (int il = 0; il < B; il++) {
+        for (int t = 0; t < WL; t++) { lv[t] = Lv[ell_at(il, t, WL, nblk, blk)]; lc[t] = Lc[ell_at(il, t, WL, nblk, blk)]; }
+        for (int t = 0; t < WU; t++) { uv[t] = Uv[ell_at(il, t, WU, nblk, blk)]; uc[t] = Uc[ell_at(il, t, WU, nblk, blk)]; }
+        double d = D[(long long)il * nblk + blk];
+        for (int t = 0; t < WL; t++) {
+            const int k = lc[t];
+            const double l = lv[t] / D[(long long)k * nblk + blk];
+            lv[t] = l;
+            if (l == 0.0) continue;
+            for (int s = 0; s < WU; s++) {
+                const double ukj = Uv[ell_at(k, s, WU, nblk, blk)];
+                const int j = Uc[ell_at(k, s, WU, nblk, blk)];
+                if (j <= k) continue;                           // padding
+                if (j == il) d -= l * ukj;
+                else if (j < il) {
+                    for (int t2 = t + 1; t2 < WL; t2++)
+                        if (lc[t2] == j) { lv[t2] -= l * ukj; break; }
+                } else {
+                    for (int t2 = 0; t2 < WU; t2++)
+                        if (uc[t2] == j) { uv[t2] -= l * ukj; break; }
+                }
+            }
+        }
+        for (int t = 0; t < WL; t++) Lv[ell_at(il, t, WL, nblk, blk)] = lv[t];
+        for (int t = 0; t < WU; t++) Uv[ell_at(il, t, WU, nblk, blk)] = uv[t];
+        D[(long long)il * nblk + blk] = d;
+    }
+}
+
+// W = padded slot count (2, 4, 8, 16).  Rows go in chunks of PF whose slot loads (independent of
+// the chain) are all issued before the chunk's sequential updates out of shared memory.
+template <int W>
+__global__ void __launch_bounds__(TPB_CTA) k_ell_solve(long long n, int B, long long nblk, const double *__restrict__ Lv,
+                                                       const uint8_t *__restrict__ Lc, const double *__restrict__ Uv,
+                                                       const uint8_t *__restrict__ Uc, const double *__restrict__ D,
+                                                       const double *__restrict__ r, double *__restrict__ z) {
+    constexpr int PF = W >= 16 ? 1 : 16 / W;
+    extern __shared__ double zsm[];
+    const int tid = threadIdx.x, ld = B + 1;
+    const long long cta_r0 = (long long)blockIdx.x * TPB_CTA * B;
+    for (int idx = tid; idx < TPB_CTA * B; idx += TPB_CTA) {
+        const long long g = cta_r0 + idx;
+        zsm[(idx / B) * ld + idx % B] = g < n ? r[g] : 0.0;
+    }
+    __syncthreads();
+    const long long blk = (long long)blockIdx.x * TPB_CTA + tid;
+    if (blk < nblk) {
+        double *my = zsm + tid * ld;
+        for (int c = 0; c < B; c += PF) {
+            double v[PF][W];
+            int k[PF][W];
+#pragma unroll
+            for (int q = 0; q < PF; q++) {
+                const int il = min(c + q, B - 1);
+#pragma unroll
+                for (int t = 0; t < W; t++) {
+                    v[q][t] = Lv[ell_at(il, t, W, nblk, blk)];
+                    k[q][t] = Lc[ell_at(il, t, W, nblk, blk)];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < PF; q++) {
+                if (c + q < B) {
+                    double acc = my[c + q];
+#pragma unroll
+                    for (int t = 0; t < W; t++) acc -= v[q][t] * my[k[q][t]];
+                    my[c + q] = acc;
+                }
+            }
+        }
+        for (int c = B - 1; c >= 0; c -= PF) {
+            double v[PF][W], d[PF];
+            int k[PF][W];
+#pragma unroll
+            for (int q = 0; q < PF; q++) {
+                const int il = max(c - q, 0);
+                d[q] = D[(long long)il * nblk + blk];
+#pragma unroll
+                for (int t = 0; t < W; t++) {
+                    v[q][t] = Uv[ell_at(il, t, W, nblk, blk)];
+                    k[q][t] = Uc[ell_at(il, t, W, nblk, blk)];
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < PF; q++) {
+                if (c - q >= 0) {
+                    double acc = my[c - q];
+#pragma unroll
+                    for (int t = 0; t < W; t++) acc -= v[q][t] * my[k[q][t]];
+                    my[c - q] = acc / d[q];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < TPB_CTA * B; idx += TPB_CTA) {
+        const long long g = cta_r0 + idx;
+        if (g < n) z[g] = zsm[(idx / B) * ld + idx % B];
+    }
+}
+
+// y = A x with LPR lanes per row (short IGA rows: 4-16 lanes keep the warp's lanes busy)
+// (bsub != NULL: y = bsub - A x, the residual)
+template <int LPR>
+__global__ void k_spmv_sw(long long n, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                          const double *__restrict__ a, const double *__restrict__ x, double *__restrict__ y,
+                          const double *__restrict__ bsub) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long row = t / LPR;
+    const int sub = (int)(t % LPR);
+    double s = 0.0;
+    if (row < n)
+        for (long long p = rp[row] + sub; p < rp[row + 1]; p += LPR) s += a[p] * __ldg(x + ci[p]);
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (row < n && sub == 0) y[row] = bsub ? bsub[row] - s : s;
+}
+
+// z = D^{-1} r
+__global__ void k_jacobi(long long n, const int64_t *__restrict__ dp, const double *__restrict__ a, const double *__restrict__ r,
+                         double *__restrict__ z) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        z[i] = r[i] / a[dp[i]];
+}
+
+iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, const double *a, const double *b, double *x,
+                       const iga_krylov *opt, int *iters_out, double *relres_out, cudaStream_t st) {
+    const long long n = s->nrows_owned, nnz = s->nnz_owned;
+    const int m = std::max(1, opt->restart), maxit = std::max(0, opt->maxit);
+    const int B = opt->block_rows > 0 ? opt->block_rows : 64;
+    if (s->nranks > 1) { set_error("gmres: single-rank in this build"); return IGA_ERR_STATE; }
+    // workspace, cached on the space (gm_buf): [0] V[m+1][n], Z[m][n], w[n], dp[n], h[2(m+1)];
+    // [1] the preconditioner (packed blocks or the CSR copy of the ILU factor)
+    auto ensure = [&](int slot, size_t bytes) -> void * {
+        if (s->gm_cap[slot] < bytes) {
+            if (s->gm_buf[slot]) cudaFree(s->gm_buf[slot]);
+            s->gm_buf[slot] = nullptr;
+            s->gm_cap[slot] = 0;
+            if (cudaMalloc(&s->gm_buf[slot], bytes) != cudaSuccess) { cudaGetLastError(); s->gm_buf[slot] = nullptr; return nullptr; }
+            s->gm_cap[slot] = bytes;
+        }
+        return s->gm_buf[slot];
+    };
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t szV = al(sizeof(double) * (size_t)(m + 1) * n), szZ = al(sizeof(double) * (size_t)m * n),
+                 szw = al(sizeof(double) * (size_t)n), szdp = al(sizeof(int64_t) * (size_t)n),
+                 szh = al(sizeof(double) * 2 * (size_t)(m + 1));
+    char *base = (char *)ensure(0, szV + szZ + szw + szdp + szh);
+    if (!base) { set_error("gmres workspace"); return IGA_ERR_NOMEM; }
+    double *V = (double *)base, *Z = (double *)(base + szV), *w = (double *)(base + szV + szZ);
+    int64_t *dp = (int64_t *)(base + szV + szZ + szw);
+    double *dh = (double *)(base + szV + szZ + szw + szdp);
+    double *lu = nullptr, *Lv = nullptr, *Uv = nullptr, *Dd = nullptr;
+    uint8_t *Lc = nullptr, *Uc = nullptr;
+    cudaError_t ce = cudaSuccess;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    const unsigned gv = (unsigned)std::min<long long>((n + 255) / 256, (long long)nsm * 8);
+    const long long avg = n > 0 ? nnz / n : 0;
+    const int lpr = avg <= 12 ? 4 : avg <= 40 ? 8 : avg <= 96 ? 16 : 32;
+    const unsigned grow = (unsigned)((n * lpr + 255) / 256);
+    auto spmv = [&](const double *xin, double *yout, const double *bsub) {
+        if (lpr == 4) k_spmv_sw<4><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
+        else if (lpr == 8) k_spmv_sw<8><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
+        else if (lpr == 16) k_spmv_sw<16><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
+        else k_spmv_sw<32><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
+    };
+    const unsigned gblk = (unsigned)((((n + B - 1) / B) * 32 + 127) / 128);
+    int launches = 0;
+    k_diagpos<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, rp, ci, dp);
+    launches++;
+    // block-Jacobi ILU(0): packed thread-per-block path for small blocks, CSR warp path otherwise
+    const long long nblk = (n + B - 1) / B;
+    bool ell = false;
+    int WL = 0, WU = 0;
+    if (opt->precond == 2 && B <= TPB_MAXB && n > 0) {
+        int wm[2] = {0, 0};
+        cudaMemsetAsync(dh, 0, 2 * sizeof(int), st);
+        k_ell_count<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, B, rp, ci, dp, (int *)dh);
+        launches++;
+        cudaMemcpyAsync(wm, dh, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        const int wmax = std::max(wm[0], wm[1]);
+        WL = WU = wmax <= 2 ? 2 : wmax <= 4 ? 4 : wmax <= 8 ? 8 : 16;       // padded slot count
+        if (wmax <= TPB_MAXW) {
+            const size_t rows = (size_t)nblk * B;
+            const size_t sv = al(sizeof(double) * rows * WL), sd = al(sizeof(double) * rows), sc = al(rows * WL);
+            char *pb = (char *)ensure(1, 2 * sv + sd + 2 * sc);
+            if (!pb) { set_error("gmres workspace"); return IGA_ERR_NOMEM; }
+            Lv = (double *)pb;
+            Uv = (double *)(pb + sv);
+            Dd = (double *)(pb + 2 * sv);
+            Lc = (uint8_t *)(pb + 2 * sv + sd);
+            Uc = (uint8_t *)(pb + 2 * sv + sd + sc);
+            k_ell_pack<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(n, B, nblk, rp, ci, dp, a, WL, WU, Lv, Lc, Uv, Uc, Dd);
+            k_ell_ilu0<<<(unsigned)((nblk + 63) / 64), 64, 0, st>>>(nblk, B, WL, WU, Lv, Lc, Uv, Uc, Dd);
+            launches += 2;
+            ell = true;
+        }
+    }
+    if (opt->precond == 2 && !ell) {
+        lu = (double *)ensure(1, sizeof(double) * (size_t)nnz);
+        if (!lu) { set_error("gmres workspace"); return IGA_ERR_NOMEM; }
+        cudaMemcpyAsync(lu, a, sizeof(double) * (size_t)nnz, cudaMemcpyDeviceToDevice, st);
+        k_ilu0<<<gblk, 128, 0, st>>>(n, B, rp, ci, dp, lu);
+        launches++;
+    }
+    const unsigned gell = (unsigned)((nblk + TPB_CTA - 1) / TPB_CTA);
+    const size_t smell = sizeof(double) * (size_t)TPB_CTA * (B + 1);
+    auto precond = [&](const double *r, double *z) {
+        if (ell && WL == 2) k_ell_solve<2><<<gell, TPB_CTA, smell, st>>>(n, B, nblk, Lv, Lc, Uv, Uc, Dd, r, z);
+        else if (ell && WL == 4) k_ell_solve<4><<<gell, TPB_CTA, smell, st>>>(n, B, nblk, Lv, Lc, Uv, Uc, Dd, r, z);
+        else if (ell && WL == 8) k_ell_solve<8><<<gell, TPB_CTA, smell, st>>>(n, B, nblk, Lv, Lc, Uv, Uc, Dd, r, z);
+        else if (ell) k_ell_solve<16><<<gell, TPB_CTA, smell, st>>>(n, B, nblk, Lv, Lc, Uv, Uc, Dd, r, z);
+        else if (opt->precond == 2 && B <= 1024) k_ilu0_solve_g<<<gblk, 128, 4 * B * sizeof(double), st>>>(n, B, rp, ci, dp, lu, r, z);
+        else if (opt->precond == 2) k_ilu0_solve<<<gblk, 128, 0, st>>>(n, B, rp, ci, dp, lu, r, z);
+        else if (opt->precond == 1) k_jacobi<<<gv, 256, 0, st>>>(n, dp, a, r, z);
+        else cudaMemcpyAsync(z, r, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+        launches++;
+    };
+    auto norm2 = [&](const double *v) -> double {
+        cudaMemsetAsync(dh, 0, sizeof(double), st);
+        k_multidot<<<gv, 256, 0, st>>>(n, 1, v, n, v, dh);
+        launches++;
+        double h = 0.0;
+        cudaMemcpyAsync(&h, dh, sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        return std::sqrt(h);
+    };
+    const double bnorm = norm2(b);
+    const double target = opt->rtol * (bnorm > 0.0 ? bnorm : 1.0);
+    std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hcol(m + 1), y(m);
+    int it = 0;
+    double res = 0.0;
+    std::vector<double> hp(m + 2), ny(m);
+    while (true) {
+        // r = b - A x -> V[0]
+        spmv(x, V, b);
+        launches++;
+        const double beta = norm2(V);
+        res = beta;
+        if (beta <= target || it >= maxit) break;
+        k_axpby<<<gv, 256, 0, st>>>(n, 1.0 / beta, V, 0.0, V);
+        launches++;
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int j = 0;
+        for (; j < m && it < maxit; j++, it++) {
+            double *vj1 = V + (size_t)(j + 1) * n;
+            precond(V + (size_t)j * n, Z + (size_t)j * n);
+            spmv(Z + (size_t)j * n, vj1, nullptr);            // w, in place of v_{j+1}
+            launches++;
+            // classical Gram-Schmidt with DGKS selective reorthogonalisation: one multi-dot gives
+            // V_j^T w and w.w; ||w - V_j h||^2 = w.w - h.h when V_j is orthonormal; a second pass
+            // only when that loses more than half of w.w (eta = 1/sqrt 2).  The final pass
+            // normalises v_{j+1} in the same sweep.
+            std::fill(hcol.begin(), hcol.end(), 0.0);
+            double hj1 = 0.0;
+            for (int pass = 0; pass < 2; pass++) {
+                cudaMemsetAsync(dh, 0, sizeof(double) * (size_t)(j + 2), st);
+                k_multidot<<<gv, 256, 0, st>>>(n, j + 2, V, n, vj1, dh);
+                launches++;
+                cudaMemcpyAsync(hp.data(), dh, sizeof(double) * (size_t)(j + 2), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                double hh = 0.0;
+                for (int i = 0; i <= j; i++) { hh += hp[i] * hp[i]; hcol[i] += hp[i]; }
+                const double ww = hp[j + 1], nrm2 = ww - hh;
+                const bool last = pass == 1 || nrm2 > 0.5 * ww;
+                double scale = 1.0;
+                if (last) {
+                    hj1 = nrm2 > 0.0 ? std::sqrt(nrm2) : 0.0;
+                    if (hj1 > 0.0) scale = 1.0 / hj1;
+                }
+                k_multiaxpy<<<gv, 256, 0, st>>>(n, j + 1, V, n, dh, vj1, scale);
+                launches++;
+                if (last) break;
+            }
+            hcol[j + 1] = hj1;
+            // Givens
+            for (int i = 0; i < j; i++) {
+                const double t = cs[i] * hcol[i] + sn[i] * hcol[i + 1];
+                hcol[i + 1] = -sn[i] * hcol[i] + cs[i] * hcol[i + 1];
+                hcol[i] = t;
+            }
+            const double den = std::hypot(hcol[j], hcol[j + 1]);
+            cs[j] = den > 0.0 ? hcol[j] / den : 1.0;
+            sn[j] = den > 0.0 ? hcol[j + 1] / den : 0.0;
+            hcol[j] = den;
+            hcol[j + 1] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            for (int i = 0; i <= j; i++) H[(size_t)i * m + j] = hcol[i];
+            res = std::fabs(g[j + 1]);
+            if (res <= target || hj1 == 0.0) { j++; it++; break; }
+        }
+        // y = R^{-1} g, x += Z y (one multi-axpy with -y)
+        for (int i = j - 1; i >= 0; i--) {
+            double t = g[i];
+            for (int k = i + 1; k < j; k++) t -= H[(size_t)i * m + k] * y[k];
+            y[i] = t / H[(size_t)i * m + i];
+        }
+        for (int k = 0; k < j; k++) ny[k] = -y[k];
+        if (j > 0) {
+            cudaMemcpyAsync(dh, ny.data(), sizeof(double) * (size_t)j, cudaMemcpyHostToDevice, st);
+            k_multiaxpy<<<gv, 256, 0, st>>>(n, j, Z, n, dh, x, 1.0);
+            launches++;
+        }
+        if (res <= target || it >= maxit) {
+            // true residual of the final iterate
+            spmv(x, w, b);
+            launches++;
+            res = norm2(w);
+            break;
+        }
+    }
+    s->last_launches = launches;
+    if (iters_out) *iters_out = it;
+    if (relres_out) *relres_out = res / (bnorm > 0.0 ? bnorm : 1.0);
+    ce = cudaGetLastError();
+    if (ce != cudaSuccess) { set_error(std::string("gmres: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return IGA_OK;
+}
+
+}  // namespace iga

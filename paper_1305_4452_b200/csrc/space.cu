@@ -275,6 +275,7 @@ static void free_space(iga_space_s *s) {
     dist_destroy(s);
     for (cudaEvent_t e : s->prof_pool) cudaEventDestroy(e);
     for (void *p : s->allocs) cudaFree(p);
+    for (void *p : s->gm_buf) if (p) cudaFree(p);
     cudaSetDevice(prev);
     delete s;
 }
@@ -855,6 +856,21 @@ iga_status iga_basis_eval(iga_space s, int order, double *out, void *stream) {
     cudaGetDevice(&prev);
     cudaSetDevice(s->device);
     iga_status st = launch_basis3(s, order, out, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
+iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx, const double *val, const double *b,
+                     double *x, const iga_krylov *opt, int *iters, double *relres, void *stream) {
+    if (!s || !row_ptr || !col_idx || !val || !b || !x || !opt) { set_error("null argument"); return IGA_ERR_PARAM; }
+    if (opt->precond < 0 || opt->precond > 2 || opt->restart < 1 || opt->maxit < 0 || !(opt->rtol >= 0.0)) {
+        set_error("gmres: bad options");
+        return IGA_ERR_PARAM;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    iga_status st = gmres_solve(s, row_ptr, col_idx, val, b, x, opt, iters, relres, (cudaStream_t)stream);
     cudaSetDevice(prev);
     return st;
 }
