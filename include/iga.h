@@ -222,6 +222,35 @@ iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx
                      const double *b, double *x, const iga_krylov *opt, int *iters, double *relres,
                      void *stream);
 
+/* One generalized-alpha time step with a fixed-budget Newton loop -- eq. (ga) of P:697-709 with
+ * the rho_inf parametrisation of P:719-723 (am = (3 - rho)/(2 (1 + rho)), af = 1/(1 + rho),
+ * gamma = 1/2 + am - af), Newton on Udot_{n+1} from the constant-U predictor
+ * U_{n+1} = U_n, Udot_{n+1} = (gamma - 1)/gamma Udot_n (reading A-29), and the §5 protocol
+ * (P:866-876): exactly `newton_its` iterations, each
+ *     assemble R(U_{n+af}, Udot_{n+am}) and J = am dR/dUdot + af gamma dt dR/dU (iga_form_jacobian),
+ *     solve J dx = R with iga_gmres(krylov) from x = 0,   Udot_{n+1} -= dx,  U_{n+1} -= gamma dt dx.
+ * No convergence test (the paper's fixed budget: 2 Newton x 30 GMRES).  row_ptr/col_idx: this
+ * space's pattern; val: caller's device buffer of nnz doubles (holds the last Jacobian on
+ * return).  U, Udot: device, all rows; in: step n, out: step n+1.  Physics time-step parameters
+ * (e.g. NS-VMS p[1] = dt) are the caller's to keep consistent with opt->dt.  stats (may be NULL):
+ * ||R|| at each Newton iterate and each solve's iterations / true relative residual.
+ * Single-rank spaces; newton_its in [1, 8]; 0 <= rho_inf <= 1; dt > 0 (IGA_ERR_PARAM otherwise).
+ * Stage vectors (6 n doubles) are kept with the space; the call synchronises `stream`. */
+typedef struct {
+    double rho_inf;
+    double dt;
+    int newton_its;     /* paper: 2 */
+    iga_krylov krylov;  /* paper: GMRES, 30 iterations, block-Jacobi ILU(0) */
+} iga_alpha;
+typedef struct {
+    double res_norm[8];       /* ||R(U_{n+af}, Udot_{n+am})|| at Newton iterate k */
+    int gmres_its[8];
+    double gmres_relres[8];
+} iga_step_stats;
+iga_status iga_alpha_step(iga_space s, const iga_phys *phys, const iga_alpha *opt, const int64_t *row_ptr,
+                          const int32_t *col_idx, double *val, double *U, double *Udot,
+                          iga_step_stats *stats, void *stream);
+
 /* Synchronises `stream` and reports (then clears) the device error flag of the last form
  * call: IGA_OK, IGA_ERR_SINGULAR_MAP or IGA_ERR_NONFINITE. */
 iga_status iga_space_check(iga_space s, void *stream);

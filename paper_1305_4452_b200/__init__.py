@@ -60,6 +60,14 @@ class _Krylov(C.Structure):
 PC_NONE, PC_JACOBI, PC_BJACOBI_ILU0 = 0, 1, 2
 
 
+class _Alpha(C.Structure):
+    _fields_ = [("rho_inf", C.c_double), ("dt", C.c_double), ("newton_its", C.c_int), ("krylov", _Krylov)]
+
+
+class _StepStats(C.Structure):
+    _fields_ = [("res_norm", C.c_double * 8), ("gmres_its", C.c_int * 8), ("gmres_relres", C.c_double * 8)]
+
+
 class _Phys(C.Structure):
     _fields_ = [("kind", C.c_int), ("p", C.c_double * 8)]
 
@@ -70,7 +78,7 @@ EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_p
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
            "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
            "iga_microbench", "iga_space_set_option", "iga_form_jacobian_group", "iga_form_residual_group",
-           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres"]
+           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step"]
 
 
 def lib():
@@ -111,12 +119,13 @@ def lib():
         L.iga_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte * 128)]
         L.iga_basis_eval.argtypes = [vp, C.c_int, vp, vp]
         L.iga_gmres.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
+        L.iga_alpha_step.argtypes = [vp, C.POINTER(_Phys), C.POINTER(_Alpha), vp, vp, vp, vp, vp, C.POINTER(_StepStats), vp]
         L.iga_last_error.restype = C.c_char_p
         L.iga_version.restype = C.c_char_p
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
                   "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
                   "iga_profile_reset", "iga_form_jacobian_group", "iga_form_residual_group", "iga_dist_plan",
-                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres"):
+                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -381,6 +390,20 @@ class Space:
         _check(lib().iga_gmres(self.h, _ptr(row_ptr), _ptr(col_idx), _ptr(val), _ptr(b), _ptr(x), C.byref(opt),
                                C.byref(it), C.byref(rr), _stream(stream)))
         return x, int(it.value), float(rr.value)
+
+    def alpha_step(self, phys, U, Udot, row_ptr, col_idx, val, rho_inf, dt, newton_its=2, restart=30, maxit=30,
+                   rtol=0.0, precond=PC_BJACOBI_ILU0, block_rows=64, stream=None):
+        """One generalized-alpha step with the fixed Newton / GMRES budget (iga_alpha_step); U and
+        Udot (device fp64) advance in place from step n to n+1; val is the Jacobian buffer.
+        Returns {"res_norm": [...], "gmres_its": [...], "gmres_relres": [...]} per Newton iterate."""
+        opt = _Alpha(float(rho_inf), float(dt), int(newton_its),
+                     _Krylov(int(restart), int(maxit), float(rtol), int(precond), int(block_rows)))
+        stt = _StepStats()
+        _check(lib().iga_alpha_step(self.h, C.byref(phys), C.byref(opt), _ptr(row_ptr), _ptr(col_idx), _ptr(val),
+                                    _ptr(U), _ptr(Udot), C.byref(stt), _stream(stream)))
+        k = int(newton_its)
+        return {"res_norm": list(stt.res_norm[:k]), "gmres_its": list(stt.gmres_its[:k]),
+                "gmres_relres": list(stt.gmres_relres[:k])}
 
     def check(self, stream=None):
         _check(lib().iga_space_check(self.h, _stream(stream)))

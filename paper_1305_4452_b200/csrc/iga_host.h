@@ -59,9 +59,10 @@ struct iga_space_s {
     int tab_uniform[3] = {0, 0, 0};
     std::vector<double> tab0[3], qw0[3];
     double hp0[3] = {1.0, 1.0, 1.0};
-    // iga_gmres workspace (solver.cu): [0] Krylov vectors, [1] preconditioner; kept until destroy
-    void *gm_buf[2] = {nullptr, nullptr};
-    size_t gm_cap[2] = {0, 0};
+    // iga_gmres workspace (solver.cu): [0] Krylov vectors, [1] preconditioner; kept until destroy;
+    // iga_alpha_step: [2] its stage vectors
+    void *gm_buf[3] = {nullptr, nullptr, nullptr};
+    size_t gm_cap[3] = {0, 0, 0};
     // kernel timing hook (iga_profile_*)
     struct ProfRec { const char *name; cudaEvent_t a, b; };
     bool prof_on = false;
@@ -101,6 +102,11 @@ iga_status launch_pattern(iga_space_s *s, int64_t *row_ptr, int32_t *col_idx, cu
 iga_status launch_basis3(iga_space_s *s, int order, double *out, cudaStream_t st);   // basis3.cu
 iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, const double *a, const double *b, double *x,
                        const iga_krylov *opt, int *iters, double *relres, cudaStream_t st);        // solver.cu
+iga_status alpha_step(iga_space_s *s, const iga_phys *phys, const iga_alpha *opt, const int64_t *rp, const int32_t *ci,
+                      double *val, double *U, double *Udot, iga_step_stats *stats, cudaStream_t st);  // solver.cu
+iga_status check_phys(iga_space_s *s, const iga_phys *phys);                                          // space.cu
+iga_status form_one(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U, const double *Ud,
+                    double *val, double *F, cudaStream_t st);                                         // space.cu
 // dist.cu
 iga_status dist_setup(iga_space_s *s, const iga_dist *dist);
 void dist_destroy(iga_space_s *s);

@@ -437,6 +437,18 @@ __global__ void k_jacobi(long long n, const int64_t *__restrict__ dp, const doub
         z[i] = r[i] / a[dp[i]];
 }
 
+// device buffer `slot` of the space's solver workspace, grown to >= bytes (contents not kept)
+static void *ws_ensure(iga_space_s *s, int slot, size_t bytes) {
+    if (s->gm_cap[slot] < bytes) {
+        if (s->gm_buf[slot]) cudaFree(s->gm_buf[slot]);
+        s->gm_buf[slot] = nullptr;
+        s->gm_cap[slot] = 0;
+        if (cudaMalloc(&s->gm_buf[slot], bytes) != cudaSuccess) { cudaGetLastError(); s->gm_buf[slot] = nullptr; return nullptr; }
+        s->gm_cap[slot] = bytes;
+    }
+    return s->gm_buf[slot];
+}
+
 iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, const double *a, const double *b, double *x,
                        const iga_krylov *opt, int *iters_out, double *relres_out, cudaStream_t st) {
     const long long n = s->nrows_owned, nnz = s->nnz_owned;
@@ -445,16 +457,7 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
     if (s->nranks > 1) { set_error("gmres: single-rank in this build"); return IGA_ERR_STATE; }
     // workspace, cached on the space (gm_buf): [0] V[m+1][n], Z[m][n], w[n], dp[n], h[2(m+1)];
     // [1] the preconditioner (packed blocks or the CSR copy of the ILU factor)
-    auto ensure = [&](int slot, size_t bytes) -> void * {
-        if (s->gm_cap[slot] < bytes) {
-            if (s->gm_buf[slot]) cudaFree(s->gm_buf[slot]);
-            s->gm_buf[slot] = nullptr;
-            s->gm_cap[slot] = 0;
-            if (cudaMalloc(&s->gm_buf[slot], bytes) != cudaSuccess) { cudaGetLastError(); s->gm_buf[slot] = nullptr; return nullptr; }
-            s->gm_cap[slot] = bytes;
-        }
-        return s->gm_buf[slot];
-    };
+    auto ensure = [&](int slot, size_t bytes) { return ws_ensure(s, slot, bytes); };
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t szV = al(sizeof(double) * (size_t)(m + 1) * n), szZ = al(sizeof(double) * (size_t)m * n),
                  szw = al(sizeof(double) * (size_t)n), szdp = al(sizeof(int64_t) * (size_t)n),
@@ -632,6 +635,91 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
     if (relres_out) *relres_out = res / (bnorm > 0.0 ? bnorm : 1.0);
     ce = cudaGetLastError();
     if (ce != cudaSuccess) { set_error(std::string("gmres: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return IGA_OK;
+}
+
+// ---- generalized-alpha step (eq. (ga)) with the §5 fixed Newton budget ----------
+// predictor: U1 = U, Ud1 = c Ud
+__global__ void k_ga_predict(long long n, const double *__restrict__ U, const double *__restrict__ Ud, double c,
+                             double *__restrict__ U1, double *__restrict__ Ud1) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        U1[i] = U[i];
+        Ud1[i] = c * Ud[i];
+    }
+}
+
+// stage values: Ua = U + af (U1 - U), Uda = Ud + am (Ud1 - Ud)
+__global__ void k_ga_stage(long long n, const double *__restrict__ U, const double *__restrict__ Ud,
+                           const double *__restrict__ U1, const double *__restrict__ Ud1, double af, double am,
+                           double *__restrict__ Ua, double *__restrict__ Uda) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        Ua[i] = U[i] + af * (U1[i] - U[i]);
+        Uda[i] = Ud[i] + am * (Ud1[i] - Ud[i]);
+    }
+}
+
+// Newton update: Ud1 -= dx, U1 -= gdt dx
+__global__ void k_ga_update(long long n, const double *__restrict__ dx, double gdt, double *__restrict__ U1,
+                            double *__restrict__ Ud1) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        Ud1[i] -= dx[i];
+        U1[i] -= gdt * dx[i];
+    }
+}
+
+iga_status alpha_step(iga_space_s *s, const iga_phys *phys, const iga_alpha *opt, const int64_t *rp, const int32_t *ci,
+                      double *val, double *U, double *Udot, iga_step_stats *stats, cudaStream_t st) {
+    if (s->nranks > 1) { set_error("alpha_step: single-rank in this build"); return IGA_ERR_STATE; }
+    const long long n = s->nrows_owned;
+    const double rho = opt->rho_inf, dt = opt->dt;
+    const double am = 0.5 * (3.0 - rho) / (1.0 + rho), af = 1.0 / (1.0 + rho), gamma = 0.5 + am - af;
+    const size_t vb = ((sizeof(double) * (size_t)n + 255) & ~(size_t)255);
+    char *base = (char *)ws_ensure(s, 2, 6 * vb + 256);
+    if (!base) { set_error("alpha_step workspace"); return IGA_ERR_NOMEM; }
+    double *U1 = (double *)base, *Ud1 = (double *)(base + vb), *Ua = (double *)(base + 2 * vb),
+           *Uda = (double *)(base + 3 * vb), *R = (double *)(base + 4 * vb), *dx = (double *)(base + 5 * vb),
+           *dn = (double *)(base + 6 * vb);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    const unsigned gv = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)nsm * 8));
+    int launches = 0;
+    if (stats) *stats = iga_step_stats{};
+    k_ga_predict<<<gv, 256, 0, st>>>(n, U, Udot, (gamma - 1.0) / gamma, U1, Ud1);
+    launches++;
+    for (int k = 0; k < opt->newton_its; k++) {
+        k_ga_stage<<<gv, 256, 0, st>>>(n, U, Udot, U1, Ud1, af, am, Ua, Uda);
+        launches++;
+        iga_status e = form_one(s, phys, am, af * gamma * dt, Ua, Uda, val, R, st);
+        if (e != IGA_OK) return e;
+        launches += s->last_launches;
+        if (stats) {
+            double r2 = 0.0;
+            cudaMemsetAsync(dn, 0, sizeof(double), st);
+            k_multidot<<<gv, 256, 0, st>>>(n, 1, R, n, R, dn);
+            launches++;
+            cudaMemcpyAsync(&r2, dn, sizeof(double), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            stats->res_norm[k] = std::sqrt(r2);
+        }
+        cudaMemsetAsync(dx, 0, sizeof(double) * (size_t)n, st);
+        int its = 0;
+        double rr = 0.0;
+        e = gmres_solve(s, rp, ci, val, R, dx, &opt->krylov, &its, &rr, st);
+        if (e != IGA_OK) return e;
+        launches += s->last_launches;
+        if (stats) {
+            stats->gmres_its[k] = its;
+            stats->gmres_relres[k] = rr;
+        }
+        k_ga_update<<<gv, 256, 0, st>>>(n, dx, gamma * dt, U1, Ud1);
+        launches++;
+    }
+    cudaMemcpyAsync(U, U1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(Udot, Ud1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+    cudaStreamSynchronize(st);
+    s->last_launches = launches;
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) { set_error(std::string("alpha_step: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
     return IGA_OK;
 }
 

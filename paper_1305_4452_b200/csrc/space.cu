@@ -652,6 +652,25 @@ fail:
 
 using namespace iga;
 
+iga_status iga::check_phys(iga_space s, const iga_phys *phys) {
+    if (!s || !phys) { set_error("null argument"); return IGA_ERR_PARAM; }
+    return IGA_OK;
+}
+
+// single-space form: one rank, or one rank of an NCCL decomposition
+iga_status iga::form_one(iga_space s, const iga_phys *phys, double a, double b, const double *U, const double *Ud,
+                           double *val, double *F, cudaStream_t st) {
+    if (s->nranks > 1) {
+        if (!s->dist || dist_transport(s->dist) != IGA_XPORT_NCCL) {
+            set_error("IGA_XPORT_LOCAL spaces form through iga_form_*_group");
+            return IGA_ERR_STATE;
+        }
+        return dist_form(&s, 1, phys, a, b, &U, &Ud, &val, &F, st);
+    }
+    return launch_form(s, phys, a, b, U, Ud, val, F, st);
+}
+
+
 extern "C" {
 
 const char *iga_last_error(void) { return g_err.c_str(); }
@@ -692,24 +711,6 @@ iga_status iga_csr_pattern(iga_space s, int64_t *row_ptr, int32_t *col_idx, void
     iga_status st = launch_pattern(s, row_ptr, col_idx, (cudaStream_t)stream);
     cudaSetDevice(prev);
     return st;
-}
-
-static iga_status check_phys(iga_space s, const iga_phys *phys) {
-    if (!s || !phys) { set_error("null argument"); return IGA_ERR_PARAM; }
-    return IGA_OK;
-}
-
-// single-space form: one rank, or one rank of an NCCL decomposition
-static iga_status form_one(iga_space s, const iga_phys *phys, double a, double b, const double *U, const double *Ud,
-                           double *val, double *F, cudaStream_t st) {
-    if (s->nranks > 1) {
-        if (!s->dist || dist_transport(s->dist) != IGA_XPORT_NCCL) {
-            set_error("IGA_XPORT_LOCAL spaces form through iga_form_*_group");
-            return IGA_ERR_STATE;
-        }
-        return dist_form(&s, 1, phys, a, b, &U, &Ud, &val, &F, st);
-    }
-    return launch_form(s, phys, a, b, U, Ud, val, F, st);
 }
 
 static iga_status form_group(int n, const iga_space *spaces, const iga_phys *phys, double a, double b,
@@ -871,6 +872,25 @@ iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx
     cudaGetDevice(&prev);
     cudaSetDevice(s->device);
     iga_status st = gmres_solve(s, row_ptr, col_idx, val, b, x, opt, iters, relres, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
+iga_status iga_alpha_step(iga_space s, const iga_phys *phys, const iga_alpha *opt, const int64_t *row_ptr,
+                          const int32_t *col_idx, double *val, double *U, double *Udot, iga_step_stats *stats,
+                          void *stream) {
+    iga_status st = check_phys(s, phys);
+    if (st != IGA_OK) return st;
+    if (!opt || !row_ptr || !col_idx || !val || !U || !Udot) { set_error("null argument"); return IGA_ERR_PARAM; }
+    if (opt->newton_its < 1 || opt->newton_its > 8 || !(opt->dt > 0.0) || !(opt->rho_inf >= 0.0 && opt->rho_inf <= 1.0) ||
+        opt->krylov.precond < 0 || opt->krylov.precond > 2 || opt->krylov.restart < 1 || opt->krylov.maxit < 0) {
+        set_error("alpha_step: bad options");
+        return IGA_ERR_PARAM;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->device);
+    st = alpha_step(s, phys, opt, row_ptr, col_idx, val, U, Udot, stats, (cudaStream_t)stream);
     cudaSetDevice(prev);
     return st;
 }
