@@ -35,9 +35,11 @@ DEFAULT_CONFIG = 2          # BASELINE.json configs[1]
 # Algorithmic model:
 #   F_J  = min over rank / test-side sum-factorised / sum-factorised contraction flops per qpt
 #   F_R  = residual rank-form flops per qpt;  B = CSR values written once + vectors, bytes per qpt
-F_J = {1: 72.0, 2: 672.0, 3: 738.0, 4: 9477.0, 5: 40986.0}
-F_R = {1: 108.0, 2: 192.0, 3: 198.0, 4: 972.0, 5: 2376.0}
-B_QP = {1: 25.6, 2: 25.8, 3: 24.9, 4: 348.0, 5: 596.0}
+F_J = {1: 72.0, 2: 672.0, 3: 738.0, 4: 9477.0, 5: 40986.0, 7: 324.0}
+F_R = {1: 108.0, 2: 192.0, 3: 198.0, 4: 972.0, 5: 2376.0, 7: 108.0}
+B_QP = {1: 25.6, 2: 25.8, 3: 24.9, 4: 348.0, 5: 596.0, 7: 25.6}
+# config 7 (the Alg. 2 ring, not a BASELINE config): 2D p = 2 NURBS Laplace + mass, R' = 3, nnzD' = 9,
+# symmetric: tsf = sf = 324 flop/qpt (Appendix B with n1 = q1 = 3, C_tsf = 54, C_sf = 324)
 # FP64 peak from unit counts and clock: 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
 P64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 

@@ -68,6 +68,11 @@ typedef struct {
     int geometry;                  /* iga_geom: PARAMETRIC => x = xi (knots carry coordinates)  */
     const double *ctrl;            /* host [n0][n1][n2][dim] Euclidean control points (NURBS)  */
     const double *weights;         /* host [n0][n1][n2] projective weights > 0, NULL => 1      */
+    /* ctrl / weights live on the OPEN function grid, n_d = n_knots[d] - degree[d] - 1.  On a
+     * periodic axis they are the clamped net of a C^k-periodic geometry: the library unclamps
+     * every line with Alg. 2 in homogeneous coordinates (w x, w) and keeps the
+     * n_d - (k+1) unique points; if the last k+1 unclamped points of a line do not repeat its
+     * first k+1 (within 1e-10 relative) the geometry is not periodic: IGA_ERR_DOMAIN. */
 } iga_space_desc;
 
 /* Box decomposition of the element grid over ranks ("partitioning of the

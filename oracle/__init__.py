@@ -67,6 +67,7 @@ def lib():
         L.orc_coxdeboor_deriv.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_int]
         L.orc_gauss_legendre.argtypes = [C.c_int, dp, dp]
         L.orc_unclamp_knots.argtypes = [C.c_int, C.c_int, C.c_int, dp]
+        L.orc_unclamp_curve.argtypes = [C.c_int, C.c_int, C.c_int, dp, dp, C.c_int, C.c_long]
         L.orc_basis_stencil.argtypes = [C.c_int, C.c_int, dp, C.c_int, ip, ip]
     return _lib
 
@@ -106,6 +107,15 @@ def unclamp_knots(n: int, p: int, k: int, U):
     U = np.array(U, dtype=np.float64)
     lib().orc_unclamp_knots(n, p, k, _d(U))
     return U
+
+
+def unclamp_curve(n: int, p: int, k: int, U, Pw):
+    """Alg. 2 on a copy: returns (U', Pw') for n+1 homogeneous points Pw[n+1][h]."""
+    U = np.array(U, dtype=np.float64)
+    Pw = np.array(Pw, dtype=np.float64)
+    h = Pw.shape[1]
+    lib().orc_unclamp_curve(n, p, k, _d(U), _d(Pw), h, h)
+    return U, Pw
 
 
 def basis_stencil(i: int, p: int, U):

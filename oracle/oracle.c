@@ -11,6 +11,8 @@
  * /root/reference/PAPER.md ("P:line", section / equation / algorithm) it follows;
  * where the paper is silent the SURVEY.md §8(c) reading (A-n) is cited and repeated
  * in DESIGN.md.  There is no blocking, fusion or reordering beyond the definitions:
+ *   - periodic spaces: Alg. 1 on the knots; geometry on a periodic axis is
+ *     given as a clamped net and unclamped with Alg. 2,
  *   - univariate basis: the literal Cox-de Boor recursion of P:184-190 (not the
  *     triangular in-span scheme), derivatives by the textbook recursion (A5),
  *   - tensor product P:196-203, rational basis eqs. (rational),(drational),(ddrational)
@@ -52,6 +54,34 @@ void orc_unclamp_knots(int n, int p, int k, double *U)
         U[k - i] = U[p] - U[n + 1] + U[n - i];
         U[m - k + i] = U[n + 1] - U[p] + U[p + i + 1];
     }
+}
+
+/* ------------------------------------------------------------------------------------ */
+/* Alg. 2 ("UnclampCurve"): unclamp the knot vector U and the n+1 homogeneous  */
+/* control points of a curve for C^k periodicity, in place, in the paper's loop order.   */
+/* Point j is Pw[j*stride .. j*stride+h-1] (h = dim+1 homogeneous coordinates).  The     */
+/* pseudocode's stray '}' after the first double loop is a garble; the structure is two  */
+/* (knots, points) passes, left end then right end (the NURBS book's A12.1 shape).        */
+/* ------------------------------------------------------------------------------------ */
+void orc_unclamp_curve(int n, int p, int k, double *U, double *Pw, int h, long stride)
+{
+    int m = n + p + 1;
+    for (int i = 0; i <= k; i++) /* unclamp at left end */
+        U[k - i] = U[p] - U[n + 1] + U[n - i];
+    for (int i = p - k - 1; i <= p - 2; i++)
+        for (int j = i; j >= 0; j--) {
+            double alpha = (U[p] - U[p + j - i - 1]) / (U[p + j + 1] - U[p + j - i - 1]);
+            for (int c = 0; c < h; c++)
+                Pw[j * stride + c] = (Pw[j * stride + c] - alpha * Pw[(j + 1) * stride + c]) / (1.0 - alpha);
+        }
+    for (int i = 0; i <= k; i++) /* unclamp at right end */
+        U[m - k + i] = U[n + 1] - U[p] + U[p + i + 1];
+    for (int i = p - k - 1; i <= p - 2; i++)
+        for (int j = i; j >= 0; j--) {
+            double alpha = (U[n + 1] - U[n - j]) / (U[n - j + i + 2] - U[n - j]);
+            for (int c = 0; c < h; c++)
+                Pw[(n - j) * stride + c] = (Pw[(n - j) * stride + c] - (1.0 - alpha) * Pw[(n - j - 1) * stride + c]) / alpha;
+        }
 }
 
 /* ------------------------------------------------------------------------------------ */
@@ -249,14 +279,60 @@ orc_space *orc_space_new(int dim, const int *p, const int *nk, const double *kno
         s->colcnt[d] = (int *)calloc(1, sizeof(int)); s->colcnt[d][0] = 1;
         s->cols[d] = (int *)calloc(1, sizeof(int)); s->colmax[d] = 1;
     }
-    if (geom == ORC_NURBS) {
-        if (!ctrl) { orc_space_free(s); return NULL; }
-        s->ctrl = (double *)malloc(sizeof(double) * s->nnodes * dim);
-        memcpy(s->ctrl, ctrl, sizeof(double) * s->nnodes * dim);
-    }
-    if (wts) {
-        s->wts = (double *)malloc(sizeof(double) * s->nnodes);
-        memcpy(s->wts, wts, sizeof(double) * s->nnodes);
+    if (geom == ORC_NURBS && !ctrl) { orc_space_free(s); return NULL; }
+    if (ctrl || wts) {
+        /* geometry data is given on the OPEN function grid (nfun per axis).  On periodic axes the
+         * clamped net is unclamped with Alg. 2 in homogeneous coordinates (w x, w), line by line,
+         * and the last k+1 points -- the wrapped copies of the first k+1 on a C^k-periodic
+         * geometry -- must coincide with them (else the description is invalid); the unique
+         * nu points are kept. */
+        int h = dim + 1;
+        long nopen = 1;
+        for (int d = 0; d < dim; d++) nopen *= s->nfun[d];
+        double *Pw = (double *)malloc(sizeof(double) * nopen * h);
+        for (long q = 0; q < nopen; q++) {
+            double wq = wts ? wts[q] : 1.0;
+            for (int c = 0; c < dim; c++) Pw[q * h + c] = (ctrl ? ctrl[q * dim + c] : 0.0) * wq;
+            Pw[q * h + dim] = wq;
+        }
+        long str[ORC_MAXD];
+        long acc = h;
+        for (int d = dim - 1; d >= 0; d--) { str[d] = acc; acc *= s->nfun[d]; }
+        int bad = 0;
+        const double *kq = knots;
+        for (int d = 0; d < dim; d++) {
+            if (s->periodic[d]) {
+                int nf = s->nfun[d], k = s->cont[d];
+                double *Uc = (double *)malloc(sizeof(double) * nk[d]);
+                for (long q = 0; q < nopen; q++) {
+                    long coord = (q / (str[d] / h)) % nf;
+                    if (coord != 0) continue;             /* one line per base point */
+                    memcpy(Uc, kq, sizeof(double) * nk[d]);
+                    orc_unclamp_curve(nf - 1, p[d], k, Uc, Pw + q * h, h, str[d]);
+                    for (int g = 0; g <= k; g++)
+                        for (int c = 0; c < h; c++) {
+                            double a0 = Pw[q * h + g * str[d] + c], a1 = Pw[q * h + (s->nu[d] + g) * str[d] + c];
+                            if (fabs(a0 - a1) > 1e-10 * (1.0 + fabs(a0))) bad = 1;
+                        }
+                }
+                free(Uc);
+            }
+            kq += nk[d];
+        }
+        if (bad) { free(Pw); orc_space_free(s); return NULL; }
+        if (ctrl) s->ctrl = (double *)malloc(sizeof(double) * s->nnodes * dim);
+        if (wts) s->wts = (double *)malloc(sizeof(double) * s->nnodes);
+        for (long u = 0; u < s->nnodes; u++) {
+            /* unique node u (C order over nu) -> open-grid index */
+            long rem = u, q = 0;
+            long ui[ORC_MAXD];
+            for (int d = dim - 1; d >= 0; d--) { ui[d] = rem % s->nu[d]; rem /= s->nu[d]; }
+            for (int d = 0; d < dim; d++) q = q * s->nfun[d] + ui[d];
+            double wq = Pw[q * h + dim];
+            if (ctrl) for (int c = 0; c < dim; c++) s->ctrl[u * dim + c] = Pw[q * h + c] / wq;
+            if (wts) s->wts[u] = wq;
+        }
+        free(Pw);
     }
     return s;
 }

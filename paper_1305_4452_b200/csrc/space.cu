@@ -282,6 +282,79 @@ static void free_space(iga_space_s *s) {
 
 
 // ------------------------------------------------------------------------------------------
+// Alg. 2 ("UnclampCurve"): unclamp one line of n+1 homogeneous control points (h
+// doubles each, `st` doubles apart) for C^k periodicity, given a copy of the axis' OPEN knots;
+// left end (knots, then points), right end likewise.  Then geometry_unique() applies it to every
+// line of every periodic axis of the open control net, requires the last k+1 points of each line
+// to repeat its first k+1 (the periodic identification) and keeps the nu unique ones.
+// ------------------------------------------------------------------------------------------
+static void unclamp_line(std::vector<double> U, int p, int k, double *P, int h, long long st) {
+    const int n = (int)U.size() - p - 2, m = n + p + 1;
+    for (int i = 0; i <= k; i++) U[k - i] = U[p] - U[n + 1] + U[n - i];
+    for (int i = p - k - 1; i <= p - 2; i++)
+        for (int j = i; j >= 0; j--) {
+            const double al = (U[p] - U[p + j - i - 1]) / (U[p + j + 1] - U[p + j - i - 1]);
+            double *a = P + j * st, *b = P + (j + 1) * st;
+            for (int c = 0; c < h; c++) a[c] = (a[c] - al * b[c]) / (1.0 - al);
+        }
+    for (int i = 0; i <= k; i++) U[m - k + i] = U[n + 1] - U[p] + U[p + i + 1];
+    for (int i = p - k - 1; i <= p - 2; i++)
+        for (int j = i; j >= 0; j--) {
+            const double al = (U[n + 1] - U[n - j]) / (U[n - j + i + 2] - U[n - j]);
+            double *a = P + (n - j) * st, *b = P + (n - j - 1) * st;
+            for (int c = 0; c < h; c++) a[c] = (a[c] - (1.0 - al) * b[c]) / al;
+        }
+}
+
+static iga_status geometry_unique(const iga_space_desc *d, const int *nfun, const int *nu, std::vector<double> &ctrl,
+                                  std::vector<double> &wts) {
+    const int dim = d->dim, h = dim + 1;
+    long long nopen = 1, nuniq = 1;
+    for (int a = 0; a < dim; a++) { nopen *= nfun[a]; nuniq *= nu[a]; }
+    std::vector<double> P((size_t)nopen * h);
+    for (long long q = 0; q < nopen; q++) {
+        const double w = d->weights ? d->weights[q] : 1.0;
+        if (!(w > 0.0)) { set_error("weights must be > 0"); return IGA_ERR_DOMAIN; }
+        for (int c = 0; c < dim; c++) P[q * h + c] = (d->ctrl ? d->ctrl[q * dim + c] : 0.0) * w;
+        P[q * h + dim] = w;
+    }
+    long long pstride[3] = {1, 1, 1};          // point stride per axis on the open grid
+    for (int a = dim - 2; a >= 0; a--) pstride[a] = pstride[a + 1] * nfun[a + 1];
+    for (int a = 0; a < dim; a++) {
+        if (!d->periodic[a]) continue;
+        const int p = d->degree[a], k = d->periodic_continuity[a];
+        const std::vector<double> U0(d->knots[a], d->knots[a] + d->n_knots[a]);
+        for (long long q = 0; q < nopen; q++) {
+            if ((q / pstride[a]) % nfun[a] != 0) continue;       // one line per base point
+            double *line = P.data() + q * h;
+            unclamp_line(U0, p, k, line, h, pstride[a] * h);
+            for (int g = 0; g <= k; g++)
+                for (int c = 0; c < h; c++) {
+                    const double x0 = line[g * pstride[a] * h + c], x1 = line[(nu[a] + g) * pstride[a] * h + c];
+                    if (std::fabs(x0 - x1) > 1e-10 * (1.0 + std::fabs(x0))) {
+                        set_error("geometry on a periodic axis is not C^k periodic: Alg. 2 leaves its wrapped "
+                                  "control points distinct");
+                        return IGA_ERR_DOMAIN;
+                    }
+                }
+        }
+    }
+    ctrl.assign(d->ctrl ? (size_t)nuniq * dim : 0, 0.0);
+    wts.assign(d->weights ? (size_t)nuniq : 0, 0.0);
+    for (long long u = 0; u < nuniq; u++) {
+        long long rem = u, q = 0;
+        int ui[3] = {0, 0, 0};
+        for (int a = dim - 1; a >= 0; a--) { ui[a] = (int)(rem % nu[a]); rem /= nu[a]; }
+        for (int a = 0; a < dim; a++) q = q * nfun[a] + ui[a];
+        const double w = P[q * h + dim];
+        if (d->ctrl)
+            for (int c = 0; c < dim; c++) ctrl[u * dim + c] = P[q * h + c] / w;
+        if (d->weights) wts[u] = w;
+    }
+    return IGA_OK;
+}
+
+// ------------------------------------------------------------------------------------------
 // per-axis host setup (no CUDA): knots (Alg. 1 unclamping), elements, Gauss rule, Alg. 3
 // stencils, supports, and the box decomposition of the axis over P rank coordinates
 // (b_r = floor(N r / P)) with DOF ownership A-9 (owner of a function = owner of the
@@ -303,7 +376,6 @@ iga_status axis_host(const iga_space_desc *d, int a, int P, AxisHost &H) {
     if (H.periodic) {
         const int k = d->periodic_continuity[a];
         if (k < 0 || k > p - 1) { set_error("periodic continuity must be in [0, p-1]"); return IGA_ERR_DOMAIN; }
-        if (d->geometry == IGA_GEOM_NURBS) { set_error("periodic NURBS geometry (Alg. 2) not supported"); return IGA_ERR_PARAM; }
         unclamp(U, p, k);
         nu = nfun - (k + 1);
     }
@@ -617,15 +689,13 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
             s->nel_local *= (s->el_hi[a] - s->el_lo[a]);
             s->nqp_local *= (long long)(s->el_hi[a] - s->el_lo[a]) * s->nq[a];
         }
-        if (d->geometry == IGA_GEOM_NURBS) {
-            std::vector<double> c(d->ctrl, d->ctrl + nnodes * d->dim);
-            if ((st = upload(s, (double **)&s->dev.ctrl, c)) != IGA_OK) goto fail;
-        }
-        if (d->weights) {
-            std::vector<double> w(d->weights, d->weights + nnodes);
-            for (double v : w)
-                if (!(v > 0.0)) { st = IGA_ERR_DOMAIN; set_error("weights must be > 0"); goto fail; }
-            if ((st = upload(s, (double **)&s->dev.wts, w)) != IGA_OK) goto fail;
+        if (d->geometry == IGA_GEOM_NURBS || d->weights) {
+            // control net / weights: given on the OPEN function grid; periodic axes unclamped
+            // with Alg. 2 and reduced to the unique functions
+            std::vector<double> c, w;
+            if ((st = geometry_unique(d, s->nfun, s->nu, c, w)) != IGA_OK) goto fail;
+            if (d->geometry == IGA_GEOM_NURBS && (st = upload(s, (double **)&s->dev.ctrl, c)) != IGA_OK) goto fail;
+            if (d->weights && (st = upload(s, (double **)&s->dev.wts, w)) != IGA_OK) goto fail;
         }
         if ((st = dalloc(s, &s->errflag, 1)) != IGA_OK) goto fail;
         CUDA_TRY(cudaMemset(s->errflag, 0, sizeof(int)));

@@ -16,7 +16,7 @@ iga = pytest.importorskip("paper_1305_4452_b200")
 
 LAYOUTS = [
     (1, 16, [2, 1]), (1, 16, [2, 2]), (2, 12, [3, 2]), (3, 12, [2, 2]), (3, 12, [4, 1]),
-    (4, 6, [2, 2, 1]), (4, 6, [2, 2, 2]), (5, 8, [2, 2, 2]), (5, 9, [1, 3, 2]),
+    (4, 6, [2, 2, 1]), (4, 6, [2, 2, 2]), (5, 8, [2, 2, 2]), (5, 9, [1, 3, 2]), (7, 12, [2, 2]),
 ]
 
 

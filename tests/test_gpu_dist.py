@@ -38,6 +38,7 @@ def _owned_rows(w, sp):
 LAYOUTS = [
     (1, 16, [2, 2]), (2, 12, [2, 3]), (3, 12, [2, 1]), (3, 16, [2, 2]), (3, 33, [3, 2]),
     (4, 6, [2, 2, 1]), (4, 5, [1, 2, 2]), (5, 8, [2, 2, 2]), (5, 7, [2, 1, 3]), (6, 8, [2, 2]),
+    (7, 12, [2, 2]), (7, 10, [1, 3]),
 ]
 
 

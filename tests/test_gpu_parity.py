@@ -40,7 +40,8 @@ def _gpu_assemble(iga, w, a=None, b=None, params=None, Udot=None, want_F=True, s
         Fr.cpu().numpy()
 
 
-SMALL = [(1, 16), (1, 5), (2, 3), (2, 16), (3, 5), (3, 12), (4, 2), (4, 5), (5, 5), (5, 7), (6, 5), (6, 9)]
+SMALL = [(1, 16), (1, 5), (2, 3), (2, 16), (3, 5), (3, 12), (4, 2), (4, 5), (5, 5), (5, 7), (6, 5), (6, 9),
+         (7, 5), (7, 9), (7, 20)]
 
 
 SMALL_2D_TILES = [(1, 17), (2, 9), (2, 21), (3, 16), (3, 33), (3, 40)]   # several tiles + ragged tails
@@ -93,7 +94,7 @@ def test_term_groups(cid, n, groups):
         assert vec_rel_err(Fo, F) <= ROW_TOL
 
 
-@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5, 6, 7])
 def test_full_size_probe_rows(cid):
     """BASELINE full sizes, the launch bench.py times: complete probe rows vs the oracle's
     row-subset assembly (SURVEY O-10), pattern of those rows bit-exact, row lengths of ALL rows.
@@ -138,7 +139,7 @@ def test_full_size_probe_rows(cid):
     assert bool(torch.isfinite(vals_d).all())
 
 
-@pytest.mark.parametrize("cid", [1, 2, 3])
+@pytest.mark.parametrize("cid", [1, 2, 3, 7])
 def test_full_size_full_pattern(cid):
     iga = _gpu()
     w = workloads.make(cid)
@@ -205,6 +206,12 @@ def test_bad_arguments_rejected():
     bad.knots[0] = bad.knots[0][::-1].copy()   # decreasing knots
     with pytest.raises(iga.IgaError) as ei:
         iga.Space.from_workload(bad)
+    assert ei.value.code == 2
+    ring = workloads.make(7, n=6)
+    ring.ctrl = ring.ctrl.copy()
+    ring.ctrl[:, 0, 1] += 0.01                 # clamped net no longer C^1 periodic (Alg. 2 check)
+    with pytest.raises(iga.IgaError) as ei:
+        iga.Space.from_workload(ring)
     assert ei.value.code == 2
     sp = iga.Space.from_workload(w)
     U = torch.zeros(sp.ndof, dtype=torch.float64, device="cuda")

@@ -37,9 +37,10 @@ PHYS_LAPLACE, PHYS_CAHN_HILLIARD, PHYS_NEOHOOKE, PHYS_NS_VMS, PHYS_NSK = 0, 1, 2
 GEOM_PARAMETRIC, GEOM_NURBS = 0, 1
 
 # full-size element counts per axis (BASELINE.json configs[0..4])
-FULL_N = {1: 16, 2: 256, 3: 1024, 4: 64, 5: 128, 6: 256}
+FULL_N = {1: 16, 2: 256, 3: 1024, 4: 64, 5: 128, 6: 256, 7: 256}
 NAMES = {1: "poisson2d_p2_16x16", 2: "annulus_lapmass_p3_256x256", 3: "cahn_hilliard2d_p2_1024x1024",
-         4: "neohooke3d_p2_64x64x64", 5: "ns_vms3d_p2_128x128x128", 6: "nsk2d_p2_256x256"}
+         4: "neohooke3d_p2_64x64x64", 5: "ns_vms3d_p2_128x128x128", 6: "nsk2d_p2_256x256",
+         7: "ring_alg2_lapmass_p2_256x256"}
 
 
 @dataclass
@@ -132,7 +133,7 @@ def annulus_geometry(U0: np.ndarray, U1: np.ndarray, p: int = 3):
 def make(cid: int, n=None, seed: int | None = None) -> Workload:
     """Build config `cid` (1..5) with n elements per axis (default: the full BASELINE size); n may
     be a list with one count per axis (weak-scaling meshes of bench.py --gpus N)."""
-    dims = {1: 2, 2: 2, 3: 2, 4: 3, 5: 3, 6: 2}[cid] if cid in (1, 2, 3, 4, 5, 6) else 0
+    dims = {1: 2, 2: 2, 3: 2, 4: 3, 5: 3, 6: 2, 7: 2}[cid] if cid in FULL_N else 0
     if n is None:
         n = FULL_N[cid]
     nn = list(n) if isinstance(n, (list, tuple)) else [int(n)] * dims
@@ -239,6 +240,36 @@ def _make(cid: int, nn: list, seed: int | None = None) -> Workload:
         w = Workload(6, NAMES[6], d, [p] * d, U, [1] * d, [p - 1] * d, 3, [p + 1] * d, GEOM_PARAMETRIC,
                      None, None, PHYS_NSK, [3.0, 1.0, 8.0 / 27.0, 0.85, mub, -2.0 / 3.0 * mub, 1.0 / 512.0 ** 2],
                      5.0 / 6.0, (4.0 / 9.0) * dt, Uarr, Udot, list(nn), list(nn))
+    elif cid == 7:
+        # Periodic mapped geometry (Alg. 2): a ring, axis 0 radial (open p = 2,
+        # r = 1 + Greville abscissa in [1, 2]), axis 1 angular, periodic C^1 quadratic.  Unique
+        # homogeneous points Q_g = w_g (r cos t_g, r sin t_g, 1), t_g = 2 pi g / nu, w_g ~ U[0.8, 1.2]
+        # seed 7 (a smooth rational closed curve near the circle); the caller hands the CLAMPED net
+        # of that periodic curve: P_j = Q_j (1 <= j <= n-2), P_{n-1} = Q_0 and P_0 = P_n =
+        # (Q_0 + Q_1)/2 -- the C^1 seam condition of uniform clamped quadratics, homogeneous.  Both
+        # sides unclamp it with Alg. 2.  LAPLACE kappa = sigma = 1, f = 0, U ~ U[-1, 1]; (a, b) = (0, 1).
+        p, d = 2, 2
+        U = [open_uniform_knots(p, nn[a]) for a in range(d)]
+        r = 1.0 + _greville(U[0], p)
+        nf0, nopen1 = len(r), nn[1] + p
+        nu1 = nopen1 - 2
+        t = 2.0 * math.pi * np.arange(nu1) / nu1
+        wq = rng.uniform(0.8, 1.2, nu1)
+        Q = np.zeros((nf0, nu1, 3))
+        Q[:, :, 0] = r[:, None] * np.cos(t)[None, :] * wq[None, :]
+        Q[:, :, 1] = r[:, None] * np.sin(t)[None, :] * wq[None, :]
+        Q[:, :, 2] = wq[None, :]
+        n = nopen1 - 1
+        Pw = np.zeros((nf0, nopen1, 3))
+        Pw[:, 1:n - 1] = Q[:, 1:n - 1]
+        Pw[:, n - 1] = Q[:, 0]
+        Pw[:, 0] = Pw[:, n] = 0.5 * (Q[:, 0] + Q[:, 1])
+        ctrl = Pw[:, :, :2] / Pw[:, :, 2:]
+        weights = Pw[:, :, 2].copy()
+        nd = nf0 * nu1
+        w = Workload(7, NAMES[7], d, [p] * d, U, [0, 1], [p - 1] * d, 1, [p + 1] * d, GEOM_NURBS,
+                     ctrl, weights, PHYS_LAPLACE, [1.0, 1.0, 0.0], 0.0, 1.0,
+                     rng.uniform(-1.0, 1.0, nd), np.zeros(nd), list(nn), [nf0, nu1])
     else:
         raise ValueError(f"unknown config {cid}")
     return w
