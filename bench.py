@@ -35,11 +35,13 @@ DEFAULT_CONFIG = 2          # BASELINE.json configs[1]
 # Algorithmic model:
 #   F_J  = min over rank / test-side sum-factorised / sum-factorised contraction flops per qpt
 #   F_R  = residual rank-form flops per qpt;  B = CSR values written once + vectors, bytes per qpt
-F_J = {1: 72.0, 2: 672.0, 3: 738.0, 4: 9477.0, 5: 40986.0, 7: 324.0}
-F_R = {1: 108.0, 2: 192.0, 3: 198.0, 4: 972.0, 5: 2376.0, 7: 108.0}
-B_QP = {1: 25.6, 2: 25.8, 3: 24.9, 4: 348.0, 5: 596.0, 7: 25.6}
+F_J = {1: 72.0, 2: 672.0, 3: 738.0, 4: 9477.0, 5: 40986.0, 7: 324.0, 8: 4428.0}
+F_R = {1: 108.0, 2: 192.0, 3: 198.0, 4: 972.0, 5: 2376.0, 7: 108.0, 8: 702.0}
+B_QP = {1: 25.6, 2: 25.8, 3: 24.9, 4: 348.0, 5: 596.0, 7: 25.6, 8: 37.5}
 # config 7 (the Alg. 2 ring, not a BASELINE config): 2D p = 2 NURBS Laplace + mass, R' = 3, nnzD' = 9,
-# symmetric: tsf = sf = 324 flop/qpt (Appendix B with n1 = q1 = 3, C_tsf = 54, C_sf = 324)
+# symmetric: tsf = sf = 324 flop/qpt (Appendix B with n1 = q1 = 3, C_tsf = 54, C_sf = 324).
+# config 8 (3D CH, §8(f) rank 3): ESTIMATE -- Appendix B's tsf with n1 = q1 = 3, C_tsf = 243,
+# R' = 7 separable test kinds and nnzD' = 19 (config 3's 11 extended to d = 3; T = 1 + 3d + 2d^2)
 # FP64 peak from unit counts and clock: 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
 P64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
@@ -627,7 +629,7 @@ def main():
     ws, rank, local = dist_env()
     n = args.n
     if ws > 1 and args.scaling == "weak":
-        dim = 2 if args.config <= 3 else 3
+        dim = workloads.make(args.config, n=6).dim
         base = n if n is not None else workloads.FULL_N[args.config]
         n = [base * f for f in box_procs(ws, dim)]
     w = workloads.make(args.config, n=n)

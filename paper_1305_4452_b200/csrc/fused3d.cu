@@ -1,4 +1,4 @@
-// fused3d.cu -- K3/K4 for 3D parametric spaces (configs 4, 5): one fused kernel per call.
+// fused3d.cu -- K3/K4 for 3D parametric spaces (configs 4, 5, 8): one fused kernel per call.
 //
 // Persistent CTAs (two per SM, so that one CTA's latency-bound point phase overlaps the other's
 // FP64-bound contraction) walk the element grid; per element a CTA runs Alg. 4 in
@@ -49,8 +49,9 @@ struct F3 {
     static constexpr int STD = (sizeof(State) + 7) / 8;      // doubles per state
     // symmetric element Jacobian (hyperelastic tangent, major symmetry): contract blocks I <= J
     static constexpr bool SYMJ = std::is_same<PH, PhysNeoHooke>::value;
-    // resident CTAs per SM the register budget is sized for (m = 3: 96 threads -> 3 CTAs)
-    static constexpr int MINB = M == 3 ? 3 : 2;
+    // resident CTAs per SM the register budget is sized for (m = 3: 96 threads -> 3 CTAs; m = 1:
+    // one-warp CTAs (27 trial functions), 8 per SM)
+    static constexpr int MINB = M == 1 ? 8 : M == 3 ? 3 : 2;
     // shared-memory carve-up (in doubles)
     static constexpr int O_U = 0;                            // [NEN][M]
     static constexpr int O_UD = O_U + NEN * M;               // [NEN][M]
@@ -693,6 +694,9 @@ iga_status launch_fused3d(iga_space_s *s, const iga_phys *ph, double a, double b
     if (ph->kind == IGA_PHYS_NEOHOOKE && s->dof == 3)
         return uni ? run_fused3d<2, PhysNeoHooke, true>(s, ph, a, b, U, Ud, val, F, st, nsm)
                    : run_fused3d<2, PhysNeoHooke, false>(s, ph, a, b, U, Ud, val, F, st, nsm);
+    if (ph->kind == IGA_PHYS_CAHN_HILLIARD && s->dof == 1)      // 3D CH
+        return uni ? run_fused3d<2, PhysCahnHilliard, true>(s, ph, a, b, U, Ud, val, F, st, nsm)
+                   : run_fused3d<2, PhysCahnHilliard, false>(s, ph, a, b, U, Ud, val, F, st, nsm);
     return IGA_ERR_STATE;
 }
 

@@ -31,7 +31,7 @@ def _dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(torch.device("cuda", 0))
 
 
-@pytest.mark.parametrize("cid,n,steps,newton", [(3, 12, 2, 2), (3, 20, 1, 3), (6, 6, 2, 2)])
+@pytest.mark.parametrize("cid,n,steps,newton", [(3, 12, 2, 2), (3, 20, 1, 3), (6, 6, 2, 2), (8, 5, 1, 2)])
 def test_alpha_steps_match_oracle(cid, n, steps, newton):
     iga = _gpu()
     w = workloads.make(cid, n=n)

@@ -37,10 +37,10 @@ PHYS_LAPLACE, PHYS_CAHN_HILLIARD, PHYS_NEOHOOKE, PHYS_NS_VMS, PHYS_NSK = 0, 1, 2
 GEOM_PARAMETRIC, GEOM_NURBS = 0, 1
 
 # full-size element counts per axis (BASELINE.json configs[0..4])
-FULL_N = {1: 16, 2: 256, 3: 1024, 4: 64, 5: 128, 6: 256, 7: 256}
+FULL_N = {1: 16, 2: 256, 3: 1024, 4: 64, 5: 128, 6: 256, 7: 256, 8: 256}
 NAMES = {1: "poisson2d_p2_16x16", 2: "annulus_lapmass_p3_256x256", 3: "cahn_hilliard2d_p2_1024x1024",
          4: "neohooke3d_p2_64x64x64", 5: "ns_vms3d_p2_128x128x128", 6: "nsk2d_p2_256x256",
-         7: "ring_alg2_lapmass_p2_256x256"}
+         7: "ring_alg2_lapmass_p2_256x256", 8: "cahn_hilliard3d_p2_256x256x256"}
 
 
 @dataclass
@@ -133,7 +133,7 @@ def annulus_geometry(U0: np.ndarray, U1: np.ndarray, p: int = 3):
 def make(cid: int, n=None, seed: int | None = None) -> Workload:
     """Build config `cid` (1..5) with n elements per axis (default: the full BASELINE size); n may
     be a list with one count per axis (weak-scaling meshes of bench.py --gpus N)."""
-    dims = {1: 2, 2: 2, 3: 2, 4: 3, 5: 3, 6: 2, 7: 2}[cid] if cid in FULL_N else 0
+    dims = {1: 2, 2: 2, 3: 2, 4: 3, 5: 3, 6: 2, 7: 2, 8: 3}[cid] if cid in FULL_N else 0
     if n is None:
         n = FULL_N[cid]
     nn = list(n) if isinstance(n, (list, tuple)) else [int(n)] * dims
@@ -270,6 +270,19 @@ def _make(cid: int, nn: list, seed: int | None = None) -> Workload:
         w = Workload(7, NAMES[7], d, [p] * d, U, [0, 1], [p - 1] * d, 1, [p + 1] * d, GEOM_NURBS,
                      ctrl, weights, PHYS_LAPLACE, [1.0, 1.0, 0.0], 0.0, 1.0,
                      rng.uniform(-1.0, 1.0, nd), np.zeros(nd), list(nn), [nf0, nu1])
+    elif cid == 8:
+        # 3D Cahn-Hilliard (the Fig. 5 run): [0,1]^3 periodic C^1
+        # quadratic, 256^3 elements, random initial condition as in config 3 (c = 0.63 +
+        # U[-0.05, 0.05], seed 8), cdot = 0, theta = 1.5, alpha = 3000, rho_inf = 0.5, dt = 1e-6.
+        p, d = 2, 3
+        U = [open_uniform_knots(p, nn[a]) for a in range(d)]
+        nf = [nn[0], nn[1], nn[2]]
+        nd = nf[0] * nf[1] * nf[2]
+        c = 0.63 + rng.uniform(-0.05, 0.05, nd)
+        dt = 1e-6
+        w = Workload(8, NAMES[8], d, [p] * d, U, [1] * d, [p - 1] * d, 1, [p + 1] * d, GEOM_PARAMETRIC,
+                     None, None, PHYS_CAHN_HILLIARD, [1.5, 3000.0], 5.0 / 6.0, (4.0 / 9.0) * dt,
+                     c, np.zeros(nd), list(nn), nf)
     else:
         raise ValueError(f"unknown config {cid}")
     return w
