@@ -62,6 +62,7 @@ struct iga_space_s {
     // iga_gmres workspace (solver.cu): [0] Krylov vectors, [1] preconditioner; kept until destroy;
     // iga_alpha_step: [2] its stage vectors
     void *gm_buf[3] = {nullptr, nullptr, nullptr};
+    int gm_host_ctrl = 0;                // option "gmres_host": host-side Arnoldi control even at rtol = 0
     size_t gm_cap[3] = {0, 0, 0};
     // kernel timing hook (iga_profile_*)
     struct ProfRec { const char *name; cudaEvent_t a, b; };

@@ -10,6 +10,7 @@
 // over the CSR otherwise (the factor and the solves are sequential over a block's rows).  All vector work runs in the kernels below; the host only does the (m+1) x m
 // Hessenberg least-squares update.
 #include <cmath>
+#include <cstddef>
 #include <vector>
 
 #include "iga_host.h"
@@ -24,8 +25,9 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // out[k] += sum_i V[k][i] w[i] for k < nk (V rows of length ld); block partial sums + fp64 atomics
 __global__ void k_multidot(long long n, int nk, const double *__restrict__ V, long long ld, const double *__restrict__ w,
-                           double *__restrict__ out) {
+                           double *__restrict__ out, const int *__restrict__ gate = nullptr) {
     __shared__ double part[32][9];
+    if (gate && !*gate) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int k0 = 0; k0 < nk; k0 += 8) {
         const int kc = min(8, nk - k0);
@@ -53,7 +55,10 @@ __global__ void k_multidot(long long n, int nk, const double *__restrict__ V, lo
 
 // w = (w - sum_k V[k] h[k]) * scale
 __global__ void k_multiaxpy(long long n, int nk, const double *__restrict__ V, long long ld, const double *__restrict__ h,
-                            double *w, double scale) {
+                            double *w, double scale, const double *__restrict__ dscale = nullptr,
+                            const int *__restrict__ gate = nullptr) {
+    if (gate && !*gate) return;
+    if (dscale) scale = *dscale;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         double s = w[i];
         for (int k = 0; k < nk; k++) s -= h[k] * V[k * ld + i];
@@ -437,6 +442,93 @@ __global__ void k_jacobi(long long n, const int64_t *__restrict__ dp, const doub
         z[i] = r[i] / a[dp[i]];
 }
 
+// ---- device-driven Arnoldi control (fixed iteration budget, rtol = 0: the paper's protocol) ----
+// The decisions the host makes per iteration in the general path -- DGKS second pass, |h_{j+1}|,
+// the Givens update of the Hessenberg column -- are taken by one thread on the device, so a cycle
+// is a stream of launches with no host round trip.  Layout of the control block (doubles):
+// hbuf[m+2] (multi-dot target), hvec[m+1] (this pass's coefficients), H[(m+1) m], cs[m], sn[m],
+// g[m+1], yneg[m], then ArnCtl.
+struct ArnCtl {
+    double scale, res, beta;
+    int need2, jstop;
+};
+struct ArnLayout {
+    int m;
+    __host__ __device__ size_t hbuf() const { return 0; }
+    __host__ __device__ size_t hvec() const { return m + 2; }
+    __host__ __device__ size_t H() const { return 2 * m + 3; }
+    __host__ __device__ size_t cs() const { return H() + (size_t)(m + 1) * m; }
+    __host__ __device__ size_t sn() const { return cs() + m; }
+    __host__ __device__ size_t g() const { return sn() + m; }
+    __host__ __device__ size_t yneg() const { return g() + m + 1; }
+    __host__ __device__ size_t ctl() const { return (yneg() + m + 1) / 2 * 2; }
+    __host__ __device__ size_t total() const { return ctl() + 8; }
+};
+
+__global__ void k_arn_start(ArnLayout Lo, double *base) {
+    double *hb = base + Lo.hbuf(), *g = base + Lo.g();
+    ArnCtl *c = reinterpret_cast<ArnCtl *>(base + Lo.ctl());
+    const double beta = sqrt(fmax(hb[0], 0.0));
+    hb[0] = 0.0;
+    g[0] = beta;
+    for (int i = 1; i <= Lo.m; i++) g[i] = 0.0;
+    c->beta = beta;
+    c->scale = beta > 0.0 ? 1.0 / beta : 1.0;
+    c->res = beta;
+    c->jstop = Lo.m;
+    c->need2 = 1;
+}
+
+__global__ void k_arn_ctrl(ArnLayout Lo, double *base, int j, int pass) {
+    const int m = Lo.m;
+    double *hb = base + Lo.hbuf(), *hv = base + Lo.hvec(), *H = base + Lo.H(), *cs = base + Lo.cs(),
+           *sn = base + Lo.sn(), *g = base + Lo.g();
+    ArnCtl *c = reinterpret_cast<ArnCtl *>(base + Lo.ctl());
+    if (pass == 1 && !c->need2) return;
+    double hh = 0.0;
+    for (int i = 0; i <= j; i++) {
+        hv[i] = hb[i];
+        hh += hb[i] * hb[i];
+        H[(size_t)i * m + j] = (pass == 0 ? 0.0 : H[(size_t)i * m + j]) + hb[i];
+    }
+    const double ww = hb[j + 1], nrm2 = ww - hh;
+    for (int i = 0; i <= j + 1; i++) hb[i] = 0.0;
+    const bool last = pass == 1 || nrm2 > 0.5 * ww;
+    c->need2 = last ? 0 : 1;
+    c->scale = 1.0;
+    if (!last) return;
+    const double hj1 = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
+    if (hj1 > 0.0) c->scale = 1.0 / hj1;
+    for (int i = 0; i < j; i++) {
+        const double a0 = H[(size_t)i * m + j], a1 = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a0 + sn[i] * a1;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a0 + cs[i] * a1;
+    }
+    const double hjj = H[(size_t)j * m + j], den = hypot(hjj, hj1);
+    cs[j] = den > 0.0 ? hjj / den : 1.0;
+    sn[j] = den > 0.0 ? hj1 / den : 0.0;
+    H[(size_t)j * m + j] = den;
+    g[j + 1] = -sn[j] * g[j];
+    g[j] = cs[j] * g[j];
+    if (c->jstop == m || c->jstop > j) c->res = fabs(g[j + 1]);
+    if (hj1 == 0.0 && c->jstop > j + 1) c->jstop = j + 1;         // lucky breakdown: later columns unused
+}
+
+// y = R^{-1} g over the first min(jmax, jstop) columns; yneg = -y, zero beyond
+__global__ void k_arn_solve(ArnLayout Lo, double *base, int jmax) {
+    const int m = Lo.m;
+    const double *H = base + Lo.H(), *g = base + Lo.g();
+    double *yn = base + Lo.yneg();
+    const ArnCtl *c = reinterpret_cast<const ArnCtl *>(base + Lo.ctl());
+    const int j = min(jmax, c->jstop);
+    for (int i = jmax - 1; i >= j; i--) yn[i] = 0.0;
+    for (int i = j - 1; i >= 0; i--) {
+        double t = g[i];
+        for (int k = i + 1; k < j; k++) t += H[(size_t)i * m + k] * yn[k];     // yn = -y
+        yn[i] = -t / H[(size_t)i * m + i];
+    }
+}
+
 // device buffer `slot` of the space's solver workspace, grown to >= bytes (contents not kept)
 static void *ws_ensure(iga_space_s *s, int slot, size_t bytes) {
     if (s->gm_cap[slot] < bytes) {
@@ -461,7 +553,7 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
     auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t szV = al(sizeof(double) * (size_t)(m + 1) * n), szZ = al(sizeof(double) * (size_t)m * n),
                  szw = al(sizeof(double) * (size_t)n), szdp = al(sizeof(int64_t) * (size_t)n),
-                 szh = al(sizeof(double) * 2 * (size_t)(m + 1));
+                 szh = al(sizeof(double) * std::max<size_t>(2 * (size_t)(m + 1), ArnLayout{m}.total()));
     char *base = (char *)ensure(0, szV + szZ + szw + szdp + szh);
     if (!base) { set_error("gmres workspace"); return IGA_ERR_NOMEM; }
     double *V = (double *)base, *Z = (double *)(base + szV), *w = (double *)(base + szV + szZ);
@@ -545,6 +637,48 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
         return std::sqrt(h);
     };
     const double bnorm = norm2(b);
+    if (opt->rtol == 0.0 && !s->gm_host_ctrl) {
+        // fixed budget: device-driven cycles, one host synchronisation at the end
+        const ArnLayout Lo{m};
+        int *need2 = reinterpret_cast<int *>(reinterpret_cast<ArnCtl *>(dh + Lo.ctl())) + 6;   // ArnCtl::need2
+        const double *dscale = dh + Lo.ctl();                                                   // ArnCtl::scale
+        static_assert(offsetof(ArnCtl, need2) == 24 && offsetof(ArnCtl, scale) == 0, "ArnCtl layout");
+        cudaMemsetAsync(dh, 0, sizeof(double) * Lo.total(), st);
+        int it = 0;
+        while (it < maxit && bnorm > 0.0) {
+            spmv(x, V, b);
+            k_multidot<<<gv, 256, 0, st>>>(n, 1, V, n, V, dh);
+            k_arn_start<<<1, 1, 0, st>>>(Lo, dh);
+            k_multiaxpy<<<gv, 256, 0, st>>>(n, 0, V, n, dh, V, 1.0, dscale);
+            launches += 4;
+            const int jm = std::min(m, maxit - it);
+            for (int j = 0; j < jm; j++) {
+                double *vj1 = V + (size_t)(j + 1) * n;
+                precond(V + (size_t)j * n, Z + (size_t)j * n);
+                spmv(Z + (size_t)j * n, vj1, nullptr);
+                for (int pass = 0; pass < 2; pass++) {
+                    k_multidot<<<gv, 256, 0, st>>>(n, j + 2, V, n, vj1, dh, pass ? need2 : nullptr);
+                    k_arn_ctrl<<<1, 1, 0, st>>>(Lo, dh, j, pass);
+                    k_multiaxpy<<<gv, 256, 0, st>>>(n, j + 1, V, n, dh + Lo.hvec(), vj1, 1.0, dscale,
+                                                    pass ? need2 : nullptr);
+                }
+                launches += 7;
+            }
+            k_arn_solve<<<1, 1, 0, st>>>(Lo, dh, jm);
+            k_multiaxpy<<<gv, 256, 0, st>>>(n, jm, Z, n, dh + Lo.yneg(), x, 1.0);
+            launches += 2;
+            it += jm;
+        }
+        spmv(x, w, b);
+        launches++;
+        const double res = norm2(w);
+        s->last_launches = launches;
+        if (iters_out) *iters_out = it;
+        if (relres_out) *relres_out = res / (bnorm > 0.0 ? bnorm : 1.0);
+        ce = cudaGetLastError();
+        if (ce != cudaSuccess) { set_error(std::string("gmres: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+        return IGA_OK;
+    }
     const double target = opt->rtol * (bnorm > 0.0 ? bnorm : 1.0);
     std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), hcol(m + 1), y(m);
     int it = 0;

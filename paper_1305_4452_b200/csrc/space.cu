@@ -976,6 +976,7 @@ iga_status iga_space_set_option(iga_space s, const char *key, long long value) {
     if (std::strcmp(key, "general") == 0) { s->force_general = value != 0; return IGA_OK; }
     if (std::strcmp(key, "dbg") == 0) { s->dbg = (int)value; return IGA_OK; }
     if (std::strcmp(key, "bw") == 0) { s->bw_opt = (int)value; return IGA_OK; }
+    if (std::strcmp(key, "gmres_host") == 0) { s->gm_host_ctrl = value != 0; return IGA_OK; }
     set_error(std::string("unknown option ") + key);
     return IGA_ERR_PARAM;
 }
