@@ -494,7 +494,7 @@ __global__ void k_arn_ctrl(ArnLayout Lo, double *base, int j, int pass) {
     const double ww = hb[j + 1], nrm2 = ww - hh;
     for (int i = 0; i <= j + 1; i++) hb[i] = 0.0;
     const bool last = pass == 1 || nrm2 > 0.5 * ww;
-    c->need2 = last ? 0 : 1;
+    if (pass == 0) c->need2 = last ? 0 : 1;          // gates the second pass's three launches
     c->scale = 1.0;
     if (!last) return;
     const double hj1 = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
