@@ -347,7 +347,44 @@ __global__ void k_ell_ilu0(long long nblk, int B, int WL, int WU, double *__rest
 }
 
 // W = padded slot count (2, 4, 8, 16).  Rows go in chunks of PF whose slot loads (independent of
-// the chain) are all issued before the chunk's sequential updates out of shared memory.
+// the chain) are issued one chunk ahead (double-buffered registers), so the chain of chunk c runs
+// out of shared memory while the loads of chunk c+1 are in flight.
+template <int W, int PF>
+struct EllChunk {
+    double v[PF][W], d[PF];
+    int k[PF][W];
+};
+
+template <int W, int PF, bool LOWER>
+__device__ __forceinline__ void ell_load(EllChunk<W, PF> &C, int c0, int B, long long nblk, long long blk,
+                                         const double *__restrict__ V, const uint8_t *__restrict__ K,
+                                         const double *__restrict__ D) {
+#pragma unroll
+    for (int q = 0; q < PF; q++) {
+        const int il = LOWER ? min(c0 + q, B - 1) : max(c0 - q, 0);
+        if (!LOWER) C.d[q] = D[(long long)il * nblk + blk];
+#pragma unroll
+        for (int t = 0; t < W; t++) {
+            C.v[q][t] = V[ell_at(il, t, W, nblk, blk)];
+            C.k[q][t] = K[ell_at(il, t, W, nblk, blk)];
+        }
+    }
+}
+
+template <int W, int PF, bool LOWER>
+__device__ __forceinline__ void ell_chain(const EllChunk<W, PF> &C, int c0, int B, double *my) {
+#pragma unroll
+    for (int q = 0; q < PF; q++) {
+        const int il = LOWER ? c0 + q : c0 - q;
+        if (LOWER ? il < B : il >= 0) {
+            double acc = my[il];
+#pragma unroll
+            for (int t = 0; t < W; t++) acc -= C.v[q][t] * my[C.k[q][t]];
+            my[il] = LOWER ? acc : acc / C.d[q];
+        }
+    }
+}
+
 template <int W>
 __global__ void __launch_bounds__(TPB_CTA) k_ell_solve(long long n, int B, long long nblk, const double *__restrict__ Lv,
                                                        const uint8_t *__restrict__ Lc, const double *__restrict__ Uv,
@@ -365,56 +402,62 @@ __global__ void __launch_bounds__(TPB_CTA) k_ell_solve(long long n, int B, long 
     const long long blk = (long long)blockIdx.x * TPB_CTA + tid;
     if (blk < nblk) {
         double *my = zsm + tid * ld;
-        for (int c = 0; c < B; c += PF) {
-            double v[PF][W];
-            int k[PF][W];
-#pragma unroll
-            for (int q = 0; q < PF; q++) {
-                const int il = min(c + q, B - 1);
-#pragma unroll
-                for (int t = 0; t < W; t++) {
-                    v[q][t] = Lv[ell_at(il, t, W, nblk, blk)];
-                    k[q][t] = Lc[ell_at(il, t, W, nblk, blk)];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < PF; q++) {
-                if (c + q < B) {
-                    double acc = my[c + q];
-#pragma unroll
-                    for (int t = 0; t < W; t++) acc -= v[q][t] * my[k[q][t]];
-                    my[c + q] = acc;
-                }
-            }
+        EllChunk<W, PF> A, Bq;
+        ell_load<W, PF, true>(A, 0, B, nblk, blk, Lv, Lc, D);
+        for (int c = 0; c < B; c += 2 * PF) {
+            ell_load<W, PF, true>(Bq, c + PF, B, nblk, blk, Lv, Lc, D);
+            ell_chain<W, PF, true>(A, c, B, my);
+            ell_load<W, PF, true>(A, c + 2 * PF, B, nblk, blk, Lv, Lc, D);
+            ell_chain<W, PF, true>(Bq, c + PF, B, my);
         }
-        for (int c = B - 1; c >= 0; c -= PF) {
-            double v[PF][W], d[PF];
-            int k[PF][W];
-#pragma unroll
-            for (int q = 0; q < PF; q++) {
-                const int il = max(c - q, 0);
-                d[q] = D[(long long)il * nblk + blk];
-#pragma unroll
-                for (int t = 0; t < W; t++) {
-                    v[q][t] = Uv[ell_at(il, t, W, nblk, blk)];
-                    k[q][t] = Uc[ell_at(il, t, W, nblk, blk)];
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < PF; q++) {
-                if (c - q >= 0) {
-                    double acc = my[c - q];
-#pragma unroll
-                    for (int t = 0; t < W; t++) acc -= v[q][t] * my[k[q][t]];
-                    my[c - q] = acc / d[q];
-                }
-            }
+        ell_load<W, PF, false>(A, B - 1, B, nblk, blk, Uv, Uc, D);
+        for (int c = B - 1; c >= 0; c -= 2 * PF) {
+            ell_load<W, PF, false>(Bq, c - PF, B, nblk, blk, Uv, Uc, D);
+            ell_chain<W, PF, false>(A, c, B, my);
+            ell_load<W, PF, false>(A, c - 2 * PF, B, nblk, blk, Uv, Uc, D);
+            ell_chain<W, PF, false>(Bq, c - PF, B, my);
         }
     }
     __syncthreads();
     for (int idx = tid; idx < TPB_CTA * B; idx += TPB_CTA) {
         const long long g = cta_r0 + idx;
         if (g < n) z[g] = zsm[(idx / B) * ld + idx % B];
+    }
+}
+
+// y = A x (or bsub - A x) for short rows, CSR-stream: a CTA takes SP_R consecutive rows, streams
+// their nonzeros contiguously (coalesced a / col_idx loads, many in flight per thread) into
+// shared-memory products, then one thread per row sums its range.  Blocks whose nonzeros exceed
+// SP_CAP fall back to one warp per row.
+constexpr int SP_R = 128, SP_CAP = 4096;
+__global__ void __launch_bounds__(SP_R) k_spmv_stream(long long n, const int64_t *__restrict__ rp,
+                                                      const int32_t *__restrict__ ci, const double *__restrict__ a,
+                                                      const double *__restrict__ x, double *__restrict__ y,
+                                                      const double *__restrict__ bsub) {
+    __shared__ double prod[SP_CAP];
+    __shared__ long long srp[SP_R + 1];
+    const long long row0 = (long long)blockIdx.x * SP_R;
+    const int nr = (int)min((long long)SP_R, n - row0);
+    for (int i = threadIdx.x; i <= nr; i += SP_R) srp[i] = rp[row0 + i];
+    __syncthreads();
+    const long long p0 = srp[0], cnt = srp[nr] - p0;
+    if (cnt <= SP_CAP) {
+        for (int k = threadIdx.x; k < cnt; k += SP_R) prod[k] = a[p0 + k] * __ldg(x + ci[p0 + k]);
+        __syncthreads();
+        if (threadIdx.x < nr) {
+            const int r = threadIdx.x;
+            double s = 0.0;
+            for (long long k = srp[r] - p0; k < srp[r + 1] - p0; k++) s += prod[k];
+            y[row0 + r] = bsub ? bsub[row0 + r] - s : s;
+        }
+    } else {
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        for (int r = wid; r < nr; r += SP_R / 32) {
+            double s = 0.0;
+            for (long long p = srp[r] + lane; p < srp[r + 1]; p += 32) s += a[p] * __ldg(x + ci[p]);
+            s = warp_sum(s);
+            if (lane == 0) y[row0 + r] = bsub ? bsub[row0 + r] - s : s;
+        }
     }
 }
 
@@ -479,54 +522,75 @@ __global__ void k_arn_start(ArnLayout Lo, double *base) {
     c->need2 = 1;
 }
 
-__global__ void k_arn_ctrl(ArnLayout Lo, double *base, int j, int pass) {
-    const int m = Lo.m;
+// one warp: lanes load / reduce the column in parallel, lane 0 runs the short sequential part
+// (previous rotations, new rotation) out of shared memory
+__global__ void __launch_bounds__(32) k_arn_ctrl(ArnLayout Lo, double *base, int j, int pass) {
+    const int m = Lo.m, lane = threadIdx.x;
     double *hb = base + Lo.hbuf(), *hv = base + Lo.hvec(), *H = base + Lo.H(), *cs = base + Lo.cs(),
            *sn = base + Lo.sn(), *g = base + Lo.g();
     ArnCtl *c = reinterpret_cast<ArnCtl *>(base + Lo.ctl());
+    __shared__ double col[64], scs[64], ssn[64];
+    __shared__ int last_s;
     if (pass == 1 && !c->need2) return;
     double hh = 0.0;
-    for (int i = 0; i <= j; i++) {
-        hv[i] = hb[i];
-        hh += hb[i] * hb[i];
-        H[(size_t)i * m + j] = (pass == 0 ? 0.0 : H[(size_t)i * m + j]) + hb[i];
+    for (int i = lane; i <= j; i += 32) {
+        const double h = hb[i];
+        hv[i] = h;
+        hh += h * h;
+        col[i] = (pass == 0 ? 0.0 : H[(size_t)i * m + j]) + h;
+        if (i < j) { scs[i] = cs[i]; ssn[i] = sn[i]; }
     }
+    hh = warp_sum(hh);
     const double ww = hb[j + 1], nrm2 = ww - hh;
-    for (int i = 0; i <= j + 1; i++) hb[i] = 0.0;
-    const bool last = pass == 1 || nrm2 > 0.5 * ww;
-    if (pass == 0) c->need2 = last ? 0 : 1;          // gates the second pass's three launches
-    c->scale = 1.0;
-    if (!last) return;
-    const double hj1 = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
-    if (hj1 > 0.0) c->scale = 1.0 / hj1;
-    for (int i = 0; i < j; i++) {
-        const double a0 = H[(size_t)i * m + j], a1 = H[(size_t)(i + 1) * m + j];
-        H[(size_t)i * m + j] = cs[i] * a0 + sn[i] * a1;
-        H[(size_t)(i + 1) * m + j] = -sn[i] * a0 + cs[i] * a1;
+    __syncwarp();
+    for (int i = lane; i <= j + 1; i += 32) hb[i] = 0.0;
+    if (lane == 0) {
+        const bool last = pass == 1 || nrm2 > 0.5 * ww;
+        if (pass == 0) c->need2 = last ? 0 : 1;          // gates the second pass's three launches
+        c->scale = 1.0;
+        last_s = last;
+        if (last) {
+            const double hj1 = nrm2 > 0.0 ? sqrt(nrm2) : 0.0;
+            if (hj1 > 0.0) c->scale = 1.0 / hj1;
+            for (int i = 0; i < j; i++) {
+                const double a0 = col[i], a1 = col[i + 1];
+                col[i] = scs[i] * a0 + ssn[i] * a1;
+                col[i + 1] = -ssn[i] * a0 + scs[i] * a1;
+            }
+            const double hjj = col[j], den = hypot(hjj, hj1);
+            cs[j] = den > 0.0 ? hjj / den : 1.0;
+            sn[j] = den > 0.0 ? hj1 / den : 0.0;
+            col[j] = den;
+            const double gj = g[j];
+            g[j + 1] = -sn[j] * gj;
+            g[j] = cs[j] * gj;
+            if (c->jstop == m || c->jstop > j) c->res = fabs(g[j + 1]);
+            if (hj1 == 0.0 && c->jstop > j + 1) c->jstop = j + 1;   // lucky breakdown: later columns unused
+        }
     }
-    const double hjj = H[(size_t)j * m + j], den = hypot(hjj, hj1);
-    cs[j] = den > 0.0 ? hjj / den : 1.0;
-    sn[j] = den > 0.0 ? hj1 / den : 0.0;
-    H[(size_t)j * m + j] = den;
-    g[j + 1] = -sn[j] * g[j];
-    g[j] = cs[j] * g[j];
-    if (c->jstop == m || c->jstop > j) c->res = fabs(g[j + 1]);
-    if (hj1 == 0.0 && c->jstop > j + 1) c->jstop = j + 1;         // lucky breakdown: later columns unused
+    __syncwarp();
+    for (int i = lane; i <= j; i += 32) H[(size_t)i * m + j] = col[i];
 }
 
 // y = R^{-1} g over the first min(jmax, jstop) columns; yneg = -y, zero beyond
-__global__ void k_arn_solve(ArnLayout Lo, double *base, int jmax) {
+__global__ void __launch_bounds__(256) k_arn_solve(ArnLayout Lo, double *base, int jmax) {
     const int m = Lo.m;
     const double *H = base + Lo.H(), *g = base + Lo.g();
     double *yn = base + Lo.yneg();
     const ArnCtl *c = reinterpret_cast<const ArnCtl *>(base + Lo.ctl());
+    __shared__ double sH[64 * 64], sy[64];
     const int j = min(jmax, c->jstop);
-    for (int i = jmax - 1; i >= j; i--) yn[i] = 0.0;
-    for (int i = j - 1; i >= 0; i--) {
-        double t = g[i];
-        for (int k = i + 1; k < j; k++) t += H[(size_t)i * m + k] * yn[k];     // yn = -y
-        yn[i] = -t / H[(size_t)i * m + i];
-    }
+    for (int t = threadIdx.x; t < j * j; t += blockDim.x) sH[t] = H[(size_t)(t / j) * m + t % j];
+    for (int t = threadIdx.x; t < j; t += blockDim.x) sy[t] = g[t];
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int i = j - 1; i >= 0; i--) {                 // sy = -y
+            double t = sy[i];
+            for (int k = i + 1; k < j; k++) t += sH[i * j + k] * sy[k];
+            sy[i] = -t / sH[i * j + i];
+        }
+    __syncthreads();
+    for (int t = threadIdx.x; t < jmax; t += blockDim.x) yn[t] = t < j ? sy[t] : 0.0;
 }
 
 // device buffer `slot` of the space's solver workspace, grown to >= bytes (contents not kept)
@@ -568,8 +632,10 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
     const long long avg = n > 0 ? nnz / n : 0;
     const int lpr = avg <= 12 ? 4 : avg <= 40 ? 8 : avg <= 96 ? 16 : 32;
     const unsigned grow = (unsigned)((n * lpr + 255) / 256);
+    const bool stream_spmv = avg <= SP_CAP / SP_R && !s->gm_host_ctrl;   // mean row fits the stream tile
     auto spmv = [&](const double *xin, double *yout, const double *bsub) {
-        if (lpr == 4) k_spmv_sw<4><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
+        if (stream_spmv) k_spmv_stream<<<(unsigned)((n + SP_R - 1) / SP_R), SP_R, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
+        else if (lpr == 4) k_spmv_sw<4><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
         else if (lpr == 8) k_spmv_sw<8><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
         else if (lpr == 16) k_spmv_sw<16><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
         else k_spmv_sw<32><<<grow, 256, 0, st>>>(n, rp, ci, a, xin, yout, bsub);
@@ -637,7 +703,7 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
         return std::sqrt(h);
     };
     const double bnorm = norm2(b);
-    if (opt->rtol == 0.0 && !s->gm_host_ctrl) {
+    if (opt->rtol == 0.0 && !s->gm_host_ctrl && m <= 62) {   // (k_arn_* stage <= 64 entries in smem)
         // fixed budget: device-driven cycles, one host synchronisation at the end
         const ArnLayout Lo{m};
         int *need2 = reinterpret_cast<int *>(reinterpret_cast<ArnCtl *>(dh + Lo.ctl())) + 6;   // ArnCtl::need2
@@ -658,13 +724,13 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
                 spmv(Z + (size_t)j * n, vj1, nullptr);
                 for (int pass = 0; pass < 2; pass++) {
                     k_multidot<<<gv, 256, 0, st>>>(n, j + 2, V, n, vj1, dh, pass ? need2 : nullptr);
-                    k_arn_ctrl<<<1, 1, 0, st>>>(Lo, dh, j, pass);
+                    k_arn_ctrl<<<1, 32, 0, st>>>(Lo, dh, j, pass);
                     k_multiaxpy<<<gv, 256, 0, st>>>(n, j + 1, V, n, dh + Lo.hvec(), vj1, 1.0, dscale,
                                                     pass ? need2 : nullptr);
                 }
                 launches += 7;
             }
-            k_arn_solve<<<1, 1, 0, st>>>(Lo, dh, jm);
+            k_arn_solve<<<1, 256, 0, st>>>(Lo, dh, jm);
             k_multiaxpy<<<gv, 256, 0, st>>>(n, jm, Z, n, dh + Lo.yneg(), x, 1.0);
             launches += 2;
             it += jm;
