@@ -120,3 +120,39 @@ def test_full_size_newton_step_config3():
         assert rr < prev
         prev = rr
     assert prev < 1e-3          # the 4th-order CH system: ~3e-4 after the paper's 30 iterations
+
+
+@pytest.mark.parametrize("restart,maxit,B,precond", [(60, 60, 0, 2), (7, 0, 0, 2), (30, 30, 100000, 2),
+                                                     (30, 30, 2000, 2), (70, 70, 0, 1)])
+def test_edge_cases(restart, maxit, B, precond):
+    """restart > n (finite termination inside one cycle), maxit = 0 (x0 returned, true residual),
+    one block covering the whole matrix (device ILU(0) through the CSR warp path = full ILU(0)),
+    restart beyond the device-control limit (host path)."""
+    iga = _gpu()
+    w, rp, ci, v, b = _system(3, 6)               # 36 rows
+    sp = iga.Space.from_workload(w)
+    x0 = np.random.default_rng(2).uniform(-1e-3, 1e-3, b.size)
+    x, it, rr = sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(b), x=_dev(x0), restart=restart, maxit=maxit, rtol=0.0,
+                         precond=precond, block_rows=B)
+    xo, ito, rro = krylov.gmres(rp, ci, v, b, x0=x0, restart=restart, maxit=maxit, rtol=0.0, precond=precond,
+                                block_rows=B or 64)
+    # past n iterations the Krylov space is exhausted: the host path stops at the (Pythagoras)
+    # breakdown h_{j+1} = 0, the oracle's MGS norm stays at rounding level and it keeps iterating
+    assert it == ito or (restart > b.size and b.size <= it <= ito)
+    xg = x.cpu().numpy()
+    if maxit == 0:
+        assert np.array_equal(xg, x0)
+    assert np.max(np.abs(xg - xo)) <= 1e-7 * np.max(np.abs(xo))
+    assert abs(rr - rro) <= 1e-6 * max(rro, 1e-13) + 1e-13
+
+
+def test_ring_and_nsk_systems():
+    """GMRES on the Alg. 2 ring (NURBS, periodic) and on the nonsymmetric NSK Jacobian."""
+    iga = _gpu()
+    for cid, n in ((7, 8), (6, 7)):
+        w, rp, ci, v, b = _system(cid, n)
+        sp = iga.Space.from_workload(w)
+        x, it, rr = sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(b), restart=30, maxit=30, rtol=0.0)
+        xo, ito, rro = krylov.gmres(rp, ci, v, b, restart=30, maxit=30, rtol=0.0, precond=2, block_rows=64)
+        assert it == ito == 30
+        assert np.max(np.abs(x.cpu().numpy() - xo)) <= 1e-8 * np.max(np.abs(xo)), cid
