@@ -22,7 +22,9 @@ namespace iga {
 
 template <int P> struct Tile2 {
     static constexpr int TE0 = 16;
-    static constexpr int TE1 = P == 2 ? 36 : 16;   // 16 rounds of 36 (p = 2) element groups
+    // TE1 = the widest tile along axis 1 (shared-memory layout); the launch picks the actual
+    // width te1 <= TE1 so that the tile count fills the SMs in whole rounds (wave quantisation)
+    static constexpr int TE1 = P == 2 ? 36 : 32;
     // 12 warps (168 registers, no spills with the direct scatter; measured best for p = 2 and 3)
     static constexpr int NWARP = 12;
     static constexpr int NB0 = TE0 + P, NB1 = TE1 + P;      // touched node box (uniform knots)
@@ -147,7 +149,7 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
 template <int P, class PH, int MODE, bool JAC, int UNI>
 __global__ void __launch_bounds__(32 * Tile2<P>::NWARP, 1)
 k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
-          double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1, int dbg_,
+          double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1, int te1, int dbg_,
           const __grid_constant__ UniTab2<P> ut) {
     const int dbg = IGA_DBG ? dbg_ : 0;
     using L = Lists<PH, 2, MODE>;
@@ -185,8 +187,8 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
     for (int tile = blockIdx.x; tile < ntile0 * ntile1; tile += gridDim.x) {
         const int T0 = tile / ntile1, T1 = tile % ntile1;
-        const int e0lo = A0.el_lo + T0 * TL::TE0, e1lo = A1.el_lo + T1 * TL::TE1;
-        const int ne0 = min(TL::TE0, A0.el_hi - e0lo), ne1 = min(TL::TE1, A1.el_hi - e1lo);
+        const int e0lo = A0.el_lo + T0 * TL::TE0, e1lo = A1.el_lo + T1 * te1;
+        const int ne0 = min(TL::TE0, A0.el_hi - e0lo), ne1 = min(te1, A1.el_hi - e1lo);
         const int F00 = A0.first[e0lo], F01 = A1.first[e1lo];
         const int nb0 = ne0 + P, nb1 = ne1 + P;
         // ---- stage the tile: node data, scatter metadata, tables ----
@@ -372,7 +374,7 @@ static size_t fused2d_smem(bool jac) {
 
 template <int P, class PH, int MODE, bool JAC, int UNI>
 static iga_status launch_k2(iga_space_s *s, const Prm &prm, double a, double b, const double *U, const double *Ud,
-                            double *val, double *F, int nt0, int nt1, const UniTab2<P> &ut, cudaStream_t st, int nsm) {
+                            double *val, double *F, int ne0, int ne1, const UniTab2<P> &ut, cudaStream_t st, int nsm) {
     using TL = Tile2<P>;
     constexpr int NT = 32 * TL::NWARP;
     const size_t smem = fused2d_smem<P, PH, MODE>(JAC);
@@ -386,9 +388,20 @@ static iga_status launch_k2(iga_space_s *s, const Prm &prm, double a, double b, 
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, JAC, UNI>, NT, smem);
     occ = std::max(occ, 1);
-    const int grid = std::min(nt0 * nt1, nsm * occ);
+    // tile width along axis 1: fewest whole rounds of the persistent CTAs times the per-tile work
+    // (te1 + P node columns), ties to the wider tile
+    const int nt0 = (ne0 + TL::TE0 - 1) / TL::TE0, slots = nsm * occ;
+    int te1 = TL::TE1;
+    long long best = -1;
+    for (int w = TL::TE1; w >= std::max(4, TL::TE1 / 2); w--) {
+        const long long nt = (long long)nt0 * ((ne1 + w - 1) / w);
+        const long long cost = ((nt + slots - 1) / slots) * (w + P);
+        if (best < 0 || cost < best) { best = cost; te1 = w; }
+    }
+    const int nt1 = (ne1 + te1 - 1) / te1;
+    const int grid = (int)std::min<long long>((long long)nt0 * nt1, slots);
     ProfScope ps(s, "k_fused2d", st);
-    k_fused2d<P, PH, MODE, JAC, UNI><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1, s->dbg, ut);
+    k_fused2d<P, PH, MODE, JAC, UNI><<<grid, NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nt0, nt1, te1, s->dbg, ut);
     return IGA_OK;
 }
 
@@ -400,7 +413,6 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
     for (int i = 0; i < 8; i++) prm.p[i] = phys->p[i];
     const bool jac = val != nullptr;
     const int ne0 = s->el_hi[0] - s->el_lo[0], ne1 = s->el_hi[1] - s->el_lo[1];
-    const int nt0 = (ne0 + TL::TE0 - 1) / TL::TE0, nt1 = (ne1 + TL::TE1 - 1) / TL::TE1;
     // fast path whenever both axes have a uniform run (all elements on periodic knots, all but p at
     // each end on open uniform knots); the kernel checks each element against the runs
     const bool runs = s->dev.ax[0].uni_hi > s->dev.ax[0].uni_lo && s->dev.ax[1].uni_hi > s->dev.ax[1].uni_lo;
@@ -417,10 +429,10 @@ iga_status run_fused2d(iga_space_s *s, const iga_phys *phys, double a, double b,
         launches++;
     }
     iga_status r;
-    if (jac) r = uni == 2 ? launch_k2<P, PH, MODE, true, 2>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
-               : uni == 1 ? launch_k2<P, PH, MODE, true, 1>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm)
-                          : launch_k2<P, PH, MODE, true, 0>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
-    else r = launch_k2<P, PH, MODE, false, 0>(s, prm, a, b, U, Ud, val, F, nt0, nt1, ut, st, nsm);
+    if (jac) r = uni == 2 ? launch_k2<P, PH, MODE, true, 2>(s, prm, a, b, U, Ud, val, F, ne0, ne1, ut, st, nsm)
+               : uni == 1 ? launch_k2<P, PH, MODE, true, 1>(s, prm, a, b, U, Ud, val, F, ne0, ne1, ut, st, nsm)
+                          : launch_k2<P, PH, MODE, true, 0>(s, prm, a, b, U, Ud, val, F, ne0, ne1, ut, st, nsm);
+    else r = launch_k2<P, PH, MODE, false, 0>(s, prm, a, b, U, Ud, val, F, ne0, ne1, ut, st, nsm);
     if (r != IGA_OK) return r;
     launches++;
     s->last_launches = launches;
