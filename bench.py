@@ -267,10 +267,21 @@ def run_iga(args, w, ws, rank, local):
     def step():
         sp.form_jacobian(ph, w.a, w.b, U, Ud, vals=vals, F=F)
 
+    experiment = any(kv.startswith("dbg=") and kv != "dbg=0" for kv in args.opt)   # phase-skip A/B: results invalid
+
+    def check():
+        if experiment:
+            try:
+                sp.check()
+            except iga.IgaError:
+                pass
+        else:
+            sp.check()
+
     for _ in range(args.warmup):
         flush.zero_()
         step()
-    sp.check()
+    check()
     torch.cuda.synchronize()
     launches_per_step = sp.last_launch_count()
 
@@ -297,7 +308,7 @@ def run_iga(args, w, ws, rank, local):
 
     with ClockSampler(local) as clk:
         ms, _ = timed_region(args.steps)
-    sp.check()
+    check()
     step_ms = sum(ms) / len(ms)
     nqp_total = sp.nqp
     if ws > 1:
