@@ -266,6 +266,118 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             const int fo0 = le0, fo1 = le1;
             const double *tb0 = tb + (size_t)(0 * TL::TE1 + le0) * NQ1 * 3 * NP1;
             const double *tb1 = tb + (size_t)(1 * TL::TE1 + le1) * NQ1 * 3 * NP1;
+            // (0) the point's homogeneous sums (w, w x, w u, w udot and their kinds), sum factorised
+            //     over the element's functions by the lane group: stage 1, lane (a0, q1):
+            //     S1[a0][q1][f][o1] = sum_a1 T1(q1, o1, a1) f(a0, a1), into the group scratch;
+            //     stage 2, lane (q0, q1): S[f][o0][o1] = sum_a0 T0(q0, o0, a0) S1[a0][q1][f][o1]
+            //     (2 (p+1)^3 FMA per field and order pair instead of (p+1)^4 per point)
+            constexpr int NFW = MODE == MODE_NURBS ? 3 : 0;               // w, w x0, w x1
+            constexpr int NF = NFW + 1 + (PH::UDOT ? 1 : 0);              // + w u (+ w udot)
+            constexpr bool SFP = P == 3 && NP1 == NQ1 && NP1 * NQ1 * NF * 3 <= SCR * NQ;   // p = 2: slower (A/B)
+            constexpr int NPRE = KS::NC * (1 + 2 + 1) + 1;
+            if constexpr (SFP) {
+                double pre[NPRE];
+                const int base_n = fo0 * NB1 + fo1;
+                constexpr auto used = [](int o0, int o1) {
+                    for (int c = 0; c < KS::NC; c++)
+                        for (int tt = 0; tt < KS::nterms(c); tt++)
+                            if (KS::ord(c, tt, 0) == o0 && KS::ord(c, tt, 1) == o1) return true;
+                    return o0 == 0 && o1 == 0;
+                };
+                constexpr auto used1 = [](int o1) {
+                    for (int o0 = 0; o0 < 3; o0++)
+                        for (int c = 0; c < KS::NC; c++)
+                            for (int tt = 0; tt < KS::nterms(c); tt++)
+                                if (KS::ord(c, tt, 0) == o0 && KS::ord(c, tt, 1) == o1) return true;
+                    return o1 == 0;
+                };
+                const double *fsrc[5] = {nw, nx0, nx1, nU, nUd};
+                if (act && !(dbg & 4)) {
+                    const int a0 = t / NQ1, q1 = t % NQ1;
+                    double fv[NF][NP1];
+#pragma unroll
+                    for (int f = 0; f < NF; f++)
+#pragma unroll
+                        for (int a1 = 0; a1 < NP1; a1++) fv[f][a1] = fsrc[NFW ? f : f + 3][base_n + a0 * NB1 + a1];
+                    static_for<3>([&](auto O1) {
+                        constexpr int o1 = decltype(O1)::value;
+                        if constexpr (used1(o1)) {
+                            double t1[NP1];
+#pragma unroll
+                            for (int a1 = 0; a1 < NP1; a1++) t1[a1] = tb1[(q1 * 3 + o1) * NP1 + a1];
+#pragma unroll
+                            for (int f = 0; f < NF; f++) {
+                                double acc = 0.0;
+#pragma unroll
+                                for (int a1 = 0; a1 < NP1; a1++) acc += t1[a1] * fv[f][a1];
+                                gs[((a0 * NQ1 + q1) * NF + f) * 3 + o1] = acc;
+                            }
+                        }
+                    });
+                }
+                __syncwarp();
+                if (act && !(dbg & 4)) {
+                    const int q0 = t / NQ1, q1 = t % NQ1;
+                    double S[NF][3][3];
+                    static_for<3>([&](auto O0) {
+                        constexpr int o0 = decltype(O0)::value;
+                        static_for<3>([&](auto O1) {
+                            constexpr int o1 = decltype(O1)::value;
+                            if constexpr (used(o0, o1)) {
+#pragma unroll
+                                for (int f = 0; f < NF; f++) {
+                                    double acc = 0.0;
+#pragma unroll
+                                    for (int a0 = 0; a0 < NP1; a0++)
+                                        acc += tb0[(q0 * 3 + o0) * NP1 + a0] * gs[((a0 * NQ1 + q1) * NF + f) * 3 + o1];
+                                    S[f][o0][o1] = acc;
+                                }
+                            }
+                        });
+                    });
+                    // kinds: sum of the kind's separable terms; pre = [W][X0][X1][Phi][Phit]
+                    static_for<KS::NC>([&](auto C) {
+                        constexpr int c = decltype(C)::value;
+                        double kv[NF];
+#pragma unroll
+                        for (int f = 0; f < NF; f++) kv[f] = 0.0;
+                        static_for<KS::nterms(c)>([&](auto TT) {
+                            constexpr int tt = decltype(TT)::value;
+#pragma unroll
+                            for (int f = 0; f < NF; f++) kv[f] += S[f][KS::ord(c, tt, 0)][KS::ord(c, tt, 1)];
+                        });
+                        pre[c] = NFW ? kv[0] : 1.0;
+                        pre[KS::NC + c] = NFW ? kv[1] : 0.0;
+                        pre[2 * KS::NC + c] = NFW ? kv[2] : 0.0;
+                        pre[3 * KS::NC + c] = kv[NFW];
+                    });
+                    pre[4 * KS::NC] = PH::UDOT ? S[NF - 1][0][0] : 0.0;
+                }
+                __syncwarp();                    // S1 consumed before pointwise_qp writes the scratch
+            if (act) {
+                // (1) pointwise at quadrature point q = t
+                const int q0 = t / NQ1, q1 = t % NQ1;
+                double v[2][3][NP1];
+#pragma unroll
+                for (int k = 0; k < 3; k++)
+#pragma unroll
+                    for (int x = 0; x < NP1; x++) {
+                        v[0][k][x] = tb0[(q0 * 3 + k) * NP1 + x];
+                        v[1][k][x] = tb1[(q1 * 3 + k) * NP1 + x];
+                    }
+                const double wq = qwb[le0 * NQ1 + q0] * qwb[TL::TE1 * NQ1 + le1 * NQ1 + q1];
+                const double xq[2] = {qxb[le0 * NQ1 + q0], qxb[TL::TE1 * NQ1 + le1 * NQ1 + q1]};
+                const double hp[2] = {hpb[le0], hpb[TL::TE1 + le1]};
+                SmemNodes2<NP1, NB1> nodes;
+                nodes.pu = nU; nodes.pud = nUd; nodes.pw = s.wts ? nw : nullptr; nodes.px0 = nx0; nodes.px1 = nx1;
+                nodes.hud = Ud != nullptr;
+                nodes.base = base_n;
+                if (!(dbg & 4))          // dbg bits skip phases (A/B timing only; results invalid)
+                    errbits |= pointwise_qp<2, P, PH, MODE, JAC, SmemNodes2<NP1, NB1>, true, SFP>(
+                        s, prm, a, b, v, wq, xq, hp, nodes, JAC ? gs + t : nullptr, NQ,
+                        Fout ? gs + (JAC ? NE * NQ : 0) + t : nullptr, NQ, pre);
+            }
+            } else {
             if (act) {
                 // (1) pointwise at quadrature point q = t
                 const int q0 = t / NQ1, q1 = t % NQ1;
@@ -285,9 +397,10 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 nodes.hud = Ud != nullptr;
                 nodes.base = fo0 * NB1 + fo1;
                 if (!(dbg & 4))          // dbg bits skip phases (A/B timing only; results invalid)
-                    errbits |= pointwise_qp<2, P, PH, MODE, JAC, SmemNodes2<NP1, NB1>, true>(s, prm, a, b, v, wq, xq, hp, nodes,
-                                                                 JAC ? gs + t : nullptr, NQ,
-                                                                 Fout ? gs + (JAC ? NE * NQ : 0) + t : nullptr, NQ);
+                    errbits |= pointwise_qp<2, P, PH, MODE, JAC, SmemNodes2<NP1, NB1>, true>(
+                        s, prm, a, b, v, wq, xq, hp, nodes, JAC ? gs + t : nullptr, NQ,
+                        Fout ? gs + (JAC ? NE * NQ : 0) + t : nullptr, NQ);
+            }
             }
             __syncwarp();
             if (act) {

@@ -32,11 +32,15 @@ __device__ __forceinline__ double kind_value(const V &v, const int *aa) {
 // Nodes: accessor with u(A,m), ud(A,m), has_ud(), w(A), x(A,i) for the element's local functions;
 // Nodes::PREMUL = the accessor returns w_A u, w_A udot, w_A x (homogeneous coordinates, staged once).
 // Returns error bits (1: detJ <= 0, 2: non-finite).
-template <int DIM, int P, class PH, int MODE, bool JAC, class Nodes, bool UNROLL_A = false>
+// PRE: the caller already formed the homogeneous sums of the point (fused2d: sum factorised over
+// the element's lane group) and passes them in `pre` = [W: NC][X: DIM x NC][Phi: M x NC][Phit: M];
+// the per-function loop is skipped.
+template <int DIM, int P, class PH, int MODE, bool JAC, class Nodes, bool UNROLL_A = false, bool PRE = false>
 __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, double a, double b,
                                             const double (&v)[DIM][3][P + 1], double wq, const double (&xq)[DIM],
                                             const double (&hp)[DIM], const Nodes &nodes, double *__restrict__ Dt,
-                                            long long dstr, double *__restrict__ Rt, long long rstr) {
+                                            long long dstr, double *__restrict__ Rt, long long rstr,
+                                            const double *pre = nullptr) {
     using L = Lists<PH, DIM, MODE>;
     using KS = typename L::KS;
     constexpr int M = PH::M, NP1 = P + 1;
@@ -91,7 +95,18 @@ __device__ __forceinline__ int pointwise_qp(const SpaceDev &s, const Prm &prm, d
                 Phit[m] += ((MODE == MODE_NURBS && Nodes::PREMUL) ? nodes.ud(A, m) : wA * nodes.ud(A, m)) * Pc[0];
         }
     };
-    if constexpr (UNROLL_A) {
+    if constexpr (PRE) {
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            W[c] = pre[c];
+#pragma unroll
+            for (int i = 0; i < DIM; i++) X[i][c] = pre[NC + i * NC + c];
+#pragma unroll
+            for (int m = 0; m < M; m++) Phi[m][c] = pre[NC + DIM * NC + m * NC + c];
+        }
+#pragma unroll
+        for (int m = 0; m < M; m++) Phit[m] = pre[NC + DIM * NC + M * NC + m];
+    } else if constexpr (UNROLL_A) {
         static_for<NEN>([&](auto AA) { body(decltype(AA)::value); });
     } else {
 #pragma unroll 1
