@@ -605,7 +605,7 @@ def run_protocol(args, w, local):
         "unit": "steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t,
         "higher_is_better": True, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "op": "iga_alpha_step", "rho_inf": rho, "dt": dt, "newton_its": 2,
-                   "gmres": "GMRES(30), 30 iterations, block-Jacobi ILU(0), 64-row blocks",
+                   "gmres": "GMRES(30), 30 iterations, block-Jacobi ILU(0), 32-row blocks",
                    "l2": "inputs larger than L2 (matrix)"},
         "breakdown_ms": {"assembly_jacobian_and_residual": t_asm, "gmres_setup_and_residual": t_g0,
                          "gmres_per_iteration": t_it, "gmres_30_iterations": t_g30},

@@ -205,7 +205,7 @@ iga_status iga_basis_eval(iga_space s, int order, double *out, void *stream);
  * cited P:872), classical Gram-Schmidt applied twice, Givens rotations; stops when the
  * preconditioned-Krylov residual estimate |g_{j+1}| <= rtol * ||b|| or after maxit total
  * iterations.  Preconditioner `precond`: 0 none, 1 point Jacobi (diag), 2 block Jacobi with ILU(0)
- * (Saad's IKJ ILU(0), no fill) in each diagonal block of `block_rows` consecutive rows (0 -> 64;
+ * (Saad's IKJ ILU(0), no fill) in each diagonal block of `block_rows` consecutive rows (0 -> 32;
  * reading A-28: the GPU's blocks are row runs, not one per process).  Entries outside the block
  * are not part of the preconditioner.
  * row_ptr/col_idx/val: this space's CSR (iga_csr_pattern + iga_form_jacobian), device, sorted
@@ -221,7 +221,7 @@ typedef struct {
     int maxit;      /* total iteration cap (paper: 30 per Newton step) */
     double rtol;    /* relative tolerance on ||b - A x|| / ||b|| */
     int precond;    /* 0 none, 1 Jacobi, 2 block-Jacobi ILU(0) */
-    int block_rows; /* rows per block-Jacobi block (precond 2); 0 -> 64 */
+    int block_rows; /* rows per block-Jacobi block (precond 2); 0 -> 32 */
 } iga_krylov;
 iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
                      const double *b, double *x, const iga_krylov *opt, int *iters, double *relres,

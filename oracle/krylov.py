@@ -95,7 +95,7 @@ def csr_matvec(rp, ci, val, x):
     return y
 
 
-def make_precond(rp, ci, val, precond, block_rows=256):
+def make_precond(rp, ci, val, precond, block_rows=32):
     """M^{-1} as a function: 0 identity, 1 point Jacobi, 2 block-Jacobi ILU(0)."""
     n = len(rp) - 1
     if precond == 0:
@@ -107,7 +107,7 @@ def make_precond(rp, ci, val, precond, block_rows=256):
     return lambda r: ilu0_solve(rp, ci, lu, r, block_rows)
 
 
-def gmres(rp, ci, val, b, x0=None, restart=30, maxit=30, rtol=1e-8, precond=2, block_rows=256):
+def gmres(rp, ci, val, b, x0=None, restart=30, maxit=30, rtol=1e-8, precond=2, block_rows=32):
     """Right-preconditioned GMRES(m), Saad Alg. 9.5 with MGS Arnoldi.  Returns (x, iters, relres)."""
     n = len(rp) - 1
     b = np.asarray(b, dtype=np.float64)

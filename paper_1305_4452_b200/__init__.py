@@ -377,7 +377,7 @@ class Space:
         return out
 
     def gmres(self, row_ptr, col_idx, val, b, x=None, restart=30, maxit=30, rtol=1e-8, precond=PC_BJACOBI_ILU0,
-              block_rows=64, stream=None):
+              block_rows=32, stream=None):
         """Solve J x = b with this space's assembled CSR (iga_gmres: right-preconditioned GMRES,
         block-Jacobi ILU(0)); x (device fp64) is the initial guess (zeros if None) and is
         overwritten.  Returns (x, iterations, true relative residual)."""
@@ -392,7 +392,7 @@ class Space:
         return x, int(it.value), float(rr.value)
 
     def alpha_step(self, phys, U, Udot, row_ptr, col_idx, val, rho_inf, dt, newton_its=2, restart=30, maxit=30,
-                   rtol=0.0, precond=PC_BJACOBI_ILU0, block_rows=64, stream=None):
+                   rtol=0.0, precond=PC_BJACOBI_ILU0, block_rows=32, stream=None):
         """One generalized-alpha step with the fixed Newton / GMRES budget (iga_alpha_step); U and
         Udot (device fp64) advance in place from step n to n+1; val is the Jacobian buffer.
         Returns {"res_norm": [...], "gmres_its": [...], "gmres_relres": [...]} per Newton iterate."""

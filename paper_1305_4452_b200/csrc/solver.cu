@@ -6,7 +6,7 @@
 // on the host.  Preconditioner: block
 // Jacobi with ILU(0) in each block.  Reading A-28: on one GPU "one block per process"
 // would serialise the triangular solves, so the blocks are contiguous runs of `block_rows` rows
-// (default 64): one thread each over packed in-block entries for blocks <= 64 rows, one warp each
+// (default 32): one thread each over packed in-block entries for blocks <= 64 rows, one warp each
 // over the CSR otherwise (the factor and the solves are sequential over a block's rows).  All vector work runs in the kernels below; the host only does the (m+1) x m
 // Hessenberg least-squares update.
 #include <cmath>
@@ -615,7 +615,7 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
                        const iga_krylov *opt, int *iters_out, double *relres_out, cudaStream_t st) {
     const long long n = s->nrows_owned, nnz = s->nnz_owned;
     const int m = std::max(1, opt->restart), maxit = std::max(0, opt->maxit);
-    const int B = opt->block_rows > 0 ? opt->block_rows : 64;
+    const int B = opt->block_rows > 0 ? opt->block_rows : 32;
     if (s->nranks > 1) { set_error("gmres: single-rank in this build"); return IGA_ERR_STATE; }
     // workspace, cached on the space (gm_buf): [0] V[m+1][n], Z[m][n], w[n], dp[n], h[2(m+1)];
     // [1] the preconditioner (packed blocks or the CSR copy of the ILU factor)

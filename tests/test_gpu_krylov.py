@@ -52,7 +52,7 @@ def test_one_iteration_applies_preconditioner(cid, n, precond, B):
     sp = iga.Space.from_workload(w)
     x, it, rr = sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(b), restart=1, maxit=1, rtol=0.0, precond=precond,
                          block_rows=B)
-    xo, ito, rro = krylov.gmres(rp, ci, v, b, restart=1, maxit=1, rtol=0.0, precond=precond, block_rows=B or 64)
+    xo, ito, rro = krylov.gmres(rp, ci, v, b, restart=1, maxit=1, rtol=0.0, precond=precond, block_rows=B or 32)
     assert it == ito == 1
     xg = x.cpu().numpy()
     assert np.max(np.abs(xg - xo)) <= 1e-12 * np.max(np.abs(xo))
@@ -135,7 +135,7 @@ def test_edge_cases(restart, maxit, B, precond):
     x, it, rr = sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(b), x=_dev(x0), restart=restart, maxit=maxit, rtol=0.0,
                          precond=precond, block_rows=B)
     xo, ito, rro = krylov.gmres(rp, ci, v, b, x0=x0, restart=restart, maxit=maxit, rtol=0.0, precond=precond,
-                                block_rows=B or 64)
+                                block_rows=B or 32)
     # past n iterations the Krylov space is exhausted: the host path stops at the (Pythagoras)
     # breakdown h_{j+1} = 0, the oracle's MGS norm stays at rounding level and it keeps iterating
     assert it == ito or (restart > b.size and b.size <= it <= ito)
@@ -153,6 +153,6 @@ def test_ring_and_nsk_systems():
         w, rp, ci, v, b = _system(cid, n)
         sp = iga.Space.from_workload(w)
         x, it, rr = sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(b), restart=30, maxit=30, rtol=0.0)
-        xo, ito, rro = krylov.gmres(rp, ci, v, b, restart=30, maxit=30, rtol=0.0, precond=2, block_rows=64)
+        xo, ito, rro = krylov.gmres(rp, ci, v, b, restart=30, maxit=30, rtol=0.0, precond=2, block_rows=32)
         assert it == ito == 30
         assert np.max(np.abs(x.cpu().numpy() - xo)) <= 1e-8 * np.max(np.abs(xo)), cid

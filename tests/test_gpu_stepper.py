@@ -1,7 +1,7 @@
 """GPU parity of iga_alpha_step (generalized-alpha, eq. (ga) P:697-739,
 with the §5 fixed budget of Newton / GMRES iterations) against the oracle stepper
 (oracle/stepper.py) driving the oracle assembly and the oracle GMRES.  Both run the same
-rho_inf, dt, Newton count and GMRES(30) + block-Jacobi ILU(0) settings.
+rho_inf, dt, Newton count and GMRES(30) + block-Jacobi ILU(0) (32-row blocks, the library default) settings.
 
 Tolerance: each Newton step carries the GMRES parity difference (<= 1e-8 relative, see
 test_gpu_krylov.py) into the update; after 2 steps x 2 Newton iterations U and Udot agree within
@@ -45,7 +45,7 @@ def test_alpha_steps_match_oracle(cid, n, steps, newton):
     def solve(J, R):
         rp, ci, v = J
         x, _, _ = krylov.gmres(np.asarray(rp, np.int64), np.asarray(ci, np.int32), np.asarray(v), R, restart=30,
-                               maxit=30, rtol=0.0, precond=2, block_rows=64)
+                               maxit=30, rtol=0.0, precond=2, block_rows=32)
         return x
 
     U0 = np.array(w.U, dtype=np.float64)

@@ -15,7 +15,7 @@ import workloads   # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--maxit", type=int, default=30)
-ap.add_argument("--block", type=int, default=64)
+ap.add_argument("--block", type=int, default=32)
 ap.add_argument("--precond", type=int, default=2)
 ap.add_argument("--reps", type=int, default=5)
 a = ap.parse_args()
