@@ -27,8 +27,10 @@
  *     with every touched entry required to lie in that pattern.
  *
  * Parity-unpinned pieces (no paper pin): the Cahn-Hilliard mobility and
- * chemical potential (A-10) and the VMS stabilisation (A-14) are readings, guarded only by
- * invariants and finite differences in tests/test_oracle_*.py.
+ * chemical potential (A-10) and the VMS stabilisation (A-14) are readings, guarded by invariants
+ * and finite differences in tests/test_oracle_*.py; the weak forms around them are pinned to the
+ * paper's strong forms (test_oracle_ch_strong.py, test_oracle_vms_consistency.py, and the NSK
+ * strong-form test in test_oracle_nsk.py).
  */
 #include <math.h>
 #include <stdint.h>
