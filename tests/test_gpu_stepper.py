@@ -91,3 +91,27 @@ def test_full_size_config3_step():
     assert float((U - rhs).abs().max()) <= 1e-12 * float(U.abs().max())
     assert st["res_norm"][1] < 0.1 * st["res_norm"][0]
     assert all(i == 30 for i in st["gmres_its"]) and max(st["gmres_relres"]) < 1e-2
+
+
+def test_alpha_step_rejects_bad_options_and_multirank():
+    iga = _gpu()
+    w = workloads.make(3, n=6)
+    sp = iga.Space.from_workload(w)
+    rp, ci = sp.csr_pattern()
+    val = torch.empty(ci.numel(), dtype=torch.float64, device=rp.device)
+    ph = iga.make_phys(w.phys, w.params)
+    U, Ud = _dev(w.U), _dev(w.Udot)
+    for kw in ({"rho_inf": 1.5, "dt": 1e-6}, {"rho_inf": 0.5, "dt": 0.0}, {"rho_inf": 0.5, "dt": 1e-6, "newton_its": 9},
+               {"rho_inf": 0.5, "dt": 1e-6, "precond": 3}):
+        with pytest.raises(iga.IgaError) as ei:
+            sp.alpha_step(ph, U, Ud, rp, ci, val, **kw)
+        assert ei.value.code == 1
+    # a rank of a multi-rank decomposition: the solver is single-rank in this build
+    spaces = [iga.Space.from_workload(w, dist={"rank": r, "nranks": 2, "procs": [2, 1],
+                                               "transport": iga.XPORT_LOCAL}) for r in range(2)]
+    rp2, ci2 = spaces[0].csr_pattern()
+    b = torch.zeros(spaces[0].nrows, dtype=torch.float64, device=rp.device)
+    v2 = torch.zeros(ci2.numel(), dtype=torch.float64, device=rp.device)
+    with pytest.raises(iga.IgaError) as ei:
+        spaces[0].gmres(rp2, ci2, v2, b)
+    assert ei.value.code == 9
