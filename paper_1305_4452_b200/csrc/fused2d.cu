@@ -268,7 +268,8 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             const double *tb1 = tb + (size_t)(1 * TL::TE1 + le1) * NQ1 * 3 * NP1;
             // (0) the point's homogeneous sums (w, w x, w u, w udot and their kinds), sum factorised
             //     over the element's functions by the lane group: stage 1, lane (a0, q1):
-            //     S1[a0][q1][f][o1] = sum_a1 T1(q1, o1, a1) f(a0, a1), into the group scratch;
+            //     S1[f][o1][a0][q1] = sum_a1 T1(q1, o1, a1) f(a0, a1), into the group scratch (lane-
+            //     contiguous: no bank conflicts);
             //     stage 2, lane (q0, q1): S[f][o0][o1] = sum_a0 T0(q0, o0, a0) S1[a0][q1][f][o1]
             //     (2 (p+1)^3 FMA per field and order pair instead of (p+1)^4 per point)
             constexpr int NFW = MODE == MODE_NURBS ? 3 : 0;               // w, w x0, w x1
@@ -310,7 +311,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                                 double acc = 0.0;
 #pragma unroll
                                 for (int a1 = 0; a1 < NP1; a1++) acc += t1[a1] * fv[f][a1];
-                                gs[((a0 * NQ1 + q1) * NF + f) * 3 + o1] = acc;
+                                gs[((f * 3 + o1) * NP1 + a0) * NQ1 + q1] = acc;
                             }
                         }
                     });
@@ -329,7 +330,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                                     double acc = 0.0;
 #pragma unroll
                                     for (int a0 = 0; a0 < NP1; a0++)
-                                        acc += tb0[(q0 * 3 + o0) * NP1 + a0] * gs[((a0 * NQ1 + q1) * NF + f) * 3 + o1];
+                                        acc += tb0[(q0 * 3 + o0) * NP1 + a0] * gs[((f * 3 + o1) * NP1 + a0) * NQ1 + q1];
                                     S[f][o0][o1] = acc;
                                 }
                             }
