@@ -171,7 +171,10 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     double *hpb = qxb + 2 * TL::TE1 * NQ1;              // [2][TE]
     double *scr = hpb + 2 * TL::TE1;                    // [NGRP][SCR][NQ]
     // scatter metadata of the tile's rows (computed once per node, not per entry)
-    long long *rowOff = reinterpret_cast<long long *>(scr + (size_t)NGRP * SCR * NQ);   // [NBN] CSR row start - val
+    // group scratch stride: p = 3 pads one double so the two groups of a warp (whose lanes all
+    // read their own group's coefficient at the same offset) hit different banks
+    constexpr int GSTR = SCR * NQ + (P == 3 ? 1 : 0);
+    long long *rowOff = reinterpret_cast<long long *>(scr + (size_t)NGRP * GSTR);   // [NBN] CSR row start - val
     long long *fIdx = rowOff + NBN;                         // [NBN] residual entry of the node
     int *rowW1 = reinterpret_cast<int *>(fIdx + NBN);       // [NBN] Alg. 3 width along axis 1
     int *pd0 = rowW1 + NBN;                                 // [NB0][W2] position of column g0+delta in row g0
@@ -181,7 +184,7 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     const int grp_in_warp = lane / G, t = lane % G;
     const bool lane_ok = grp_in_warp < GPW;
     const int grp = warp * GPW + (lane_ok ? grp_in_warp : 0);
-    double *gs = scr + (size_t)grp * SCR * NQ;
+    double *gs = scr + (size_t)grp * GSTR;
     const AxisDev &A0 = s.ax[0], &A1 = s.ax[1];
     int errbits = 0;
 
@@ -481,7 +484,7 @@ static size_t fused2d_smem(bool jac) {
     constexpr int NGRP = TL::NWARP * (32 / (NP1 * NP1));
     const int NBN = TL::NB0 * TL::NB1;
     size_t n = 5 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
-               + 2 * TL::TE1 + (size_t)NGRP * ((jac ? L::NE : 0) + L::NR) * NQ;
+               + 2 * TL::TE1 + (size_t)NGRP * (((jac ? L::NE : 0) + L::NR) * NQ + (P == 3 ? 1 : 0));
     // scatter metadata: rowOff, fIdx (8 B) + rowW1 (4 B) per node, posd tables
     return n * sizeof(double) + (size_t)NBN * 20 + (size_t)(TL::NB0 + TL::NB1) * (2 * P + 1) * sizeof(int);
 }
