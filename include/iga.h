@@ -214,8 +214,13 @@ iga_status iga_basis_eval(iga_space s, int order, double *out, void *stream);
  * or nnz doubles for blocks > 64 rows) is allocated on first use, kept with the space for later
  * calls and freed by iga_space_destroy; the call synchronises `stream`.
  * iters (total iterations) / relres (TRUE ||b - A x|| / ||b|| of the returned x) may be NULL.
- * Single-rank spaces only (IGA_ERR_STATE otherwise); IGA_ERR_NOMEM if the workspace does not
- * fit. */
+ * Multi-rank spaces (box decomposition): with IGA_XPORT_NCCL every rank calls iga_gmres with
+ * its owned rows (global column indices, as iga_csr_pattern returns them); in-process
+ * (IGA_XPORT_LOCAL) ranks call iga_gmres_group.  The distributed solve exchanges a ghost layer
+ * of width p of x per SpMV, all-reduces the Gram-Schmidt dots, and factors block-Jacobi ILU(0)
+ * on each rank's owned-owned block (the paper's "one block per process", cut into block_rows
+ * runs); it supports the fixed budget only (rtol = 0, IGA_ERR_PARAM otherwise) and restart <= 62.
+ * IGA_ERR_NOMEM if the workspace does not fit. */
 typedef struct {
     int restart;    /* m, Krylov dimension per cycle (paper: 30) */
     int maxit;      /* total iteration cap (paper: 30 per Newton step) */
@@ -226,6 +231,12 @@ typedef struct {
 iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
                      const double *b, double *x, const iga_krylov *opt, int *iters, double *relres,
                      void *stream);
+/* All n in-process ranks (IGA_XPORT_LOCAL spaces, rank k = spaces[k]) solve together on one
+ * stream; per-rank arrays as for iga_gmres; iters / relres are global. */
+iga_status iga_gmres_group(int n, const iga_space *spaces, const int64_t *const *row_ptr,
+                           const int32_t *const *col_idx, const double *const *val,
+                           const double *const *b, double *const *x, const iga_krylov *opt,
+                           int *iters, double *relres, void *stream);
 
 /* One generalized-alpha time step with a fixed-budget Newton loop -- eq. (ga) of P:697-709 with
  * the rho_inf parametrisation of P:719-723 (am = (3 - rho)/(2 (1 + rho)), af = 1/(1 + rho),

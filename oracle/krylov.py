@@ -29,20 +29,37 @@ import math
 import numpy as np
 
 
+def _block_of(n, block_rows):
+    """[r0, r1) of every row's block: block_rows = int (runs of that many rows), None (one block)
+    or a list of block start rows (explicit partition, e.g. per-rank runs of a distributed solve)."""
+    lo = np.zeros(n, np.int64)
+    hi = np.zeros(n, np.int64)
+    if block_rows is None or (np.isscalar(block_rows) and not block_rows):
+        starts = [0]
+    elif np.isscalar(block_rows):
+        starts = list(range(0, n, int(block_rows)))
+    else:
+        starts = sorted(int(v) for v in block_rows)
+    starts = [v for v in starts if v < n] + [n]
+    for k in range(len(starts) - 1):
+        lo[starts[k]:starts[k + 1]] = starts[k]
+        hi[starts[k]:starts[k + 1]] = starts[k + 1]
+    return lo, hi
+
+
 def ilu0(rp, ci, val, block_rows=None):
     """Block-Jacobi ILU(0) factors of the CSR matrix (rp, ci, val) with sorted columns: returns
     `lu` on the same pattern (unit-lower L strictly below the diagonal, U on and above), only
-    the entries inside each diagonal block of `block_rows` rows are meaningful."""
+    the entries inside each diagonal block (see _block_of) are meaningful."""
     n = len(rp) - 1
-    B = n if not block_rows else int(block_rows)
+    blo, bhi = _block_of(n, block_rows)
     lu = np.array(val, dtype=np.float64, copy=True)
     pos = [dict() for _ in range(n)]               # column -> position, per row
     for i in range(n):
         for p in range(rp[i], rp[i + 1]):
             pos[i][int(ci[p])] = p
     for i in range(n):
-        r0 = (i // B) * B
-        r1 = min(n, r0 + B)
+        r0, r1 = int(blo[i]), int(bhi[i])
         for p in range(rp[i], rp[i + 1]):
             k = int(ci[p])
             if k >= i:
@@ -63,10 +80,10 @@ def ilu0(rp, ci, val, block_rows=None):
 def ilu0_solve(rp, ci, lu, r, block_rows=None):
     """z = (L U)^{-1} r blockwise: forward substitution with unit L, back substitution with U."""
     n = len(rp) - 1
-    B = n if not block_rows else int(block_rows)
+    blo, bhi = _block_of(n, block_rows)
     z = np.zeros(n)
-    for r0 in range(0, n, B):
-        r1 = min(n, r0 + B)
+    for r0 in sorted(set(blo.tolist())):
+        r1 = int(bhi[r0])
         for i in range(r0, r1):
             s = r[i]
             for p in range(rp[i], rp[i + 1]):

@@ -78,7 +78,7 @@ EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_p
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
            "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
            "iga_microbench", "iga_space_set_option", "iga_form_jacobian_group", "iga_form_residual_group",
-           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step"]
+           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group"]
 
 
 def lib():
@@ -119,13 +119,15 @@ def lib():
         L.iga_nccl_unique_id.argtypes = [C.POINTER(C.c_ubyte * 128)]
         L.iga_basis_eval.argtypes = [vp, C.c_int, vp, vp]
         L.iga_gmres.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
+        L.iga_gmres_group.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                      C.POINTER(vp), C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
         L.iga_alpha_step.argtypes = [vp, C.POINTER(_Phys), C.POINTER(_Alpha), vp, vp, vp, vp, vp, C.POINTER(_StepStats), vp]
         L.iga_last_error.restype = C.c_char_p
         L.iga_version.restype = C.c_char_p
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
                   "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
                   "iga_profile_reset", "iga_form_jacobian_group", "iga_form_residual_group", "iga_dist_plan",
-                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step"):
+                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -258,6 +260,23 @@ def form_jacobian_group(spaces, phys, a, b, Us, Udots=None, vals=None, Fs=None, 
                                          _pp(Udots) if Udots is not None else None, _pp(vals),
                                          _pp(Fs) if Fs is not None else None, _stream(stream)))
     return vals, Fs
+
+
+def gmres_group(spaces, row_ptrs, col_idxs, vals, bs, xs=None, restart=30, maxit=30, precond=PC_BJACOBI_ILU0,
+                block_rows=32, stream=None):
+    """Distributed fixed-budget GMRES of in-process ranks (iga_gmres_group); returns (xs, iters, relres)."""
+    import torch
+    n = len(spaces)
+    if xs is None:
+        xs = [torch.zeros_like(bb) for bb in bs]
+    arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() for t in ts])
+    hs = (C.c_void_p * n)(*[sp.h.value for sp in spaces])
+    opt = _Krylov(int(restart), int(maxit), 0.0, int(precond), int(block_rows))
+    it = C.c_int(0)
+    rr = C.c_double(0.0)
+    _check(lib().iga_gmres_group(n, hs, arr(row_ptrs), arr(col_idxs), arr(vals), arr(bs), arr(xs), C.byref(opt),
+                                 C.byref(it), C.byref(rr), _stream(stream)))
+    return xs, int(it.value), float(rr.value)
 
 
 def form_residual_group(spaces, phys, Us, Udots=None, Fs=None, stream=None):

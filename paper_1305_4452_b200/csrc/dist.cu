@@ -37,6 +37,7 @@ struct NcclApi {
     int (*GroupEnd)() = nullptr;
     int (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     int (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    int (*AllReduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
 };
 constexpr int NCCL_FLOAT64 = 8;
@@ -57,6 +58,7 @@ static NcclApi &nccl() {
     api.Send = (int (*)(const void *, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclSend");
     api.Recv = (int (*)(void *, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclRecv");
     api.GetErrorString = (const char *(*)(int))dlsym(h, "ncclGetErrorString");
+    api.AllReduce = (int (*)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllReduce");
     api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart && api.GroupEnd && api.Send &&
              api.Recv;
     return api;
@@ -646,6 +648,29 @@ iga_status dist_plan_host(const iga_space_desc *d, const iga_dist *dist, int64_t
     };
     put(up, send, nsend);
     put(down, recv, nrecv);
+    return IGA_OK;
+}
+
+// ---- collectives for the distributed Krylov solve (solver.cu) ---------------------------------
+// sum-all-reduce of n doubles in place on `st` (NCCL transport)
+iga_status dist_allreduce_sum(iga_space_s *s, double *buf, size_t n, cudaStream_t st) {
+    NcclApi &api = nccl();
+    if (!s->dist || !s->dist->comm || !api.ok || !api.AllReduce) { set_error("allreduce: no NCCL communicator"); return IGA_ERR_COMM; }
+    const int r = api.AllReduce(buf, buf, n, NCCL_FLOAT64, 0 /* ncclSum */, s->dist->comm, st);
+    if (r) { set_error("ncclAllReduce failed"); return IGA_ERR_COMM; }
+    return IGA_OK;
+}
+
+// grouped point-to-point exchange: sends in the given order, receives in the given order
+iga_status dist_sendrecv(iga_space_s *s, int ns, const int *speer, const double *const *sbuf, const long long *scount,
+                         int nr, const int *rpeer, double *const *rbuf, const long long *rcount, cudaStream_t st) {
+    NcclApi &api = nccl();
+    if (!s->dist || !s->dist->comm || !api.ok) { set_error("sendrecv: no NCCL communicator"); return IGA_ERR_COMM; }
+    int r = api.GroupStart();
+    for (int k = 0; k < ns && !r; k++) r = api.Send(sbuf[k], (size_t)scount[k], NCCL_FLOAT64, speer[k], s->dist->comm, st);
+    for (int k = 0; k < nr && !r; k++) r = api.Recv(rbuf[k], (size_t)rcount[k], NCCL_FLOAT64, rpeer[k], s->dist->comm, st);
+    const int r2 = api.GroupEnd();
+    if (r || r2) { set_error("NCCL send/recv failed"); return IGA_ERR_COMM; }
     return IGA_OK;
 }
 

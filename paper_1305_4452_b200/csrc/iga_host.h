@@ -110,6 +110,12 @@ iga_status form_one(iga_space_s *s, const iga_phys *phys, double a, double b, co
                     double *val, double *F, cudaStream_t st);                                         // space.cu
 // dist.cu
 iga_status dist_setup(iga_space_s *s, const iga_dist *dist);
+iga_status dist_allreduce_sum(iga_space_s *s, double *buf, size_t n, cudaStream_t st);
+iga_status dist_sendrecv(iga_space_s *s, int ns, const int *speer, const double *const *sbuf, const long long *scount,
+                         int nr, const int *rpeer, double *const *rbuf, const long long *rcount, cudaStream_t st);
+iga_status gmres_group(int nr, iga_space_s *const *sp, const int64_t *const *rp, const int32_t *const *ci,
+                       const double *const *a, const double *const *b, double *const *x, const iga_krylov *opt,
+                       int *iters, double *relres, cudaStream_t st);                              // solver.cu
 void dist_destroy(iga_space_s *s);
 iga_status dist_form(iga_space_s **sp, int n, const iga_phys *ph, double a, double b, const double *const *U,
                      const double *const *Ud, double *const *val, double *const *F, cudaStream_t st);

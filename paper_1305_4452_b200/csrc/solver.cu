@@ -9,9 +9,12 @@
 // (default 32): one thread each over packed in-block entries for blocks <= 64 rows, one warp each
 // over the CSR otherwise (the factor and the solves are sequential over a block's rows).  All vector work runs in the kernels below; the host only does the (m+1) x m
 // Hessenberg least-squares update.
+#include <array>
 #include <cmath>
 #include <cstddef>
 #include <vector>
+
+#include <cub/device/device_scan.cuh>
 
 #include "iga_host.h"
 
@@ -616,7 +619,13 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
     const long long n = s->nrows_owned, nnz = s->nnz_owned;
     const int m = std::max(1, opt->restart), maxit = std::max(0, opt->maxit);
     const int B = opt->block_rows > 0 ? opt->block_rows : 32;
-    if (s->nranks > 1) { set_error("gmres: single-rank in this build"); return IGA_ERR_STATE; }
+    if (s->nranks > 1) {
+        if (!s->dist || dist_transport(s->dist) != IGA_XPORT_NCCL) {
+            set_error("gmres: in-process (IGA_XPORT_LOCAL) ranks solve through iga_gmres_group");
+            return IGA_ERR_STATE;
+        }
+        return gmres_group(1, &s, &rp, &ci, &a, &b, &x, opt, iters_out, relres_out, st);
+    }
     // workspace, cached on the space (gm_buf): [0] V[m+1][n], Z[m][n], w[n], dp[n], h[2(m+1)];
     // [1] the preconditioner (packed blocks or the CSR copy of the ILU factor)
     auto ensure = [&](int slot, size_t bytes) { return ws_ensure(s, slot, bytes); };
@@ -926,6 +935,467 @@ iga_status alpha_step(iga_space_s *s, const iga_phys *phys, const iga_alpha *opt
     s->last_launches = launches;
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) { set_error(std::string("alpha_step: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return IGA_OK;
+}
+
+
+// ============================================================================================
+// Distributed GMRES over the box decomposition (SURVEY §8(e) x §8(f) rank 2): every rank holds
+// its owned rows; the SpMV needs x on a ghost layer of width p around the owned box on the
+// partitioned axes (the Alg. 3 stencil reaches p functions either way), exchanged per SpMV as
+// box messages (one per neighbour offset in {-1,0,1}^d); the Gram-Schmidt dots are all-reduced
+// (NCCL: ncclAllReduce on the stream; in-process ranks: a device sum over the ranks' buffers);
+// block Jacobi ILU(0) runs on each rank's owned-owned block only -- the paper's "one block per
+// process", cut into runs of block_rows rows as on one rank (reading A-28).  Fixed
+// iteration budget only (rtol = 0, the §5 protocol): the Arnoldi control runs on the device.
+// ============================================================================================
+struct DPlan {
+    int dim, m;
+    int E[3], G[3], N[3], lo[3], nu[3], part[3];
+};
+
+__device__ __forceinline__ void dplan_coords(const DPlan &P, long long node, int g[3]) {
+    long long r = node;
+    for (int a = P.dim - 1; a >= 0; a--) { g[a] = (int)(r % P.nu[a]); r /= P.nu[a]; }
+    for (int a = P.dim; a < 3; a++) g[a] = 0;
+}
+
+// column (global dof) -> ext-box index; *own = owned-box local index or -1
+__device__ __forceinline__ long long dplan_ext(const DPlan &P, int col, long long *own) {
+    const long long node = col / P.m;
+    const int comp = col - (int)node * P.m;
+    int g[3];
+    dplan_coords(P, node, g);
+    long long e = 0, o = 0;
+    bool owned = true;
+    for (int a = 0; a < 3; a++) {
+        int l;
+        if (a >= P.dim) l = 0;
+        else if (P.part[a]) {
+            int d = g[a] - P.lo[a];
+            if (d < -P.G[a]) d += P.nu[a];
+            else if (d >= P.N[a] + P.G[a]) d -= P.nu[a];
+            l = d + P.G[a];
+            owned = owned && d >= 0 && d < P.N[a];
+            o = o * P.N[a] + d;
+        } else {
+            l = g[a];
+            o = o * P.N[a] + g[a];
+        }
+        e = e * P.E[a] + l;
+    }
+    *own = owned ? o * P.m + comp : -1;
+    return e * P.m + comp;
+}
+
+__global__ void k_dplan_lci(DPlan P, long long nnz, const int32_t *__restrict__ ci, int32_t *__restrict__ lci) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
+        long long own;
+        lci[p] = (int32_t)dplan_ext(P, ci[p], &own);
+    }
+}
+
+__global__ void k_dplan_own_count(DPlan P, long long n, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                  int64_t *__restrict__ cnt) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long c = 0;
+    for (long long p = rp[i]; p < rp[i + 1]; p++) {
+        long long own;
+        dplan_ext(P, ci[p], &own);
+        c += own >= 0;
+    }
+    cnt[i + 1] = c;
+    if (i == 0) cnt[0] = 0;
+}
+
+__global__ void k_dplan_own_fill(DPlan P, long long n, const int64_t *__restrict__ rp, const int32_t *__restrict__ ci,
+                                 const double *__restrict__ a, const int64_t *__restrict__ orp, int32_t *__restrict__ oci,
+                                 double *__restrict__ oval) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long q = orp[i];
+    for (long long p = rp[i]; p < rp[i + 1]; p++) {
+        long long own;
+        dplan_ext(P, ci[p], &own);
+        if (own >= 0) { oci[q] = (int32_t)own; oval[q] = a[p]; q++; }
+    }
+}
+
+// owned vector (owned-box C order, dof innermost) <-> ext box interior
+__global__ void k_dplan_scatter(DPlan P, long long n, const double *__restrict__ x, double *__restrict__ xe) {
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+        long long node = r / P.m;
+        const int comp = (int)(r - node * P.m);
+        int o[3] = {0, 0, 0};
+        for (int a = P.dim - 1; a >= 0; a--) { o[a] = (int)(node % P.N[a]); node /= P.N[a]; }
+        long long e = 0;
+        for (int a = 0; a < 3; a++) e = e * P.E[a] + (a < P.dim ? o[a] + (P.part[a] ? P.G[a] : 0) : 0);
+        xe[e * P.m + comp] = x[r];
+    }
+}
+
+// box [lo, lo+bn) of the ext vector <-> contiguous buffer (node C order, dof innermost)
+struct DBox { int lo[3], n[3]; };
+__global__ void k_dplan_box(DPlan P, DBox B, double *__restrict__ xe, double *__restrict__ buf, int unpack) {
+    const long long cnt = (long long)B.n[0] * B.n[1] * B.n[2] * P.m;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += (long long)gridDim.x * blockDim.x) {
+        long long node = k / P.m;
+        const int comp = (int)(k - node * P.m);
+        const int b2 = (int)(node % B.n[2]);
+        node /= B.n[2];
+        const int b1 = (int)(node % B.n[1]);
+        const int b0 = (int)(node / B.n[1]);
+        const long long e = (((long long)(B.lo[0] + b0) * P.E[1] + (B.lo[1] + b1)) * P.E[2] + (B.lo[2] + b2)) * P.m + comp;
+        if (unpack) xe[e] = buf[k];
+        else buf[k] = xe[e];
+    }
+}
+
+// in-process ranks: out[r][i] = sum_q in[q][i] for every rank r
+__global__ void k_sum_ranks(int nr, double *const *bufs, int cnt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    double s = 0.0;
+    for (int r = 0; r < nr; r++) s += bufs[r][i];
+    for (int r = 0; r < nr; r++) bufs[r][i] = s;
+}
+
+struct DMsg {
+    int peer, o[3];
+    DBox box;
+    long long off, cnt;
+};
+
+struct DRank {
+    iga_space_s *s = nullptr;
+    const int64_t *rp = nullptr;
+    const int32_t *ci = nullptr;
+    const double *a = nullptr, *b = nullptr;
+    double *x = nullptr;
+    long long n = 0, nnz = 0, next = 0, onnz = 0;
+    DPlan P{};
+    std::vector<DMsg> snd, rcv;
+    long long sn = 0, rn = 0;
+    int32_t *lci = nullptr, *oci = nullptr;
+    int64_t *orp = nullptr, *dp = nullptr;
+    double *oval = nullptr, *xe = nullptr, *sbuf = nullptr, *rbuf = nullptr, *V = nullptr, *Z = nullptr, *w = nullptr,
+           *dh = nullptr, *lu = nullptr, *Lv = nullptr, *Uv = nullptr, *Dd = nullptr;
+    uint8_t *Lc = nullptr, *Uc = nullptr;
+    int W = 0;
+    bool ell = false;
+    std::vector<void *> mem;
+    template <class T> T *alloc(size_t count) {
+        void *p = nullptr;
+        if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        mem.push_back(p);
+        return (T *)p;
+    }
+    ~DRank() { for (void *p : mem) cudaFree(p); }
+};
+
+static void dplan_build(DRank &R) {
+    iga_space_s *s = R.s;
+    DPlan &P = R.P;
+    P.dim = s->dim;
+    P.m = s->dof;
+    for (int a = 0; a < 3; a++) {
+        P.nu[a] = a < s->dim ? s->nu[a] : 1;
+        P.part[a] = a < s->dim && s->procs[a] > 1;
+        P.lo[a] = a < s->dim ? s->own_lo[a] : 0;
+        P.N[a] = a < s->dim ? s->own_hi[a] - s->own_lo[a] : 1;
+        P.G[a] = P.part[a] ? s->p[a] : 0;
+        P.E[a] = P.part[a] ? P.N[a] + 2 * P.G[a] : P.N[a];
+    }
+    R.next = (long long)P.E[0] * P.E[1] * P.E[2] * P.m;
+    // messages: offsets in {-1,0,1}^dim on the partitioned axes, sends ascending, receives descending
+    std::vector<std::array<int, 3>> offs;
+    for (int o0 = -1; o0 <= 1; o0++)
+        for (int o1 = -1; o1 <= 1; o1++)
+            for (int o2 = -1; o2 <= 1; o2++) {
+                const int o[3] = {o0, o1, o2};
+                bool ok = !(o0 == 0 && o1 == 0 && o2 == 0);
+                for (int a = 0; a < 3 && ok; a++)
+                    if (o[a] && !P.part[a]) ok = false;
+                if (ok) offs.push_back({o0, o1, o2});
+            }
+    R.snd.clear();
+    R.rcv.clear();
+    R.sn = R.rn = 0;
+    auto peer_of = [&](const int o[3], int &peer) {
+        int c[3];
+        for (int a = 0; a < 3; a++) {
+            c[a] = s->rcoord[a] + o[a];
+            if (c[a] < 0 || c[a] >= s->procs[a]) {
+                if (!(a < s->dim && s->periodic[a])) return false;
+                c[a] = (c[a] + s->procs[a]) % s->procs[a];
+            }
+        }
+        peer = (c[0] * s->procs[1] + c[1]) * s->procs[2] + c[2];
+        return true;
+    };
+    for (size_t k = 0; k < offs.size(); k++) {
+        const int *o = offs[k].data();
+        DMsg M{};
+        if (!peer_of(o, M.peer)) continue;
+        for (int a = 0; a < 3; a++) {
+            M.o[a] = o[a];
+            // my owned slab on side o (what the neighbour at c+o keeps as its ghost on side -o)
+            M.box.lo[a] = o[a] > 0 ? P.G[a] + P.N[a] - P.G[a] : P.G[a];
+            M.box.n[a] = o[a] ? P.G[a] : P.N[a];
+        }
+        M.cnt = (long long)M.box.n[0] * M.box.n[1] * M.box.n[2] * P.m;
+        M.off = R.sn;
+        R.sn += M.cnt;
+        R.snd.push_back(M);
+    }
+    for (size_t kk = offs.size(); kk-- > 0;) {
+        const int *o = offs[kk].data();
+        DMsg M{};
+        if (!peer_of(o, M.peer)) continue;
+        for (int a = 0; a < 3; a++) {
+            M.o[a] = o[a];
+            // my ghost layer on side o
+            M.box.lo[a] = o[a] < 0 ? 0 : o[a] > 0 ? P.G[a] + P.N[a] : P.G[a];
+            M.box.n[a] = o[a] ? P.G[a] : P.N[a];
+        }
+        M.cnt = (long long)M.box.n[0] * M.box.n[1] * M.box.n[2] * P.m;
+        M.off = R.rn;
+        R.rn += M.cnt;
+        R.rcv.push_back(M);
+    }
+}
+
+iga_status gmres_group(int nr, iga_space_s *const *sp, const int64_t *const *rp, const int32_t *const *ci,
+                       const double *const *a, const double *const *b, double *const *x, const iga_krylov *opt,
+                       int *iters_out, double *relres_out, cudaStream_t st) {
+    if (opt->rtol != 0.0) { set_error("distributed gmres: fixed iteration budget only (rtol = 0)"); return IGA_ERR_PARAM; }
+    const int m = std::max(1, opt->restart), maxit = std::max(0, opt->maxit);
+    if (m > 62) { set_error("distributed gmres: restart <= 62"); return IGA_ERR_PARAM; }
+    const int B = opt->block_rows > 0 ? opt->block_rows : 32;
+    const bool local = nr > 1 || sp[0]->nranks == 1 || dist_transport(sp[0]->dist) == IGA_XPORT_LOCAL;
+    if (!local && nr != 1) { set_error("distributed gmres: one NCCL rank per process"); return IGA_ERR_PARAM; }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, sp[0]->device);
+    std::vector<DRank> R(nr);
+    const ArnLayout Lo{m};
+    // ---- setup ----
+    for (int r = 0; r < nr; r++) {
+        DRank &D = R[r];
+        D.s = sp[r];
+        D.rp = rp[r]; D.ci = ci[r]; D.a = a[r]; D.b = b[r]; D.x = x[r];
+        D.n = D.s->nrows_owned;
+        D.nnz = D.s->nnz_owned;
+        dplan_build(D);
+        D.lci = D.alloc<int32_t>(D.nnz);
+        D.orp = D.alloc<int64_t>(D.n + 1);
+        D.dp = D.alloc<int64_t>(D.n);
+        D.xe = D.alloc<double>(D.next);
+        D.sbuf = D.alloc<double>(D.sn);
+        D.rbuf = D.alloc<double>(D.rn);
+        D.V = D.alloc<double>((size_t)(m + 1) * D.n);
+        D.Z = D.alloc<double>((size_t)m * D.n);
+        D.w = D.alloc<double>(D.n);
+        D.dh = D.alloc<double>(Lo.total());
+        if (!D.lci || !D.orp || !D.dp || !D.xe || !D.sbuf || !D.rbuf || !D.V || !D.Z || !D.w || !D.dh) {
+            set_error("distributed gmres workspace");
+            return IGA_ERR_NOMEM;
+        }
+        const unsigned gn = (unsigned)std::max<long long>(1, (D.n + 255) / 256);
+        k_dplan_lci<<<(unsigned)std::min<long long>((D.nnz + 255) / 256, (long long)nsm * 16), 256, 0, st>>>(D.P, D.nnz, D.ci, D.lci);
+        k_dplan_own_count<<<gn, 256, 0, st>>>(D.P, D.n, D.rp, D.ci, D.orp);
+        size_t tmp = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, tmp, D.orp, D.orp, (int)(D.n + 1), st);
+        void *tbuf = D.alloc<char>(tmp);
+        cub::DeviceScan::InclusiveSum(tbuf, tmp, D.orp, D.orp, (int)(D.n + 1), st);
+        cudaMemcpyAsync(&D.onnz, D.orp + D.n, sizeof(long long), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        D.oci = D.alloc<int32_t>(D.onnz);
+        D.oval = D.alloc<double>(D.onnz);
+        if (!D.oci || !D.oval) { set_error("distributed gmres workspace"); return IGA_ERR_NOMEM; }
+        k_dplan_own_fill<<<gn, 256, 0, st>>>(D.P, D.n, D.rp, D.ci, D.a, D.orp, D.oci, D.oval);
+        k_diagpos<<<gn, 256, 0, st>>>(D.n, D.orp, D.oci, D.dp);
+        // block-Jacobi ILU(0) of the owned-owned block (as gmres_solve)
+        const long long nblk = (D.n + B - 1) / B;
+        if (opt->precond == 2) {
+            int wm[2] = {0, 0};
+            cudaMemsetAsync(D.dh, 0, 2 * sizeof(int), st);
+            k_ell_count<<<gn, 256, 0, st>>>(D.n, B, D.orp, D.oci, D.dp, (int *)D.dh);
+            cudaMemcpyAsync(wm, D.dh, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            const int wmax = std::max(wm[0], wm[1]);
+            if (B <= TPB_MAXB && wmax <= TPB_MAXW) {
+                D.W = wmax <= 2 ? 2 : wmax <= 4 ? 4 : wmax <= 8 ? 8 : 16;
+                const size_t rows = (size_t)nblk * B;
+                D.Lv = D.alloc<double>(rows * D.W); D.Uv = D.alloc<double>(rows * D.W); D.Dd = D.alloc<double>(rows);
+                D.Lc = D.alloc<uint8_t>(rows * D.W); D.Uc = D.alloc<uint8_t>(rows * D.W);
+                if (!D.Lv || !D.Uv || !D.Dd || !D.Lc || !D.Uc) { set_error("distributed gmres workspace"); return IGA_ERR_NOMEM; }
+                k_ell_pack<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(D.n, B, nblk, D.orp, D.oci, D.dp, D.oval, D.W, D.W,
+                                                                            D.Lv, D.Lc, D.Uv, D.Uc, D.Dd);
+                k_ell_ilu0<<<(unsigned)((nblk + 63) / 64), 64, 0, st>>>(nblk, B, D.W, D.W, D.Lv, D.Lc, D.Uv, D.Uc, D.Dd);
+                D.ell = true;
+            } else {
+                D.lu = D.alloc<double>(D.onnz);
+                if (!D.lu) { set_error("distributed gmres workspace"); return IGA_ERR_NOMEM; }
+                cudaMemcpyAsync(D.lu, D.oval, sizeof(double) * (size_t)D.onnz, cudaMemcpyDeviceToDevice, st);
+                k_ilu0<<<(unsigned)(((nblk * 32) + 127) / 128), 128, 0, st>>>(D.n, B, D.orp, D.oci, D.dp, D.lu);
+            }
+        }
+        cudaMemsetAsync(D.xe, 0, sizeof(double) * (size_t)D.next, st);
+    }
+    // pointer table for the in-process all-reduce
+    double **dptrs = nullptr;
+    std::vector<double *> hptrs(nr);
+    for (int r = 0; r < nr; r++) hptrs[r] = R[r].dh;
+    if (cudaMalloc(&dptrs, sizeof(double *) * nr) != cudaSuccess) { cudaGetLastError(); set_error("gmres ptrs"); return IGA_ERR_NOMEM; }
+    R[0].mem.push_back(dptrs);
+    cudaMemcpyAsync(dptrs, hptrs.data(), sizeof(double *) * nr, cudaMemcpyHostToDevice, st);
+    auto allreduce = [&](int cnt) -> iga_status {
+        if (local) {
+            if (nr > 1) k_sum_ranks<<<(cnt + 63) / 64, 64, 0, st>>>(nr, dptrs, cnt);
+            return IGA_OK;
+        }
+        return dist_allreduce_sum(R[0].s, R[0].dh, (size_t)cnt, st);
+    };
+    // ghost exchange of the ext vectors (after the owned interiors are current)
+    auto exchange = [&]() -> iga_status {
+        for (int r = 0; r < nr; r++)
+            for (const DMsg &M : R[r].snd)
+                k_dplan_box<<<(unsigned)std::max<long long>(1, std::min<long long>((M.cnt + 255) / 256, (long long)nsm * 4)), 256, 0, st>>>(
+                    R[r].P, M.box, R[r].xe, R[r].sbuf + M.off, 0);
+        if (local) {
+            // rank r's receive for offset o from peer q = the send of q for offset -o to r
+            std::vector<std::vector<int>> used(nr);
+            for (int r = 0; r < nr; r++) used[r].assign(R[r].snd.size(), 0);
+            for (int r = 0; r < nr; r++)
+                for (const DMsg &M : R[r].rcv) {
+                    const DRank &Q = R[M.peer];
+                    int found = -1;
+                    for (size_t k = 0; k < Q.snd.size(); k++) {
+                        const DMsg &S = Q.snd[k];
+                        if (S.peer == r && S.o[0] == -M.o[0] && S.o[1] == -M.o[1] && S.o[2] == -M.o[2]) { found = (int)k; break; }
+                    }
+                    if (found < 0 || Q.snd[found].cnt != M.cnt) { set_error("distributed gmres: inconsistent ghost plan"); return IGA_ERR_STATE; }
+                    cudaMemcpyAsync(R[r].rbuf + M.off, Q.sbuf + Q.snd[found].off, sizeof(double) * (size_t)M.cnt,
+                                    cudaMemcpyDeviceToDevice, st);
+                }
+        } else {
+            DRank &D = R[0];
+            std::vector<int> sp_(D.snd.size()), rp_(D.rcv.size());
+            std::vector<const double *> sb(D.snd.size());
+            std::vector<double *> rb(D.rcv.size());
+            std::vector<long long> sc(D.snd.size()), rc(D.rcv.size());
+            for (size_t k = 0; k < D.snd.size(); k++) { sp_[k] = D.snd[k].peer; sb[k] = D.sbuf + D.snd[k].off; sc[k] = D.snd[k].cnt; }
+            for (size_t k = 0; k < D.rcv.size(); k++) { rp_[k] = D.rcv[k].peer; rb[k] = D.rbuf + D.rcv[k].off; rc[k] = D.rcv[k].cnt; }
+            iga_status e = dist_sendrecv(D.s, (int)sp_.size(), sp_.data(), sb.data(), sc.data(), (int)rp_.size(), rp_.data(),
+                                         rb.data(), rc.data(), st);
+            if (e != IGA_OK) return e;
+        }
+        for (int r = 0; r < nr; r++)
+            for (const DMsg &M : R[r].rcv)
+                k_dplan_box<<<(unsigned)std::max<long long>(1, std::min<long long>((M.cnt + 255) / 256, (long long)nsm * 4)), 256, 0, st>>>(
+                    R[r].P, M.box, R[r].xe, R[r].rbuf + M.off, 1);
+        return IGA_OK;
+    };
+    // y_r = (bsub_r -) A_r x_r for every rank
+    auto spmv_all = [&](const std::vector<const double *> &xs, const std::vector<double *> &ys,
+                        const std::vector<const double *> &bs) -> iga_status {
+        for (int r = 0; r < nr; r++)
+            k_dplan_scatter<<<(unsigned)std::max<long long>(1, std::min<long long>((R[r].n + 255) / 256, (long long)nsm * 8)), 256, 0, st>>>(
+                R[r].P, R[r].n, xs[r], R[r].xe);
+        iga_status e = exchange();
+        if (e != IGA_OK) return e;
+        for (int r = 0; r < nr; r++)
+            k_spmv_stream<<<(unsigned)std::max<long long>(1, (R[r].n + SP_R - 1) / SP_R), SP_R, 0, st>>>(
+                R[r].n, R[r].rp, R[r].lci, R[r].a, R[r].xe, ys[r], bs[r]);
+        return IGA_OK;
+    };
+    auto gv_of = [&](long long n) { return (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)nsm * 8)); };
+    auto precond = [&](int r, const double *in, double *out) {
+        DRank &D = R[r];
+        const long long nblk = (D.n + B - 1) / B;
+        const unsigned gell = (unsigned)((nblk + TPB_CTA - 1) / TPB_CTA);
+        const size_t smell = sizeof(double) * (size_t)TPB_CTA * (B + 1);
+        const unsigned gblk = (unsigned)(((nblk * 32) + 127) / 128);
+        if (opt->precond == 2 && D.ell) {
+            if (D.W == 2) k_ell_solve<2><<<gell, TPB_CTA, smell, st>>>(D.n, B, nblk, D.Lv, D.Lc, D.Uv, D.Uc, D.Dd, in, out);
+            else if (D.W == 4) k_ell_solve<4><<<gell, TPB_CTA, smell, st>>>(D.n, B, nblk, D.Lv, D.Lc, D.Uv, D.Uc, D.Dd, in, out);
+            else if (D.W == 8) k_ell_solve<8><<<gell, TPB_CTA, smell, st>>>(D.n, B, nblk, D.Lv, D.Lc, D.Uv, D.Uc, D.Dd, in, out);
+            else k_ell_solve<16><<<gell, TPB_CTA, smell, st>>>(D.n, B, nblk, D.Lv, D.Lc, D.Uv, D.Uc, D.Dd, in, out);
+        } else if (opt->precond == 2 && B <= 1024) {
+            k_ilu0_solve_g<<<gblk, 128, 4 * B * sizeof(double), st>>>(D.n, B, D.orp, D.oci, D.dp, D.lu, in, out);
+        } else if (opt->precond == 2) {
+            k_ilu0_solve<<<gblk, 128, 0, st>>>(D.n, B, D.orp, D.oci, D.dp, D.lu, in, out);
+        } else if (opt->precond == 1) {
+            k_jacobi<<<gv_of(D.n), 256, 0, st>>>(D.n, D.dp, D.oval, in, out);
+        } else {
+            cudaMemcpyAsync(out, in, sizeof(double) * (size_t)D.n, cudaMemcpyDeviceToDevice, st);
+        }
+    };
+    auto norm2_all = [&](const std::vector<const double *> &vs) -> double {
+        for (int r = 0; r < nr; r++) {
+            cudaMemsetAsync(R[r].dh, 0, sizeof(double), st);
+            k_multidot<<<gv_of(R[r].n), 256, 0, st>>>(R[r].n, 1, vs[r], R[r].n, vs[r], R[r].dh);
+        }
+        allreduce(1);
+        double h = 0.0;
+        cudaMemcpyAsync(&h, R[0].dh, sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        return std::sqrt(h);
+    };
+    std::vector<const double *> bvec(nr), xvec(nr), wvec(nr), V0c(nr);
+    std::vector<double *> V0(nr), wv(nr);
+    for (int r = 0; r < nr; r++) { bvec[r] = R[r].b; xvec[r] = R[r].x; V0[r] = R[r].V; V0c[r] = R[r].V; wv[r] = R[r].w; wvec[r] = R[r].w; }
+    const double bnorm = norm2_all(bvec);
+    for (int r = 0; r < nr; r++) cudaMemsetAsync(R[r].dh, 0, sizeof(double) * Lo.total(), st);
+    int it = 0;
+    iga_status e = IGA_OK;
+    while (it < maxit && bnorm > 0.0) {
+        if ((e = spmv_all(xvec, V0, bvec)) != IGA_OK) return e;
+        for (int r = 0; r < nr; r++) k_multidot<<<gv_of(R[r].n), 256, 0, st>>>(R[r].n, 1, R[r].V, R[r].n, R[r].V, R[r].dh);
+        if ((e = allreduce(1)) != IGA_OK) return e;
+        for (int r = 0; r < nr; r++) {
+            k_arn_start<<<1, 1, 0, st>>>(Lo, R[r].dh);
+            k_multiaxpy<<<gv_of(R[r].n), 256, 0, st>>>(R[r].n, 0, R[r].V, R[r].n, R[r].dh, R[r].V, 1.0, R[r].dh + Lo.ctl());
+        }
+        const int jm = std::min(m, maxit - it);
+        for (int j = 0; j < jm; j++) {
+            std::vector<const double *> zj(nr);
+            std::vector<double *> vj1(nr);
+            for (int r = 0; r < nr; r++) {
+                precond(r, R[r].V + (size_t)j * R[r].n, R[r].Z + (size_t)j * R[r].n);
+                zj[r] = R[r].Z + (size_t)j * R[r].n;
+                vj1[r] = R[r].V + (size_t)(j + 1) * R[r].n;
+            }
+            std::vector<const double *> nob(nr, nullptr);
+            if ((e = spmv_all(zj, vj1, nob)) != IGA_OK) return e;
+            for (int pass = 0; pass < 2; pass++) {
+                for (int r = 0; r < nr; r++) {
+                    int *need2 = &reinterpret_cast<ArnCtl *>(R[r].dh + Lo.ctl())->need2;
+                    k_multidot<<<gv_of(R[r].n), 256, 0, st>>>(R[r].n, j + 2, R[r].V, R[r].n, vj1[r], R[r].dh, pass ? need2 : nullptr);
+                }
+                if ((e = allreduce(j + 2)) != IGA_OK) return e;
+                for (int r = 0; r < nr; r++) {
+                    int *need2 = &reinterpret_cast<ArnCtl *>(R[r].dh + Lo.ctl())->need2;
+                    k_arn_ctrl<<<1, 32, 0, st>>>(Lo, R[r].dh, j, pass);
+                    k_multiaxpy<<<gv_of(R[r].n), 256, 0, st>>>(R[r].n, j + 1, R[r].V, R[r].n, R[r].dh + Lo.hvec(), vj1[r], 1.0,
+                                                                R[r].dh + Lo.ctl(), pass ? need2 : nullptr);
+                }
+            }
+        }
+        for (int r = 0; r < nr; r++) {
+            k_arn_solve<<<1, 256, 0, st>>>(Lo, R[r].dh, jm);
+            k_multiaxpy<<<gv_of(R[r].n), 256, 0, st>>>(R[r].n, jm, R[r].Z, R[r].n, R[r].dh + Lo.yneg(), R[r].x, 1.0);
+        }
+        it += jm;
+    }
+    if ((e = spmv_all(xvec, wv, bvec)) != IGA_OK) return e;
+    const double res = norm2_all(wvec);
+    if (iters_out) *iters_out = it;
+    if (relres_out) *relres_out = res / (bnorm > 0.0 ? bnorm : 1.0);
+    cudaStreamSynchronize(st);
+    cudaError_t ce = cudaGetLastError();
+    if (ce != cudaSuccess) { set_error(std::string("distributed gmres: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
     return IGA_OK;
 }
 

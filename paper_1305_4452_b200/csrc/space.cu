@@ -946,6 +946,34 @@ iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx
     return st;
 }
 
+iga_status iga_gmres_group(int n, const iga_space *spaces, const int64_t *const *row_ptr, const int32_t *const *col_idx,
+                           const double *const *val, const double *const *b, double *const *x, const iga_krylov *opt,
+                           int *iters, double *relres, void *stream) {
+    if (n < 1 || n > 64 || !spaces || !row_ptr || !col_idx || !val || !b || !x || !opt) {
+        set_error("bad group arguments");
+        return IGA_ERR_PARAM;
+    }
+    if (opt->precond < 0 || opt->precond > 2 || opt->restart < 1 || opt->maxit < 0) { set_error("gmres: bad options"); return IGA_ERR_PARAM; }
+    std::vector<iga_space_s *> sp(n);
+    for (int k = 0; k < n; k++) {
+        sp[k] = spaces[k];
+        if (!sp[k] || sp[k]->nranks != n || sp[k]->rank != k || sp[k]->device != sp[0]->device) {
+            set_error("group: spaces[k] must be rank k of an n-rank decomposition on one device");
+            return IGA_ERR_PARAM;
+        }
+        if (n > 1 && (!sp[k]->dist || dist_transport(sp[k]->dist) != IGA_XPORT_LOCAL)) {
+            set_error("group solves need IGA_XPORT_LOCAL spaces");
+            return IGA_ERR_STATE;
+        }
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(sp[0]->device);
+    iga_status st = gmres_group(n, sp.data(), row_ptr, col_idx, val, b, x, opt, iters, relres, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
 iga_status iga_alpha_step(iga_space s, const iga_phys *phys, const iga_alpha *opt, const int64_t *row_ptr,
                           const int32_t *col_idx, double *val, double *U, double *Udot, iga_step_stats *stats,
                           void *stream) {
