@@ -250,7 +250,10 @@ iga_status iga_gmres_group(int n, const iga_space *spaces, const int64_t *const 
  * return).  U, Udot: device, all rows; in: step n, out: step n+1.  Physics time-step parameters
  * (e.g. NS-VMS p[1] = dt) are the caller's to keep consistent with opt->dt.  stats (may be NULL):
  * ||R|| at each Newton iterate and each solve's iterations / true relative residual.
- * Single-rank spaces; newton_its in [1, 8]; 0 <= rho_inf <= 1; dt > 0 (IGA_ERR_PARAM otherwise).
+ * Multi-rank: IGA_XPORT_NCCL ranks each call iga_alpha_step with their owned vectors (the forms
+ * and the distributed GMRES exchange internally; the fixed GMRES budget rtol = 0 is required);
+ * in-process ranks call iga_alpha_step_group.  newton_its in [1, 8]; 0 <= rho_inf <= 1; dt > 0
+ * (IGA_ERR_PARAM otherwise).
  * Stage vectors (6 n doubles) are kept with the space; the call synchronises `stream`. */
 typedef struct {
     double rho_inf;
@@ -266,6 +269,10 @@ typedef struct {
 iga_status iga_alpha_step(iga_space s, const iga_phys *phys, const iga_alpha *opt, const int64_t *row_ptr,
                           const int32_t *col_idx, double *val, double *U, double *Udot,
                           iga_step_stats *stats, void *stream);
+iga_status iga_alpha_step_group(int n, const iga_space *spaces, const iga_phys *phys, const iga_alpha *opt,
+                                const int64_t *const *row_ptr, const int32_t *const *col_idx,
+                                double *const *val, double *const *U, double *const *Udot,
+                                iga_step_stats *stats, void *stream);
 
 /* Synchronises `stream` and reports (then clears) the device error flag of the last form
  * call: IGA_OK, IGA_ERR_SINGULAR_MAP or IGA_ERR_NONFINITE. */

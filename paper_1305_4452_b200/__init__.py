@@ -78,7 +78,7 @@ EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_p
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
            "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
            "iga_microbench", "iga_space_set_option", "iga_form_jacobian_group", "iga_form_residual_group",
-           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group"]
+           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group", "iga_alpha_step_group"]
 
 
 def lib():
@@ -121,13 +121,16 @@ def lib():
         L.iga_gmres.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
         L.iga_gmres_group.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                       C.POINTER(vp), C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
+        L.iga_alpha_step_group.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(_Phys), C.POINTER(_Alpha), C.POINTER(vp),
+                                           C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
+                                           C.POINTER(_StepStats), vp]
         L.iga_alpha_step.argtypes = [vp, C.POINTER(_Phys), C.POINTER(_Alpha), vp, vp, vp, vp, vp, C.POINTER(_StepStats), vp]
         L.iga_last_error.restype = C.c_char_p
         L.iga_version.restype = C.c_char_p
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
                   "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
                   "iga_profile_reset", "iga_form_jacobian_group", "iga_form_residual_group", "iga_dist_plan",
-                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group"):
+                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group", "iga_alpha_step_group"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -277,6 +280,22 @@ def gmres_group(spaces, row_ptrs, col_idxs, vals, bs, xs=None, restart=30, maxit
     _check(lib().iga_gmres_group(n, hs, arr(row_ptrs), arr(col_idxs), arr(vals), arr(bs), arr(xs), C.byref(opt),
                                  C.byref(it), C.byref(rr), _stream(stream)))
     return xs, int(it.value), float(rr.value)
+
+
+def alpha_step_group(spaces, phys, Us, Udots, row_ptrs, col_idxs, vals, rho_inf, dt, newton_its=2, restart=30,
+                     maxit=30, precond=PC_BJACOBI_ILU0, block_rows=32, stream=None):
+    """One generalized-alpha step of in-process ranks (iga_alpha_step_group); Us / Udots advance in place."""
+    n = len(spaces)
+    arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() for t in ts])
+    hs = (C.c_void_p * n)(*[sp.h.value for sp in spaces])
+    opt = _Alpha(float(rho_inf), float(dt), int(newton_its),
+                 _Krylov(int(restart), int(maxit), 0.0, int(precond), int(block_rows)))
+    stt = _StepStats()
+    _check(lib().iga_alpha_step_group(n, hs, C.byref(phys), C.byref(opt), arr(row_ptrs), arr(col_idxs), arr(vals),
+                                      arr(Us), arr(Udots), C.byref(stt), _stream(stream)))
+    k = int(newton_its)
+    return {"res_norm": list(stt.res_norm[:k]), "gmres_its": list(stt.gmres_its[:k]),
+            "gmres_relres": list(stt.gmres_relres[:k])}
 
 
 def form_residual_group(spaces, phys, Us, Udots=None, Fs=None, stream=None):

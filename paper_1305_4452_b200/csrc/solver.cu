@@ -882,60 +882,102 @@ __global__ void k_ga_update(long long n, const double *__restrict__ dx, double g
     }
 }
 
-iga_status alpha_step(iga_space_s *s, const iga_phys *phys, const iga_alpha *opt, const int64_t *rp, const int32_t *ci,
-                      double *val, double *U, double *Udot, iga_step_stats *stats, cudaStream_t st) {
-    if (s->nranks > 1) { set_error("alpha_step: single-rank in this build"); return IGA_ERR_STATE; }
-    const long long n = s->nrows_owned;
+__global__ void k_sum_ranks(int nr, double *const *bufs, int cnt);
+
+// all ranks of a decomposition (in-process: nr = nranks; NCCL: nr = 1, this process's rank; one
+// rank: the plain step)
+iga_status alpha_step_group(int nr, iga_space_s *const *sp, const iga_phys *phys, const iga_alpha *opt,
+                            const int64_t *const *rp, const int32_t *const *ci, double *const *val, double *const *U,
+                            double *const *Udot, iga_step_stats *stats, cudaStream_t st) {
     const double rho = opt->rho_inf, dt = opt->dt;
     const double am = 0.5 * (3.0 - rho) / (1.0 + rho), af = 1.0 / (1.0 + rho), gamma = 0.5 + am - af;
-    const size_t vb = ((sizeof(double) * (size_t)n + 255) & ~(size_t)255);
-    char *base = (char *)ws_ensure(s, 2, 6 * vb + 256);
-    if (!base) { set_error("alpha_step workspace"); return IGA_ERR_NOMEM; }
-    double *U1 = (double *)base, *Ud1 = (double *)(base + vb), *Ua = (double *)(base + 2 * vb),
-           *Uda = (double *)(base + 3 * vb), *R = (double *)(base + 4 * vb), *dx = (double *)(base + 5 * vb),
-           *dn = (double *)(base + 6 * vb);
+    const bool multi = sp[0]->nranks > 1;
+    const bool local = !multi || dist_transport(sp[0]->dist) == IGA_XPORT_LOCAL;
+    if (multi && opt->krylov.rtol != 0.0) { set_error("alpha_step: multi-rank steps use the fixed GMRES budget (rtol = 0)"); return IGA_ERR_PARAM; }
+    std::vector<double *> U1(nr), Ud1(nr), Ua(nr), Uda(nr), R(nr), dx(nr), dn(nr);
+    std::vector<long long> n(nr);
+    for (int r = 0; r < nr; r++) {
+        n[r] = sp[r]->nrows_owned;
+        const size_t vb = ((sizeof(double) * (size_t)n[r] + 255) & ~(size_t)255);
+        char *base = (char *)ws_ensure(sp[r], 2, 6 * vb + 256);
+        if (!base) { set_error("alpha_step workspace"); return IGA_ERR_NOMEM; }
+        U1[r] = (double *)base; Ud1[r] = (double *)(base + vb); Ua[r] = (double *)(base + 2 * vb);
+        Uda[r] = (double *)(base + 3 * vb); R[r] = (double *)(base + 4 * vb); dx[r] = (double *)(base + 5 * vb);
+        dn[r] = (double *)(base + 6 * vb);
+    }
+    double **dptrs = nullptr;
+    if (local && nr > 1) {
+        if (cudaMalloc(&dptrs, sizeof(double *) * nr) != cudaSuccess) { cudaGetLastError(); set_error("alpha_step ptrs"); return IGA_ERR_NOMEM; }
+        cudaMemcpyAsync(dptrs, dn.data(), sizeof(double *) * nr, cudaMemcpyHostToDevice, st);
+    }
     int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
-    const unsigned gv = (unsigned)std::max<long long>(1, std::min<long long>((n + 255) / 256, (long long)nsm * 8));
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, sp[0]->device);
+    auto gv = [&](long long m_) { return (unsigned)std::max<long long>(1, std::min<long long>((m_ + 255) / 256, (long long)nsm * 8)); };
     int launches = 0;
+    iga_status e = IGA_OK;
     if (stats) *stats = iga_step_stats{};
-    k_ga_predict<<<gv, 256, 0, st>>>(n, U, Udot, (gamma - 1.0) / gamma, U1, Ud1);
-    launches++;
-    for (int k = 0; k < opt->newton_its; k++) {
-        k_ga_stage<<<gv, 256, 0, st>>>(n, U, Udot, U1, Ud1, af, am, Ua, Uda);
-        launches++;
-        iga_status e = form_one(s, phys, am, af * gamma * dt, Ua, Uda, val, R, st);
-        if (e != IGA_OK) return e;
-        launches += s->last_launches;
+    for (int r = 0; r < nr; r++) k_ga_predict<<<gv(n[r]), 256, 0, st>>>(n[r], U[r], Udot[r], (gamma - 1.0) / gamma, U1[r], Ud1[r]);
+    launches += nr;
+    for (int k = 0; k < opt->newton_its && e == IGA_OK; k++) {
+        for (int r = 0; r < nr; r++) k_ga_stage<<<gv(n[r]), 256, 0, st>>>(n[r], U[r], Udot[r], U1[r], Ud1[r], af, am, Ua[r], Uda[r]);
+        launches += nr;
+        if (!multi) e = form_one(sp[0], phys, am, af * gamma * dt, Ua[0], Uda[0], val[0], R[0], st);
+        else {
+            std::vector<const double *> ua(Ua.begin(), Ua.end()), uda(Uda.begin(), Uda.end());
+            std::vector<iga_space_s *> spv(sp, sp + nr);
+            e = dist_form(spv.data(), nr, phys, am, af * gamma * dt, ua.data(), uda.data(), val, R.data(), st);
+        }
+        if (e != IGA_OK) break;
+        launches += sp[0]->last_launches;
         if (stats) {
             double r2 = 0.0;
-            cudaMemsetAsync(dn, 0, sizeof(double), st);
-            k_multidot<<<gv, 256, 0, st>>>(n, 1, R, n, R, dn);
-            launches++;
-            cudaMemcpyAsync(&r2, dn, sizeof(double), cudaMemcpyDeviceToHost, st);
+            for (int r = 0; r < nr; r++) {
+                cudaMemsetAsync(dn[r], 0, sizeof(double), st);
+                k_multidot<<<gv(n[r]), 256, 0, st>>>(n[r], 1, R[r], n[r], R[r], dn[r]);
+            }
+            if (multi && local) k_sum_ranks<<<1, 64, 0, st>>>(nr, dptrs, 1);
+            else if (multi && (e = dist_allreduce_sum(sp[0], dn[0], 1, st)) != IGA_OK) break;
+            cudaMemcpyAsync(&r2, dn[0], sizeof(double), cudaMemcpyDeviceToHost, st);
             cudaStreamSynchronize(st);
             stats->res_norm[k] = std::sqrt(r2);
         }
-        cudaMemsetAsync(dx, 0, sizeof(double) * (size_t)n, st);
+        for (int r = 0; r < nr; r++) cudaMemsetAsync(dx[r], 0, sizeof(double) * (size_t)n[r], st);
         int its = 0;
         double rr = 0.0;
-        e = gmres_solve(s, rp, ci, val, R, dx, &opt->krylov, &its, &rr, st);
-        if (e != IGA_OK) return e;
-        launches += s->last_launches;
+        if (!multi) e = gmres_solve(sp[0], rp[0], ci[0], val[0], R[0], dx[0], &opt->krylov, &its, &rr, st);
+        else {
+            std::vector<const double *> vv(val, val + nr), bb(R.begin(), R.end());
+            e = gmres_group(nr, sp, rp, ci, vv.data(), bb.data(), dx.data(), &opt->krylov, &its, &rr, st);
+        }
+        if (e != IGA_OK) break;
         if (stats) {
             stats->gmres_its[k] = its;
             stats->gmres_relres[k] = rr;
         }
-        k_ga_update<<<gv, 256, 0, st>>>(n, dx, gamma * dt, U1, Ud1);
-        launches++;
+        for (int r = 0; r < nr; r++) k_ga_update<<<gv(n[r]), 256, 0, st>>>(n[r], dx[r], gamma * dt, U1[r], Ud1[r]);
+        launches += nr;
     }
-    cudaMemcpyAsync(U, U1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(Udot, Ud1, sizeof(double) * (size_t)n, cudaMemcpyDeviceToDevice, st);
+    if (e == IGA_OK)
+        for (int r = 0; r < nr; r++) {
+            cudaMemcpyAsync(U[r], U1[r], sizeof(double) * (size_t)n[r], cudaMemcpyDeviceToDevice, st);
+            cudaMemcpyAsync(Udot[r], Ud1[r], sizeof(double) * (size_t)n[r], cudaMemcpyDeviceToDevice, st);
+        }
     cudaStreamSynchronize(st);
-    s->last_launches = launches;
+    if (dptrs) cudaFree(dptrs);
+    if (e != IGA_OK) return e;
+    sp[0]->last_launches = launches;
     cudaError_t ce = cudaGetLastError();
     if (ce != cudaSuccess) { set_error(std::string("alpha_step: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
     return IGA_OK;
+}
+
+iga_status alpha_step(iga_space_s *s, const iga_phys *phys, const iga_alpha *opt, const int64_t *rp, const int32_t *ci,
+                      double *val, double *U, double *Udot, iga_step_stats *stats, cudaStream_t st) {
+    if (s->nranks > 1 && (!s->dist || dist_transport(s->dist) != IGA_XPORT_NCCL)) {
+        set_error("alpha_step: in-process (IGA_XPORT_LOCAL) ranks step through iga_alpha_step_group");
+        return IGA_ERR_STATE;
+    }
+    return alpha_step_group(1, &s, phys, opt, &rp, &ci, &val, &U, &Udot, stats, st);
 }
 
 

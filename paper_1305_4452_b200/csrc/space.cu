@@ -974,6 +974,37 @@ iga_status iga_gmres_group(int n, const iga_space *spaces, const int64_t *const 
     return st;
 }
 
+iga_status iga_alpha_step_group(int n, const iga_space *spaces, const iga_phys *phys, const iga_alpha *opt,
+                                const int64_t *const *row_ptr, const int32_t *const *col_idx, double *const *val,
+                                double *const *U, double *const *Udot, iga_step_stats *stats, void *stream) {
+    if (n < 1 || n > 64 || !spaces || !opt || !row_ptr || !col_idx || !val || !U || !Udot) { set_error("bad group arguments"); return IGA_ERR_PARAM; }
+    iga_status st = check_phys(spaces[0], phys);
+    if (st != IGA_OK) return st;
+    if (opt->newton_its < 1 || opt->newton_its > 8 || !(opt->dt > 0.0) || !(opt->rho_inf >= 0.0 && opt->rho_inf <= 1.0) ||
+        opt->krylov.precond < 0 || opt->krylov.precond > 2 || opt->krylov.restart < 1 || opt->krylov.maxit < 0) {
+        set_error("alpha_step: bad options");
+        return IGA_ERR_PARAM;
+    }
+    std::vector<iga_space_s *> sp(n);
+    for (int k = 0; k < n; k++) {
+        sp[k] = spaces[k];
+        if (!sp[k] || sp[k]->nranks != n || sp[k]->rank != k || sp[k]->device != sp[0]->device) {
+            set_error("group: spaces[k] must be rank k of an n-rank decomposition on one device");
+            return IGA_ERR_PARAM;
+        }
+        if (n > 1 && (!sp[k]->dist || dist_transport(sp[k]->dist) != IGA_XPORT_LOCAL)) {
+            set_error("group steps need IGA_XPORT_LOCAL spaces");
+            return IGA_ERR_STATE;
+        }
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(sp[0]->device);
+    st = alpha_step_group(n, sp.data(), phys, opt, row_ptr, col_idx, val, U, Udot, stats, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    return st;
+}
+
 iga_status iga_alpha_step(iga_space s, const iga_phys *phys, const iga_alpha *opt, const int64_t *row_ptr,
                           const int32_t *col_idx, double *val, double *U, double *Udot, iga_step_stats *stats,
                           void *stream) {
