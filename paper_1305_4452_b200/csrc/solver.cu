@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(SP_R) k_spmv_stream(long long n, const int64_t
     const long long p0 = srp[0], cnt = srp[nr] - p0;
     if (cnt <= SP_CAP) {
 #pragma unroll 4
-        for (int k = threadIdx.x; k < cnt; k += SP_R) prod[k] = a[p0 + k] * __ldg(x + ci[p0 + k]);
+        for (int k = threadIdx.x; k < cnt; k += SP_R) prod[k] = __ldcs(a + p0 + k) * __ldg(x + __ldcs(ci + p0 + k));
         __syncthreads();
         if (threadIdx.x < nr) {
             const int r = threadIdx.x;
