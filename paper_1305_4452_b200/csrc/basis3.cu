@@ -106,7 +106,9 @@ __device__ __forceinline__ void tensor3(const double (&f)[DIM][4], double &m0, d
     }
 }
 
-template <int DIM, int PP>
+// MAPPED = rational basis or NURBS geometry; otherwise (parametric geometry, unit weights) the
+// spatial derivatives ARE the tensor-product parametric ones and the map / rational passes vanish
+template <int DIM, int PP, bool MAPPED>
 __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long nelem, int nq_el, int ncomp,
                                                 double *__restrict__ out, const double *__restrict__ kn0,
                                                 const double *__restrict__ kn1, const double *__restrict__ kn2) {
@@ -135,8 +137,8 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
         P.g[d] = first;
         span_ders3(first + PP, ax.qx[(size_t)e[d] * ax.nq + qd[d]], PP, d == 0 ? kn0 : d == 1 ? kn1 : kn2, P.v[d]);
     }
-    const bool rational = s.mode == MODE_NURBS;
-    const bool geom = s.geom == IGA_GEOM_NURBS;
+    const bool rational = MAPPED && s.mode == MODE_NURBS;
+    const bool geom = MAPPED && s.geom == IGA_GEOM_NURBS;
     auto decode = [&](int A, int aa[3], long long &node) {
         int r = A;
         int g[3] = {0, 0, 0};
@@ -158,6 +160,37 @@ __global__ void __launch_bounds__(128) k_basis3(SpaceDev s, int order, long long
 #pragma unroll
                     for (int k = 0; k < 4; k++) f[d][k] = P.v[d][k][a];
     };
+    if constexpr (!MAPPED) {
+        double *base = out + (size_t)el * NEN * ncomp * nq_el + q;
+#pragma unroll 1
+        for (int A = 0; A < NEN; A++) {
+            int aa[3] = {0, 0, 0};
+            long long node;
+            decode(A, aa, node);
+            double m0, m1[DIM], m2[DIM][DIM], m3[DIM][DIM][DIM], f[DIM][4];
+            fvals(aa, f);
+            tensor3<DIM>(f, m0, m1, m2, m3);
+            double *o = base + (size_t)A * ncomp * nq_el;
+            int c = 0;
+            o[(c++) * nq_el] = m0;
+            if (order >= 1)
+#pragma unroll
+                for (int i = 0; i < DIM; i++) o[(c++) * nq_el] = m1[i];
+            if (order >= 2)
+#pragma unroll
+                for (int i = 0; i < DIM; i++)
+#pragma unroll
+                    for (int j = 0; j < DIM; j++) o[(c++) * nq_el] = m2[i][j];
+            if (order >= 3)
+#pragma unroll
+                for (int i = 0; i < DIM; i++)
+#pragma unroll
+                    for (int j = 0; j < DIM; j++)
+#pragma unroll
+                        for (int k = 0; k < DIM; k++) o[(c++) * nq_el] = m3[i][j][k];
+        }
+        return;
+    }
     // ---- pass 1: w and its parametric derivatives ----
     double w0 = 0.0, w1[DIM] = {}, w2[DIM][DIM] = {}, w3[DIM][DIM][DIM] = {};
 #pragma unroll 1
@@ -387,10 +420,14 @@ iga_status launch_basis3(iga_space_s *s, int order, double *out, cudaStream_t st
         auto go = [&](auto kern) {
             kern<<<blocks, 128, 0, st>>>(s->dev, order, s->nel_local, nq_el, ncomp, out, s->dknots[0], s->dknots[1], s->dknots[2]);
         };
+        // the unmapped fast path pays in 3D (config 4: 74.5 -> 27.3 ms); in 2D the general kernel
+        // measured faster (3.49 vs 3.77 ms on config 3), so 2D always takes it
+        const bool mapped = s->mode == MODE_NURBS || s->geom == IGA_GEOM_NURBS || s->dim == 2;
         if (s->dim == 2) {
-            if (p == 1) go(k_basis3<2, 1>); else if (p == 2) go(k_basis3<2, 2>); else go(k_basis3<2, 3>);
+            if (p == 1) go(k_basis3<2, 1, true>); else if (p == 2) go(k_basis3<2, 2, true>); else go(k_basis3<2, 3, true>);
         } else {
-            if (p == 1) go(k_basis3<3, 1>); else if (p == 2) go(k_basis3<3, 2>); else go(k_basis3<3, 3>);
+            if (mapped) { if (p == 1) go(k_basis3<3, 1, true>); else if (p == 2) go(k_basis3<3, 2, true>); else go(k_basis3<3, 3, true>); }
+            else { if (p == 1) go(k_basis3<3, 1, false>); else if (p == 2) go(k_basis3<3, 2, false>); else go(k_basis3<3, 3, false>); }
         }
     }
     s->last_launches = 1;
