@@ -231,6 +231,17 @@ typedef struct {
 iga_status iga_gmres(iga_space s, const int64_t *row_ptr, const int32_t *col_idx, const double *val,
                      const double *b, double *x, const iga_krylov *opt, int *iters, double *relres,
                      void *stream);
+/* Host only (no GPU): the distributed solve's ghost-exchange plan of rank dist->rank.  The
+ * extended box (owned box + `ghost` = p layers on each side of the partitioned axes) has extent
+ * ext_n; messages are boxes of it in node units (box_lo / box_n), `rows` = nodes * dof values,
+ * `subbox` = ((o0+1)*3 + (o1+1))*3 + (o2+1) for the neighbour offset o in {-1,0,1}^3, `values` = 0.
+ * send[k]: this rank's owned slab on side o, to the rank at coordinate + o, ascending o;
+ * recv[k]: its ghost layer on side o, from the rank at coordinate + o, descending o (the order a
+ * grouped NCCL exchange pairs repeated peers in).  Up to max_msgs each; counts in nsend / nrecv. */
+iga_status iga_krylov_plan(const iga_space_desc *desc, const iga_dist *dist, int64_t own_lo[3],
+                           int64_t own_hi[3], int64_t ext_n[3], int64_t ghost[3], int max_msgs,
+                           iga_msg *send, int *nsend, iga_msg *recv, int *nrecv);
+
 /* All n in-process ranks (IGA_XPORT_LOCAL spaces, rank k = spaces[k]) solve together on one
  * stream; per-rank arrays as for iga_gmres; iters / relres are global. */
 iga_status iga_gmres_group(int n, const iga_space *spaces, const int64_t *const *row_ptr,

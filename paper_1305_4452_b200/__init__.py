@@ -78,7 +78,8 @@ EXPORTS = ["iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_p
            "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_last_launch_count",
            "iga_last_error", "iga_version", "iga_profile_enable", "iga_profile_reset", "iga_profile_read",
            "iga_microbench", "iga_space_set_option", "iga_form_jacobian_group", "iga_form_residual_group",
-           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group", "iga_alpha_step_group"]
+           "iga_dist_plan", "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group", "iga_alpha_step_group",
+           "iga_krylov_plan"]
 
 
 def lib():
@@ -121,6 +122,8 @@ def lib():
         L.iga_gmres.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
         L.iga_gmres_group.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                       C.POINTER(vp), C.POINTER(_Krylov), C.POINTER(C.c_int), dp, vp]
+        L.iga_krylov_plan.argtypes = [C.POINTER(_Desc), C.POINTER(_Dist), lp, lp, lp, lp, C.c_int,
+                                      C.POINTER(_Msg), C.POINTER(C.c_int), C.POINTER(_Msg), C.POINTER(C.c_int)]
         L.iga_alpha_step_group.argtypes = [C.c_int, C.POINTER(vp), C.POINTER(_Phys), C.POINTER(_Alpha), C.POINTER(vp),
                                            C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                            C.POINTER(_StepStats), vp]
@@ -130,7 +133,8 @@ def lib():
         for f in ("iga_space_create", "iga_space_destroy", "iga_space_info", "iga_csr_pattern", "iga_form_residual",
                   "iga_form_jacobian", "iga_form_jacobian_host", "iga_space_check", "iga_profile_enable",
                   "iga_profile_reset", "iga_form_jacobian_group", "iga_form_residual_group", "iga_dist_plan",
-                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group", "iga_alpha_step_group"):
+                  "iga_nccl_unique_id", "iga_basis_eval", "iga_gmres", "iga_alpha_step", "iga_gmres_group", "iga_alpha_step_group",
+                  "iga_krylov_plan"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -243,6 +247,28 @@ def dist_plan(w, dist) -> dict:
                  "box_lo": list(a[k].box_lo), "box_n": list(a[k].box_n)} for k in range(n)]
     own_lo, own_hi, el_lo, el_hi, ext_n = [list(x) for x in arrs]
     return {"own_lo": own_lo, "own_hi": own_hi, "el_lo": el_lo, "el_hi": el_hi, "ext_n": ext_n,
+            "send": msgs(snd, ns.value), "recv": msgs(rcv, nr.value)}
+
+
+def krylov_plan(w, dist) -> dict:
+    """Host-only ghost-exchange plan of the distributed GMRES for rank dist["rank"] (no GPU)."""
+    d, keep = _make_desc(w.dim, w.degree, w.knots, w.periodic, w.continuity, w.dof, w.quad, w.geometry, w.ctrl,
+                         w.weights)
+    dd = _make_dist(dist)
+    arrs = [(C.c_int64 * 3)() for _ in range(4)]
+    snd, rcv = (_Msg * 32)(), (_Msg * 32)()
+    ns, nr = C.c_int(), C.c_int()
+    _check(lib().iga_krylov_plan(C.byref(d), C.byref(dd), *arrs, 32, snd, C.byref(ns), rcv, C.byref(nr)))
+
+    def msgs(a, n):
+        out = []
+        for k in range(n):
+            sb = a[k].subbox
+            out.append({"peer": a[k].peer, "offset": [sb // 9 - 1, (sb // 3) % 3 - 1, sb % 3 - 1], "rows": a[k].rows,
+                        "box_lo": list(a[k].box_lo), "box_n": list(a[k].box_n)})
+        return out
+    own_lo, own_hi, ext_n, ghost = [list(x) for x in arrs]
+    return {"own_lo": own_lo, "own_hi": own_hi, "ext_n": ext_n, "ghost": ghost,
             "send": msgs(snd, ns.value), "recv": msgs(rcv, nr.value)}
 
 

@@ -105,6 +105,9 @@ iga_status gmres_solve(iga_space_s *s, const int64_t *rp, const int32_t *ci, con
                        const iga_krylov *opt, int *iters, double *relres, cudaStream_t st);        // solver.cu
 iga_status alpha_step(iga_space_s *s, const iga_phys *phys, const iga_alpha *opt, const int64_t *rp, const int32_t *ci,
                       double *val, double *U, double *Udot, iga_step_stats *stats, cudaStream_t st);  // solver.cu
+iga_status krylov_plan_host(const iga_space_desc *d, const iga_dist *dist, int64_t own_lo[3], int64_t own_hi[3],
+                            int64_t ext_n[3], int64_t ghost[3], int max_msgs, iga_msg *send, int *nsend, iga_msg *recv,
+                            int *nrecv);                                                               // solver.cu
 iga_status alpha_step_group(int nr, iga_space_s *const *sp, const iga_phys *phys, const iga_alpha *opt,
                             const int64_t *const *rp, const int32_t *const *ci, double *const *val, double *const *U,
                             double *const *Udot, iga_step_stats *stats, cudaStream_t st);              // solver.cu

@@ -1136,21 +1136,11 @@ struct DRank {
     ~DRank() { for (void *p : mem) cudaFree(p); }
 };
 
-static void dplan_build(DRank &R) {
-    iga_space_s *s = R.s;
-    DPlan &P = R.P;
-    P.dim = s->dim;
-    P.m = s->dof;
-    for (int a = 0; a < 3; a++) {
-        P.nu[a] = a < s->dim ? s->nu[a] : 1;
-        P.part[a] = a < s->dim && s->procs[a] > 1;
-        P.lo[a] = a < s->dim ? s->own_lo[a] : 0;
-        P.N[a] = a < s->dim ? s->own_hi[a] - s->own_lo[a] : 1;
-        P.G[a] = P.part[a] ? s->p[a] : 0;
-        P.E[a] = P.part[a] ? P.N[a] + 2 * P.G[a] : P.N[a];
-    }
-    R.next = (long long)P.E[0] * P.E[1] * P.E[2] * P.m;
-    // messages: offsets in {-1,0,1}^dim on the partitioned axes, sends ascending, receives descending
+// host-only: the ghost-exchange messages of the rank at coordinate rc (no GPU; also behind the
+// GPU-free iga_krylov_plan).  Sends (ascending offset) carry this rank's owned slab on side o to
+// the neighbour at rc + o; receives (descending offset) fill the ghost layer on side o.
+static void dplan_messages(const DPlan &P, const int procs[3], const int rc[3], const int per[3],
+                           std::vector<DMsg> &snd, std::vector<DMsg> &rcv, long long &sn, long long &rn) {
     std::vector<std::array<int, 3>> offs;
     for (int o0 = -1; o0 <= 1; o0++)
         for (int o1 = -1; o1 <= 1; o1++)
@@ -1161,19 +1151,19 @@ static void dplan_build(DRank &R) {
                     if (o[a] && !P.part[a]) ok = false;
                 if (ok) offs.push_back({o0, o1, o2});
             }
-    R.snd.clear();
-    R.rcv.clear();
-    R.sn = R.rn = 0;
+    snd.clear();
+    rcv.clear();
+    sn = rn = 0;
     auto peer_of = [&](const int o[3], int &peer) {
         int c[3];
         for (int a = 0; a < 3; a++) {
-            c[a] = s->rcoord[a] + o[a];
-            if (c[a] < 0 || c[a] >= s->procs[a]) {
-                if (!(a < s->dim && s->periodic[a])) return false;
-                c[a] = (c[a] + s->procs[a]) % s->procs[a];
+            c[a] = rc[a] + o[a];
+            if (c[a] < 0 || c[a] >= procs[a]) {
+                if (!per[a]) return false;
+                c[a] = (c[a] + procs[a]) % procs[a];
             }
         }
-        peer = (c[0] * s->procs[1] + c[1]) * s->procs[2] + c[2];
+        peer = (c[0] * procs[1] + c[1]) * procs[2] + c[2];
         return true;
     };
     for (size_t k = 0; k < offs.size(); k++) {
@@ -1182,14 +1172,13 @@ static void dplan_build(DRank &R) {
         if (!peer_of(o, M.peer)) continue;
         for (int a = 0; a < 3; a++) {
             M.o[a] = o[a];
-            // my owned slab on side o (what the neighbour at c+o keeps as its ghost on side -o)
             M.box.lo[a] = o[a] > 0 ? P.G[a] + P.N[a] - P.G[a] : P.G[a];
             M.box.n[a] = o[a] ? P.G[a] : P.N[a];
         }
         M.cnt = (long long)M.box.n[0] * M.box.n[1] * M.box.n[2] * P.m;
-        M.off = R.sn;
-        R.sn += M.cnt;
-        R.snd.push_back(M);
+        M.off = sn;
+        sn += M.cnt;
+        snd.push_back(M);
     }
     for (size_t kk = offs.size(); kk-- > 0;) {
         const int *o = offs[kk].data();
@@ -1197,15 +1186,93 @@ static void dplan_build(DRank &R) {
         if (!peer_of(o, M.peer)) continue;
         for (int a = 0; a < 3; a++) {
             M.o[a] = o[a];
-            // my ghost layer on side o
             M.box.lo[a] = o[a] < 0 ? 0 : o[a] > 0 ? P.G[a] + P.N[a] : P.G[a];
             M.box.n[a] = o[a] ? P.G[a] : P.N[a];
         }
         M.cnt = (long long)M.box.n[0] * M.box.n[1] * M.box.n[2] * P.m;
-        M.off = R.rn;
-        R.rn += M.cnt;
-        R.rcv.push_back(M);
+        M.off = rn;
+        rn += M.cnt;
+        rcv.push_back(M);
     }
+}
+
+static void dplan_build(DRank &R) {
+    iga_space_s *s = R.s;
+    DPlan &P = R.P;
+    P.dim = s->dim;
+    P.m = s->dof;
+    int per[3] = {0, 0, 0};
+    for (int a = 0; a < 3; a++) {
+        P.nu[a] = a < s->dim ? s->nu[a] : 1;
+        P.part[a] = a < s->dim && s->procs[a] > 1;
+        P.lo[a] = a < s->dim ? s->own_lo[a] : 0;
+        P.N[a] = a < s->dim ? s->own_hi[a] - s->own_lo[a] : 1;
+        P.G[a] = P.part[a] ? s->p[a] : 0;
+        P.E[a] = P.part[a] ? P.N[a] + 2 * P.G[a] : P.N[a];
+        per[a] = a < s->dim && s->periodic[a];
+    }
+    R.next = (long long)P.E[0] * P.E[1] * P.E[2] * P.m;
+    dplan_messages(P, s->procs, s->rcoord, per, R.snd, R.rcv, R.sn, R.rn);
+}
+
+// GPU-free: the distributed-solve plan of one rank from the space description
+iga_status krylov_plan_host(const iga_space_desc *d, const iga_dist *dist, int64_t own_lo[3], int64_t own_hi[3],
+                            int64_t ext_n[3], int64_t ghost[3], int max_msgs, iga_msg *send, int *nsend, iga_msg *recv,
+                            int *nrecv) {
+    if (!d || !dist) { set_error("null argument"); return IGA_ERR_PARAM; }
+    if (d->dim < 2 || d->dim > 3 || d->dof < 1 || d->dof > 4) { set_error("dim 2..3, dof 1..4"); return IGA_ERR_PARAM; }
+    int procs[3] = {1, 1, 1}, rc[3] = {0, 0, 0}, per[3] = {0, 0, 0}, prod = 1;
+    for (int a = 0; a < 3; a++) {
+        procs[a] = a < d->dim ? std::max(1, dist->procs[a]) : 1;
+        prod *= procs[a];
+    }
+    if (prod != dist->nranks || dist->rank < 0 || dist->rank >= dist->nranks) {
+        set_error("iga_dist: procs product must equal nranks and 0 <= rank < nranks");
+        return IGA_ERR_PARAM;
+    }
+    int r = dist->rank;
+    rc[2] = r % procs[2]; r /= procs[2];
+    rc[1] = r % procs[1]; r /= procs[1];
+    rc[0] = r;
+    DPlan P{};
+    P.dim = d->dim;
+    P.m = d->dof;
+    for (int a = 0; a < 3; a++) {
+        if (a >= d->dim) { P.nu[a] = 1; P.N[a] = 1; P.E[a] = 1; continue; }
+        AxisHost H;
+        iga_status st = axis_host(d, a, procs[a], H);
+        if (st != IGA_OK) return st;
+        P.nu[a] = H.nu;
+        P.part[a] = procs[a] > 1;
+        P.lo[a] = H.own_lo[rc[a]];
+        P.N[a] = H.own_hi[rc[a]] - H.own_lo[rc[a]];
+        P.G[a] = P.part[a] ? H.p : 0;
+        P.E[a] = P.part[a] ? P.N[a] + 2 * P.G[a] : P.N[a];
+        per[a] = H.periodic;
+        if (own_lo) own_lo[a] = H.own_lo[rc[a]];
+        if (own_hi) own_hi[a] = H.own_hi[rc[a]];
+    }
+    for (int a = 0; a < 3; a++) {
+        if (a >= d->dim) { if (own_lo) own_lo[a] = 0; if (own_hi) own_hi[a] = 1; }
+        if (ext_n) ext_n[a] = P.E[a];
+        if (ghost) ghost[a] = P.G[a];
+    }
+    std::vector<DMsg> snd, rcv;
+    long long sn, rn;
+    dplan_messages(P, procs, rc, per, snd, rcv, sn, rn);
+    auto put = [&](const std::vector<DMsg> &L, iga_msg *out, int *cnt) {
+        if (cnt) *cnt = (int)L.size();
+        for (int k = 0; k < (int)L.size() && k < max_msgs && out; k++) {
+            out[k].peer = L[k].peer;
+            out[k].subbox = ((L[k].o[0] + 1) * 3 + (L[k].o[1] + 1)) * 3 + (L[k].o[2] + 1);
+            out[k].rows = L[k].cnt;
+            out[k].values = 0;
+            for (int a = 0; a < 3; a++) { out[k].box_lo[a] = L[k].box.lo[a]; out[k].box_n[a] = L[k].box.n[a]; }
+        }
+    };
+    put(snd, send, nsend);
+    put(rcv, recv, nrecv);
+    return IGA_OK;
 }
 
 iga_status gmres_group(int nr, iga_space_s *const *sp, const int64_t *const *rp, const int32_t *const *ci,

@@ -921,6 +921,12 @@ iga_status iga_dist_plan(const iga_space_desc *desc, const iga_dist *dist, int64
     return dist_plan_host(desc, dist, own_lo, own_hi, el_lo, el_hi, ext_n, max_msgs, send, nsend, recv, nrecv);
 }
 
+iga_status iga_krylov_plan(const iga_space_desc *desc, const iga_dist *dist, int64_t own_lo[3], int64_t own_hi[3],
+                           int64_t ext_n[3], int64_t ghost[3], int max_msgs, iga_msg *send, int *nsend, iga_msg *recv,
+                           int *nrecv) {
+    return krylov_plan_host(desc, dist, own_lo, own_hi, ext_n, ghost, max_msgs, send, nsend, recv, nrecv);
+}
+
 iga_status iga_basis_eval(iga_space s, int order, double *out, void *stream) {
     if (!s || !out) { set_error("null argument"); return IGA_ERR_PARAM; }
     int prev = 0;
