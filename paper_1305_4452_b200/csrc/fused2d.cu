@@ -161,7 +161,10 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     constexpr int NWARP = TL::NWARP, NGRP = NWARP * GPW;
     constexpr int NB0 = TL::NB0, NB1 = TL::NB1, NBN = NB0 * NB1, NSL = TL::NSL, W2 = 2 * P + 1;
     constexpr int NE = L::NE, NR = L::NR;
-    constexpr int SCR = (JAC ? NE : 0) + NR;
+    // group scratch per point: coefficients D~ (Jacobian) and r~; for p = 3 also room for the
+    // sum-factorised homogeneous sums (residual-only launches need it beyond r~)
+    constexpr int SFN = P == 3 ? (NP1 * NQ1 * ((MODE == MODE_NURBS ? 3 : 0) + 1 + (PH::UDOT ? 1 : 0)) * 3 + NQ - 1) / NQ : 0;
+    constexpr int SCR = JAC ? NE + NR : (NR > SFN ? NR : SFN);
 
     extern __shared__ __align__(16) double sm[];
     double *nU = sm, *nUd = nU + NBN, *nw = nUd + NBN, *nx0 = nw + NBN, *nx1 = nx0 + NBN;
@@ -482,9 +485,10 @@ static size_t fused2d_smem(bool jac) {
     using TL = Tile2<P>;
     constexpr int NQ1 = P + 1, NP1 = P + 1, NQ = NQ1 * NQ1;
     constexpr int NGRP = TL::NWARP * (32 / (NP1 * NP1));
+    constexpr int SFN = P == 3 ? (NP1 * NQ1 * ((MODE == MODE_NURBS ? 3 : 0) + 1 + (PH::UDOT ? 1 : 0)) * 3 + NQ - 1) / NQ : 0;
     const int NBN = TL::NB0 * TL::NB1;
     size_t n = 5 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
-               + 2 * TL::TE1 + (size_t)NGRP * (((jac ? L::NE : 0) + L::NR) * NQ + (P == 3 ? 1 : 0));
+               + 2 * TL::TE1 + (size_t)NGRP * ((jac ? L::NE + L::NR : std::max(L::NR, SFN)) * NQ + (P == 3 ? 1 : 0));
     // scatter metadata: rowOff, fIdx (8 B) + rowW1 (4 B) per node, posd tables
     return n * sizeof(double) + (size_t)NBN * 20 + (size_t)(TL::NB0 + TL::NB1) * (2 * P + 1) * sizeof(int);
 }
