@@ -163,7 +163,8 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     constexpr int NE = L::NE, NR = L::NR;
     // group scratch per point: coefficients D~ (Jacobian) and r~; for p = 3 also room for the
     // sum-factorised homogeneous sums (residual-only launches need it beyond r~)
-    constexpr int SFN = P == 3 ? (NP1 * NQ1 * ((MODE == MODE_NURBS ? 3 : 0) + 1 + (PH::UDOT ? 1 : 0)) * 3 + NQ - 1) / NQ : 0;
+    constexpr int SFN = (P == 3 || MODE == MODE_NURBS)
+                            ? (NP1 * NQ1 * ((MODE == MODE_NURBS ? 3 : 0) + 1 + (PH::UDOT ? 1 : 0)) * 3 + NQ - 1) / NQ : 0;
     constexpr int SCR = JAC ? NE + NR : (NR > SFN ? NR : SFN);
 
     extern __shared__ __align__(16) double sm[];
@@ -280,7 +281,9 @@ k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             //     (2 (p+1)^3 FMA per field and order pair instead of (p+1)^4 per point)
             constexpr int NFW = MODE == MODE_NURBS ? 3 : 0;               // w, w x0, w x1
             constexpr int NF = NFW + 1 + (PH::UDOT ? 1 : 0);              // + w u (+ w udot)
-            constexpr bool SFP = P == 3 && NP1 == NQ1 && NP1 * NQ1 * NF * 3 <= SCR * NQ;   // p = 2: slower (A/B)
+            // p = 3 always; p = 2 only for residual-only NURBS launches (A/B: p = 2 Jacobian and the
+            // parametric residual are slower with it)
+            constexpr bool SFP = (P == 3 || (!JAC && MODE == MODE_NURBS)) && NP1 == NQ1 && NP1 * NQ1 * NF * 3 <= SCR * NQ;
             constexpr int NPRE = KS::NC * (1 + 2 + 1) + 1;
             if constexpr (SFP) {
                 double pre[NPRE];
@@ -485,7 +488,8 @@ static size_t fused2d_smem(bool jac) {
     using TL = Tile2<P>;
     constexpr int NQ1 = P + 1, NP1 = P + 1, NQ = NQ1 * NQ1;
     constexpr int NGRP = TL::NWARP * (32 / (NP1 * NP1));
-    constexpr int SFN = P == 3 ? (NP1 * NQ1 * ((MODE == MODE_NURBS ? 3 : 0) + 1 + (PH::UDOT ? 1 : 0)) * 3 + NQ - 1) / NQ : 0;
+    constexpr int SFN = (P == 3 || MODE == MODE_NURBS)
+                            ? (NP1 * NQ1 * ((MODE == MODE_NURBS ? 3 : 0) + 1 + (PH::UDOT ? 1 : 0)) * 3 + NQ - 1) / NQ : 0;
     const int NBN = TL::NB0 * TL::NB1;
     size_t n = 5 * (size_t)NBN + 2 * TL::TE1 * NQ1 * 3 * NP1 + 4 * TL::TE1 * NQ1
                + 2 * TL::TE1 + (size_t)NGRP * ((jac ? L::NE + L::NR : std::max(L::NR, SFN)) * NQ + (P == 3 ? 1 : 0));
