@@ -211,7 +211,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
 }
 
 template <int P, class PH, bool JAC, bool UNI>
-__global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3<P, PH>::MINB : 8)   // residual-only: 8 (A/B: 4 -> 8 = -15 % / -12 % on configs 4 / 5)
+__global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3<P, PH>::MINB : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
           int dbg, int bw) {
