@@ -147,7 +147,8 @@ __device__ __forceinline__ void tsf_column_2d(double (&Kc)[(P + 1) * (P + 1)], c
 #endif
 
 template <int P, class PH, int MODE, bool JAC, int UNI>
-__global__ void __launch_bounds__(32 * Tile2<P>::NWARP, 1)
+// residual-only parametric launches: 2 CTAs per SM (A/B: config 3 residual -6 %; NURBS slower)
+__global__ void __launch_bounds__(32 * Tile2<P>::NWARP, (!JAC && MODE == MODE_PARAM) ? 2 : 1)
 k_fused2d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, int ntile0, int ntile1, int te1, int dbg_,
           const __grid_constant__ UniTab2<P> ut) {
