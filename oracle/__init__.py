@@ -15,6 +15,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _SO = os.path.join(_HERE, "liboracle.so")
+# tests/test_oracle_state_pins.py points this at deliberately MUTATED oracle builds (seeded
+# mutations of the readings) to show that the pins fail on them; never set otherwise.
+_SO_OVERRIDE = os.environ.get("IGA_ORACLE_SO_OVERRIDE")
 
 LAPLACE, CAHN_HILLIARD, NEOHOOKE, NS_VMS, NSK = 0, 1, 2, 3, 4
 PARAMETRIC, NURBS = 0, 1
@@ -34,7 +37,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
+        _lib = C.CDLL(_SO_OVERRIDE if _SO_OVERRIDE else build())
         L = _lib
         P = C.c_void_p
         dp = C.POINTER(C.c_double)
@@ -53,6 +56,8 @@ def lib():
         L.orc_eval_point.argtypes = [P, ip, dp, dp, dp, dp, lp, dp, dp]
         L.orc_eval_point3.restype = C.c_int
         L.orc_eval_point3.argtypes = [P, ip, dp, dp, dp, dp, dp, lp, dp, dp]
+        L.orc_point_state.restype = C.c_int
+        L.orc_point_state.argtypes = [P, C.c_int, dp, dp, dp, ip, dp, dp]
         L.orc_element.restype = C.c_int
         L.orc_element.argtypes = [P, C.c_int, dp, C.c_double, C.c_double, dp, dp, dp, ip, dp, dp, lp]
         L.orc_assemble_dense.restype = C.c_int
@@ -218,6 +223,23 @@ class Space:
             raise ValueError("oracle: detJ <= 0")
         return dict(R=R[:n], dR=d1[:3 * n].reshape(n, 3), ddR=d2[:9 * n].reshape(n, 3, 3),
                     dddR=d3[:27 * n].reshape(n, 3, 3, 3), node=node[:n], x=x, detJ=det.value)
+
+    def point_state(self, kind, params, U, e, xi, Udot=None):
+        """Integrand point state at parametric point xi of element e (orc_point_state): VMS ->
+        dict(tauM, tauC, G, gg, up, pp); Cahn-Hilliard -> dict(M, Mp, Mpp, mup, mupp)."""
+        prm = np.zeros(8)
+        prm[:len(params)] = params
+        U = _f64(U)
+        Udot = _f64(Udot) if Udot is not None else np.zeros_like(U)
+        out = np.zeros(16)
+        ee = np.array(list(e) + [0] * (3 - len(e)), np.int32)
+        xx = np.array(list(xi) + [0.0] * (3 - len(xi)), np.float64)
+        n = lib().orc_point_state(self.h, kind, _d(prm), _d(U), _d(Udot), _i(ee), _d(xx), _d(out))
+        if n < 0:
+            raise ValueError(f"oracle point state failed ({n})")
+        if kind == NS_VMS:
+            return dict(tauM=out[0], tauC=out[1], G=out[2:11].reshape(3, 3), gg=out[11], up=out[12:15], pp=out[15])
+        return dict(M=out[0], Mp=out[1], Mpp=out[2], mup=out[3], mupp=out[4])
 
     def element(self, kind, params, a, b, U, Udot=None, e=(0, 0, 0), Utau=None, want_K=True):
         prm = np.zeros(8)

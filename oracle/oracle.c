@@ -26,9 +26,11 @@
  *     of a row subset scattered by binary search into the Alg. 3 pattern,
  *     with every touched entry required to lie in that pattern.
  *
- * Parity-unpinned pieces (no paper pin): the Cahn-Hilliard mobility and
- * chemical potential (A-10) and the VMS stabilisation (A-14) are readings, guarded by invariants
- * and finite differences in tests/test_oracle_*.py; the weak forms around them are pinned to the
+ * Readings without a paper value: the Cahn-Hilliard mobility and chemical potential (A-10) and
+ * the VMS stabilisation (A-14).  They are pinned to values computed independently of this file
+ * (SURVEY Appendices A and C: G, tau_M, tau_C at config 5; M, mu' and the term-group diagonal
+ * magnitudes at config 3) by tests/test_oracle_state_pins.py, which also shows that seeded
+ * mutations of these formulas fail the pins; the weak forms around them are pinned to the
  * paper's strong forms (test_oracle_ch_strong.py, test_oracle_vms_consistency.py, and the NSK
  * strong-form test in test_oracle_nsk.py).
  */
@@ -793,7 +795,7 @@ typedef struct {
     /* NH */
     double F[3][3], S[3][3], P[3][3], Ci[3][3], J, AA[3][3][3][3];
     /* VMS */
-    double tauM, tauC, rM[3], rC, up[3], pp;
+    double tauM, tauC, rM[3], rC, up[3], pp, G[3][3], gg;
     /* NSK */
     double pv, dpv;
 } orc_pt;
@@ -898,6 +900,9 @@ static void vms_tau(orc_pt *P, const orc_qp *Q, const orc_fields *ftau)
     }
     P->tauM = 1.0 / sqrt(Ct / (dt * dt) + uGu + CI * nu * nu * GG);
     P->tauC = 1.0 / (P->tauM * gg);
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) P->G[i][j] = G[i][j];
+    P->gg = gg;
 }
 
 static void vms_setup(orc_pt *P, const orc_fields *f)
@@ -1237,6 +1242,48 @@ static int element_integrate(const orc_space *s, int kind, const double *prm, do
             }
     if (Qlast) *Qlast = Q;
     return nen;
+}
+
+/* Point state of the integrand at parametric point xi[] of element e[] (tests only: it exposes
+ * the reading-dependent constitutive quantities so that tests/test_oracle_state_pins.py can pin
+ * them to the independently computed values of SURVEY Appendices A and C).  Same call sequence
+ * as element_integrate: eval_point, eval_fields, *_setup.  out[] by kind:
+ *   ORC_NS_VMS:        tauM, tauC, G[3][3] (row-major), g.g, u'[3], p'       (16 doubles)
+ *   ORC_CAHN_HILLIARD: M, M', M'', mu', mu''                                  (5 doubles)
+ * Returns the number of doubles written, or <0. */
+int orc_point_state(const orc_space *s, int kind, const double *prm, const double *U, const double *Udot,
+                    const int *e_in, const double *xi_in, double *out)
+{
+    orc_qp Q;
+    int e[3] = {0, 0, 0};
+    double xi[3] = {0, 0, 0};
+    for (int d = 0; d < s->dim; d++) { e[d] = e_in[d]; xi[d] = xi_in[d]; }
+    if (eval_point(s, e, xi, 1.0, &Q) < 0) return -1;
+    orc_fields f;
+    eval_fields(s, &Q, U, Udot, &f);
+    orc_pt P;
+    memset(&P, 0, sizeof(P));
+    P.kind = kind; P.dim = s->dim; P.m = s->dof; P.prm = prm;
+    if (kind == ORC_NS_VMS) {
+        if (s->dim != 3 || s->dof != 4) return -3;
+        vms_tau(&P, &Q, &f);
+        vms_setup(&P, &f);
+        out[0] = P.tauM;
+        out[1] = P.tauC;
+        for (int i = 0; i < 3; i++)
+            for (int j = 0; j < 3; j++) out[2 + 3 * i + j] = P.G[i][j];
+        out[11] = P.gg;
+        for (int i = 0; i < 3; i++) out[12 + i] = P.up[i];
+        out[15] = P.pp;
+        return 16;
+    }
+    if (kind == ORC_CAHN_HILLIARD) {
+        if (s->dof != 1) return -3;
+        ch_setup(&P, &f);
+        out[0] = P.M; out[1] = P.Mp; out[2] = P.Mpp; out[3] = P.mup; out[4] = P.mupp;
+        return 5;
+    }
+    return -2;
 }
 
 /* Dense element matrix / vector of element (e0,e1,e2) (for tests). nodes[] gets the nen
