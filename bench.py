@@ -31,7 +31,7 @@ import workloads  # noqa: E402
 
 METRIC = "Jacobian assembly quadrature points/sec (fp64)"
 UNIT = "qpts/s"
-DEFAULT_CONFIG = 2          # BASELINE.json configs[1]
+DEFAULT_CONFIG = 5          # BASELINE.json configs[4]: the largest single-GPU config (the headline)
 # Algorithmic model:
 #   F_J  = min over rank / test-side sum-factorised / sum-factorised contraction flops per qpt
 #   F_R  = residual rank-form flops per qpt;  B = CSR values written once + vectors, bytes per qpt
@@ -148,36 +148,11 @@ def dist_env():
 # ------------------------------------------------------------------------------------------
 # reference arm: the CPU oracle (as it stands) on a bounded sample of the same workload
 # ------------------------------------------------------------------------------------------
-def oracle_sample(w, target_s: float):
-    """Pick a node box whose complete rows take ~target_s in the oracle; returns (rows, est)."""
-    import oracle
-    osp = oracle.Space.from_workload(w)
-    nf = w.nfun
-
-    def box_rows(b):
-        import itertools
-        lo = [max(0, f // 2 - b // 2) for f in nf]
-        rows = []
-        for off in itertools.product(*[range(min(b, f)) for f in nf]):
-            node = 0
-            for ax in range(w.dim):
-                node = node * nf[ax] + lo[ax] + off[ax]
-            rows.extend(node * w.dof + c for c in range(w.dof))
-        return np.array(sorted(rows), dtype=np.int64)
-
-    b = 2
-    t0 = time.perf_counter()
-    r = osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, box_rows(b), Udot=w.Udot)
-    t1 = time.perf_counter() - t0
-    per_el = t1 / max(1, r["nvisited"])
-    # elements visited by a b-box ~ (b + p)^d
-    p = w.degree[0]
-    while b < max(nf):
-        nb = b * 2
-        if per_el * (nb + p) ** w.dim > target_s:
-            break
-        b = nb
-    return osp, box_rows(b), b
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 def oracle_rows_threads(osp, w, rows, nthreads):
@@ -191,39 +166,91 @@ def oracle_rows_threads(osp, w, rows, nthreads):
     return sum(r["nvisited"] for r in res)
 
 
-def host_cores():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+class OracleSlab:
+    """CPU baseline: the oracle, as it stands, assembling the COMPLETE rows (all dofs,
+    Jacobian + residual) of a slab of consecutive node rows of the workload -- whole node layers
+    along axis 0 when they fit the time budget (config 5: the 128 x 128 node layers of the periodic
+    box), else a run of consecutive rows inside one layer -- on all host cores (row chunks on
+    threads).  The full assembly time is extrapolated linearly in the row count (every slab of a
+    uniform periodic box costs the same; open boxes to within their boundary layers):
+        value = nqp_total * (rows_in_slab / rows_total) / t_slab   [qpts/s, labelled extrapolation]
+    The slab is sized from a one-pencil calibration so that one timed pass takes ~target_s."""
+
+    def __init__(self, w, target_s: float, threads: int):
+        import oracle
+        self.w, self.T = w, threads
+        self.osp = oracle.Space.from_workload(w)
+        self.nrows = self.osp.ndof
+        nf = w.nfun
+        self.layer = int(np.prod(nf[1:])) * w.dof            # rows of one node layer along axis 0
+        mid = (nf[0] // 2) * self.layer
+        # calibration: one pencil (the last axis) of rows, all dofs, single pass on all threads
+        pen = nf[-1] * w.dof
+        rows = np.arange(mid, mid + pen, dtype=np.int64)
+        t0 = time.perf_counter()
+        oracle_rows_threads(self.osp, w, rows, threads)
+        per_row = (time.perf_counter() - t0) / pen
+        self.target, self.grown = target_s, False
+        self._size(max(pen, int(target_s / max(per_row, 1e-12))))
+
+    def _size(self, want):
+        w, nf = self.w, self.w.nfun
+        pen = nf[-1] * w.dof
+        mid = (nf[0] // 2) * self.layer
+        if want >= self.layer:
+            nl = max(1, min(nf[0], want // self.layer))
+            lo = max(0, nf[0] // 2 - nl // 2) * self.layer
+            self.rows = np.arange(lo, lo + nl * self.layer, dtype=np.int64)
+            self.desc = f"{nl} node layer(s) along axis 0 ({len(self.rows)} rows)"
+        else:
+            n = max(pen, (want // pen) * pen)
+            self.rows = np.arange(mid, mid + n, dtype=np.int64)
+            self.desc = f"{n // pen} pencil(s) of node rows inside one axis-0 layer ({len(self.rows)} rows)"
+
+    def run(self):
+        """One timed pass; returns (seconds, extrapolated qpts/s).  A pass much shorter than the
+        target (the one-pencil calibration overestimates the per-row cost: its row chunks are tiny)
+        grows the slab for the next pass."""
+        t0 = time.perf_counter()
+        oracle_rows_threads(self.osp, self.w, self.rows, self.T)
+        dt = time.perf_counter() - t0
+        rate = self.w.nqp * (len(self.rows) / self.nrows) / dt
+        if dt < 0.5 * self.target and not self.grown:
+            self.grown = True
+            self._size(int(len(self.rows) * min(8.0, self.target / max(dt, 1e-3))))
+        return dt, rate
+
+    def sample_text(self):
+        return (f"complete Jacobian + residual rows (all {self.w.dof} dofs) of {self.desc} of {self.w.name}, "
+                f"C oracle on {self.T} host threads (row chunks); full-assembly rate extrapolated linearly in the "
+                f"row count: nqp_total x rows_sample / rows_total / t_sample")
 
 
 def run_reference(args, w, ws, rank):
+    """Reference arm of this tier: the CPU oracle (as it stands) on the host cores, same workload,
+    metric and unit as the product arm; each step is one bounded slab sample (OracleSlab) so that
+    the whole --steps K --warmup W run ends within a few minutes.  Rank 0 alone runs it."""
     if rank != 0:
         return 0
     import oracle  # noqa: F401  (test infrastructure, allowed for the reference arm)
     budget = 150.0
-    per_step = max(0.5, min(4.0, budget / max(1, args.steps + args.warmup)))
-    osp, rows, b = oracle_sample(w, per_step)
-    times, qp = [], []
-    nq = int(np.prod(w.quad))
+    per_step = max(2.0, min(20.0, budget / max(1, args.steps + args.warmup)))
     T = host_cores()
+    slab = OracleSlab(w, per_step, T)
+    times, vals = [], []
     for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        nvis = oracle_rows_threads(osp, w, rows, T)
-        dt = time.perf_counter() - t0
+        dt, v = slab.run()
         if it >= args.warmup:
             times.append(dt)
-            qp.append(nvis * nq)
-    value = sum(qp) / sum(times)
-    sample = (f"complete rows of a {b}^{w.dim}-node box (all {w.dof} dofs, {len(rows)} rows) of {w.name}: "
-              f"{qp[0] // nq if qp else 0} element integrations x {nq} qpts per step, C oracle on {T} host "
-              f"threads (row chunks)")
+            vals.append(v)
+    value = len(vals) / sum(1.0 / v for v in vals)          # = total qpts-equivalent / total time
+    ms = 1e3 * w.nqp / value
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": w.name, "nqp_per_step": int(qp[0]), "l2": "host"},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle", "sample": sample},
+           "config": {"workload": w.name, "nqp": w.nqp, "l2": "host",
+                      "sample_seconds_per_step": sum(times) / len(times)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": "oracle", "sample": slab.sample_text()},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -392,13 +419,22 @@ def run_iga(args, w, ws, rank, local):
         alg = 8.0 * sp.nnz
         bound, unit, peak = "hbm", "GB/s", peaks.get("hbm_gbs", 6650.0)
         achieved = alg / (avg_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, ncu_k = None, {}
     summ = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(summ):
         try:
-            traffic = json.load(open(summ)).get(w.name, {}).get(dom, {}).get("dram_bytes_per_launch")
+            ncu_k = json.load(open(summ)).get(w.name, {}).get(dom, {})
+            traffic = ncu_k.get("dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            ncu_k = {}
+    # executed FP64 work of the same kernel (ncu op counters, profiles/ncu_summary.json): exposes
+    # redundant work against the algorithmic model
+    executed = None
+    if ncu_k.get("exec_fp64_flop_per_launch") and dom in ASSEMBLY:
+        ef = float(ncu_k["exec_fp64_flop_per_launch"])
+        executed = {"flop_per_qpt": ef / nqp_launch, "model_flop_per_qpt": F_J[cid] + F_R[cid],
+                    "executed_over_model": ef / alg, "tflops_at_bench_time": ef / (avg_ms * 1e-3) / 1e12,
+                    "fp64_pipe_pct_ncu": ncu_k.get("fp64_pipe_pct"), "source": ncu_k.get("source")}
     t_roof = max((F_J[cid] + F_R[cid]) * sp.nqp / (P64_NOMINAL_TFLOPS * 1e12),
                  B_QP[cid] * sp.nqp / (peaks.get("hbm_gbs", 6650.0) * 1e9))
     clocks = clk.summary()
@@ -406,31 +442,12 @@ def run_iga(args, w, ws, rank, local):
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         import oracle  # noqa: F401  (bench's cpu_baseline leg may execute the oracle)
-        osp, rows, b = oracle_sample(w, 4.0)
-        nq = int(np.prod(w.quad))
-        t0 = time.perf_counter()
-        r = osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, rows, Udot=w.Udot)
-        dt = time.perf_counter() - t0
-        reps = 1
-        while time.perf_counter() - t0 < 10.0 and reps < 8:
-            osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, rows, Udot=w.Udot)
-            reps += 1
-        dt = (time.perf_counter() - t0) / reps
-        v1 = r["nvisited"] * nq / dt
-        # the same sample on all host cores (SURVEY O-11): row chunks on threads
         T = host_cores()
-        vT, cores = v1, 1
-        if T > 1:
-            t0 = time.perf_counter()
-            nvis, repsT = 0, 0
-            while repsT < 2 or (time.perf_counter() - t0 < 5.0 and repsT < 16):
-                nvis += oracle_rows_threads(osp, w, rows, T)
-                repsT += 1
-            vT, cores = nvis * nq / (time.perf_counter() - t0), T
-        cpu = {"value": vT, "unit": UNIT, "cores": cores, "kind": "oracle", "value_1thread": v1,
-               "sample": f"complete Jacobian+residual rows of a {b}^{w.dim}-node box ({len(rows)} rows, "
-                         f"{r['nvisited']} elements x {nq} qpts) of {w.name}; C oracle on {cores} host threads "
-                         f"(row chunks; 1 thread: {v1:.3g} qpts/s)"}
+        slab = OracleSlab(w, 15.0, T)
+        slab.run()                              # sizes the slab (grows it if the calibration overshot)
+        dt, vT = slab.run()
+        cpu = {"value": vT, "unit": UNIT, "cores": T, "kind": "oracle", "sample": slab.sample_text(),
+               "sample_seconds": dt}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -448,7 +465,8 @@ def run_iga(args, w, ws, rank, local):
                      if unit == "TFLOP/s" else "MEASURED_PEAKS.json hbm_gbs",
                      "kernel_ms": {k: v[1] / v[0] for k, v in kern.items()},
                      "kernel_launches_per_step": {k: v[0] / args.steps for k, v in kern.items()},
-                     "step_roofline_ms": t_roof * 1e3, "step_frac": t_roof * 1e3 / step_ms},
+                     "step_roofline_ms": t_roof * 1e3, "step_frac": t_roof * 1e3 / step_ms,
+                     "executed": executed},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(2 * 8 * sp.nrows * ws),
                 "d2h_bytes_per_step": int(8 * (sp.nnz + sp.nrows) * ws), "ms_per_step": e2e_t},
@@ -650,12 +668,34 @@ def main():
     ap.add_argument("--impl", default="iga", choices=["iga", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--opt", action="append", default=[], help="libiga option key=value (experiments)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="--gpus N > 1: weak = every GPU keeps the named config's element count (the global "
-                         "mesh grows with the box decomposition); strong = the named mesh is split N ways")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="--gpus N > 1: strong = the named mesh is split N ways (default for the 3D configs, "
+                         "incl. the headline config 5: the north star's 8-GPU target is config-5 strong "
+                         "scaling); weak = every GPU keeps the named config's element count (default for 2D)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "iga" else args.warmup
+    if args.scaling is None:
+        args.scaling = "strong" if args.config in (4, 5, 8) else "weak"
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run (127.0.0.1)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch with torch.distributed.run "
+              f"--nproc-per-node {args.gpus} (or without WORLD_SIZE to let bench.py launch the ranks)",
+              file=sys.stderr)
+        return 2
+    if args.impl == "iga":
+        import torch
+        if torch.cuda.device_count() < ws:
+            print(f"bench.py: {ws} ranks but only {torch.cuda.device_count()} CUDA device(s) visible", file=sys.stderr)
+            return 2
     n = args.n
     if ws > 1 and args.scaling == "weak":
         dim = workloads.make(args.config, n=6).dim

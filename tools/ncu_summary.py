@@ -11,7 +11,10 @@ keys = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'smsp__sass_inst_executed_op_shared_atom.sum', 'smsp__sass_inst_executed_op_shared_ld.sum',
         'smsp__sass_inst_executed_op_shared_st.sum', 'smsp__sass_inst_executed_op_global_red.sum',
         'lts__t_sectors_op_red.sum', 'sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active',
-        'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum']
+        'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum',
+        'smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed',
+        'smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed',
+        'smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed', 'smsp__cycles_elapsed.avg']
 for i, name in enumerate(h):
     if name in keys:
         print(f"{name:70s} {v[i]:>18s} {u[i]}")

@@ -10,7 +10,7 @@ import workloads  # noqa: E402
 
 summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
 summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", f"{tag}_c*_k_*.ncu-rep"))):
+for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", "**", f"{tag}_c*_k_*.ncu-rep"), recursive=True)):
     m = re.search(r"_c(\d)_(k_\w+)\.ncu-rep", rep)
     cid, kern = int(m.group(1)), m.group(2)
     name = workloads.make(cid, n=4).name.rsplit("_", 1)[0]
@@ -32,9 +32,21 @@ for rep in sorted(glob.glob(os.path.join(ROOT, "gpurun_out", f"{tag}_c*_k_*.ncu-
         x, u = float(v[0]), v[1].lower()
         return x * {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1, "msecond": 1, "s": 1e3, "second": 1e3}.get(u, 1)
     rd, wr = tobytes(vals["dram__bytes_read.sum"]), tobytes(vals["dram__bytes_write.sum"])
+
+    def cnt(k):
+        try:
+            return float(vals[k][0])
+        except (KeyError, ValueError):
+            return float("nan")
+    # executed FP64 flops of the launch: 2 x DFMA + DADD + DMUL thread-instructions
+    # (ncu reports them as rates per elapsed cycle summed over SMSPs; x the elapsed SMSP cycles)
+    pc = "smsp__sass_thread_inst_executed_op_{}_pred_on.sum.per_cycle_elapsed"
+    exec_flop = (2 * cnt(pc.format("dfma")) + cnt(pc.format("dadd")) + cnt(pc.format("dmul"))) * \
+        cnt("smsp__cycles_elapsed.avg")
     summ.setdefault(wname, {})[kern] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                                         "ncu_ms": toms(vals["gpu__time_duration.sum"]),
                                         "fp64_pipe_pct": float(vals.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", ("nan",))[0]),
+                                        "exec_fp64_flop_per_launch": exec_flop,
                                         "source": os.path.basename(rep), "tag": tag}
 json.dump(summ, open(summ_path, "w"), indent=1)
 print(json.dumps(summ, indent=1))
