@@ -44,3 +44,25 @@ def gather_rows(rowptr, cols, vals, rows):
     sub_rp = np.zeros(len(rows) + 1, np.int64)
     sub_rp[1:] = np.cumsum(lens)
     return sub_rp, np.asarray(cols)[idx], (None if vals is None else np.asarray(vals)[idx])
+
+
+def oracle_rows_parallel(osp, w, rows, threads=None, **kw):
+    """The oracle's row-subset assembly (complete rows) on host threads: the sorted rows are cut
+    into contiguous chunks, each assembled by the unchanged oracle call (ctypes releases the GIL),
+    and the per-chunk CSR pieces are concatenated."""
+    import concurrent.futures as cf
+    import os
+    T = threads or max(1, len(os.sched_getaffinity(0)))
+    chunks = [c for c in np.array_split(np.asarray(rows, np.int64), T) if len(c)]
+    with cf.ThreadPoolExecutor(max_workers=len(chunks)) as ex:
+        parts = list(ex.map(lambda c: osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, c, Udot=w.Udot, **kw),
+                            chunks))
+    rp = [np.zeros(1, np.int64)]
+    off = 0
+    for p in parts:
+        rp.append(p["rowptr"][1:] + off)
+        off += p["rowptr"][-1]
+    return dict(rowptr=np.concatenate(rp), cols=np.concatenate([p["cols"] for p in parts]),
+                vals=np.concatenate([p["vals"] for p in parts]), F=np.concatenate([p["F"] for p in parts]),
+                touched=np.concatenate([p["touched"] for p in parts]),
+                nvisited=sum(p["nvisited"] for p in parts))

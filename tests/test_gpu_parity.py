@@ -8,7 +8,7 @@ import pytest
 
 import oracle
 import workloads
-from parity_util import ROW_TOL, gather_rows, rowmax_rel_err, vec_rel_err
+from parity_util import ROW_TOL, gather_rows, oracle_rows_parallel, rowmax_rel_err, vec_rel_err
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -113,8 +113,10 @@ def test_full_size_probe_rows(cid):
     rp = rp_d.cpu().numpy()
     osp = oracle.Space.from_workload(w)
     assert sp.ndof == osp.ndof and sp.nrows == osp.ndof
-    rows = workloads.probe_rows(w, nblocks_random=2, block=3 if cid not in (5, 8) else 2)
-    ref = osp.assemble_rows(w.phys, w.params, w.a, w.b, w.U, rows, Udot=w.Udot)
+    # SURVEY O-10: 3^d structured 5^d probe blocks (seam / partition plane / interior per axis) and
+    # 64 seeded random ones, complete rows, the oracle on the host cores
+    rows = workloads.probe_rows_o10(w)
+    ref = oracle_rows_parallel(osp, w, rows)
     idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows])
     idx_d = torch.from_numpy(idx).to(dev)
     sci = ci_d[idx_d].cpu().numpy()
@@ -137,6 +139,27 @@ def test_full_size_probe_rows(cid):
                                   rl.ctypes.data_as(C.POINTER(C.c_int64)), None)
     assert np.array_equal(np.diff(rp), rl)
     assert bool(torch.isfinite(vals_d).all())
+
+
+@pytest.mark.parametrize("cid", [4, 5, 6, 8])
+def test_full_size_full_pattern_streamed(cid):
+    """O-10 "the pattern check is always full, streamed row by row": every row of the BASELINE-size
+    CSR (config 5: 4.19e9 column indices, 16.8 GB on the device) against the oracle's Alg. 3
+    pattern, in row chunks."""
+    iga = _gpu()
+    w = workloads.make(cid)
+    sp = iga.Space.from_workload(w)
+    rp_d, ci_d = sp.csr_pattern()
+    osp = oracle.Space.from_workload(w)
+    rp = rp_d.cpu().numpy()
+    assert rp[0] == 0 and rp[-1] == sp.nnz == ci_d.numel()
+    chunk = max(1, (1 << 26) // max(1, int(np.diff(rp[:2])[0])))
+    for r0 in range(0, sp.nrows, chunk):
+        r1 = min(sp.nrows, r0 + chunk)
+        orp, oci = osp.pattern_rows(np.arange(r0, r1, dtype=np.int64))
+        assert np.array_equal(rp[r0:r1 + 1] - rp[r0], orp), f"row_ptr differs in rows [{r0}, {r1})"
+        got = ci_d[int(rp[r0]):int(rp[r1])].cpu().numpy()
+        assert np.array_equal(got, oci), f"col_idx differs in rows [{r0}, {r1})"
 
 
 @pytest.mark.parametrize("cid", [1, 2, 3, 7])

@@ -310,3 +310,71 @@ def probe_rows(w: Workload, nblocks_random: int = 4, block: int = 3, seed: int =
             for c in range(w.dof):
                 rows.add(node * w.dof + c)
     return np.array(sorted(rows), dtype=np.int64)
+
+
+def custom(dim: int, degree, knots, periodic=None, continuity=None, dof: int = 1, phys: int = PHYS_LAPLACE,
+           params=(1.0, 1.0, 0.0), a: float = 0.0, b: float = 1.0, geometry: int = GEOM_PARAMETRIC,
+           field: str = "uniform", seed: int = 0, name: str = "custom") -> Workload:
+    """A seeded workload on explicit OPEN knot vectors (GPU parity of the knot-driven cases: repeated
+    interior knots, non-uniform spacing, periodic C^k with k < p-1, p = 1, mixed degrees).
+
+    geometry NURBS (open axes only): control points at the Greville abscissae of each axis plus a
+    smooth seeded shear, weights ~ U[0.8, 1.2] -- a non-affine rational map (both sides check
+    detJ > 0).  field: "uniform" U ~ U[-1, 1]; "ch" c = 0.63 + U[-0.05, 0.05]; "small" 0.02 U[-1, 1]
+    (hyperelastic displacements).  Udot ~ 0.1 U[-1, 1]."""
+    rng = np.random.default_rng(seed)
+    deg = list(degree) if isinstance(degree, (list, tuple)) else [int(degree)] * dim
+    kn = [np.asarray(k, dtype=np.float64) for k in knots]
+    per = list(periodic) if periodic is not None else [0] * dim
+    cont = list(continuity) if continuity is not None else [p - 1 for p in deg]
+    nopen = [len(kn[d]) - deg[d] - 1 for d in range(dim)]
+    nf = [nopen[d] - (cont[d] + 1) if per[d] else nopen[d] for d in range(dim)]
+    nel = [len(np.unique(kn[d])) - 1 for d in range(dim)]
+    ctrl = weights = None
+    if geometry == GEOM_NURBS:
+        assert not any(per), "custom NURBS geometry: open axes only (periodic nets go through Alg. 2, config 7)"
+        g = [_greville(kn[d], deg[d]) for d in range(dim)]
+        grids = np.meshgrid(*g, indexing="ij")
+        ctrl = np.stack(grids, axis=-1).copy()
+        span = [kn[d][-1] - kn[d][0] for d in range(dim)]
+        for d in range(dim):
+            o = (d + 1) % dim
+            ctrl[..., d] += 0.04 * span[d] * np.sin(np.pi * (grids[o] - kn[o][0]) / span[o])
+        weights = rng.uniform(0.8, 1.2, nopen)
+    nd = int(np.prod(nf)) * dof
+    if field == "ch":
+        U = 0.63 + rng.uniform(-0.05, 0.05, nd)
+    elif field == "small":
+        U = 0.02 * rng.uniform(-1.0, 1.0, nd)
+    else:
+        U = rng.uniform(-1.0, 1.0, nd)
+    Udot = 0.1 * rng.uniform(-1.0, 1.0, nd)
+    return Workload(0, name, dim, deg, kn, per, cont, dof, [p + 1 for p in deg], geometry, ctrl, weights, phys,
+                    list(params), a, b, U, Udot, nel, nf)
+
+
+def probe_rows_o10(w: Workload, block: int = 5, nrandom: int = 64, seed: int = 5) -> np.ndarray:
+    """SURVEY O-10 probe set: block^d node boxes (all dofs) centred, per axis, at every combination
+    of {periodic seam / first node 0, the partition plane N/2, the interior N/4} (3^d structured
+    probes), plus `nrandom` seeded random boxes.  Open axes clamp a box to the node range, periodic
+    axes wrap it.  Returns sorted unique global dof rows."""
+    nf, d = w.nfun, w.dim
+    rng = np.random.default_rng(seed)
+    centres = [list(c) for c in itertools.product(*[(0, f // 2, f // 4) for f in nf])]
+    for _ in range(nrandom):
+        centres.append([int(rng.integers(0, f)) for f in nf])
+    half = block // 2
+    rows = set()
+    for c in centres:
+        for off in itertools.product(range(-half, block - half), repeat=d):
+            node = 0
+            for ax in range(d):
+                g = c[ax] + off[ax]
+                if w.periodic[ax]:
+                    g %= nf[ax]
+                else:
+                    g = min(max(g, 0), nf[ax] - 1)
+                node = node * nf[ax] + g
+            for m in range(w.dof):
+                rows.add(node * w.dof + m)
+    return np.array(sorted(rows), dtype=np.int64)
