@@ -57,14 +57,16 @@ typedef struct iga_space_s *iga_space;    /* opaque, library-owned */
 typedef enum { IGA_GEOM_PARAMETRIC = 0, IGA_GEOM_NURBS = 1 } iga_geom;
 
 typedef struct {
-    int dim;                       /* 1..3 (parametric dim = spatial dim)                      */
-    int degree[3];                 /* p_d in [1,3] in this build                               */
+    int dim;                       /* 2 or 3 (parametric dim = spatial dim); 1 => IGA_ERR_PARAM */
+    int degree[3];                 /* p_d in [1,3]; the form calls need one p on every axis in
+                                      this build (IGA_ERR_PARAM otherwise)                       */
     int n_knots[3];                /* knots on axis d                                          */
     const double *knots[3];        /* host; OPEN (clamped) knot vectors, non-decreasing        */
     int periodic[3];               /* 1 => unclamp axis d with Alg. 1 for C^k periodicity      */
     int periodic_continuity[3];    /* k_d in [0, p_d-1] (read only when periodic)              */
     int dof;                       /* m dofs per node, 1..4                                    */
-    int quad[3];                   /* Gauss points per dimension; 0 => p_d+1 (only p+1 here)   */
+    int quad[3];                   /* Gauss points per dimension: 0 or p_d+1 (A-6); any other
+                                      count => IGA_ERR_PARAM in this build                       */
     int geometry;                  /* iga_geom: PARAMETRIC => x = xi (knots carry coordinates)  */
     const double *ctrl;            /* host [n0][n1][n2][dim] Euclidean control points (NURBS)  */
     const double *weights;         /* host [n0][n1][n2] projective weights > 0, NULL => 1      */

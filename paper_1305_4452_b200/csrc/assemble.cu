@@ -366,11 +366,12 @@ static iga_status dispatch_p(iga_space_s *s, const iga_phys *ph, double a, doubl
                              const double *Ud, double *val, double *F, cudaStream_t st) {
     const int p = s->p[0];
     switch (p) {
+    case 1: return dispatch_mode<DIM, 1, PH>(s, ph, a, b, U, Ud, val, F, st);
     case 2: return dispatch_mode<DIM, 2, PH>(s, ph, a, b, U, Ud, val, F, st);
     case 3: return dispatch_mode<DIM, 3, PH>(s, ph, a, b, U, Ud, val, F, st);
     default: break;
     }
-    set_error("degree must be 2 or 3 (equal on all axes) in this build");
+    set_error("degree must be 1, 2 or 3 (equal on all axes) in this build");
     return IGA_ERR_PARAM;
 }
 

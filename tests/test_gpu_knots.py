@@ -2,7 +2,7 @@
 
   * Fig. 3's knot vector U = (0,0,0,0,2,4,4,6,6,6,8,8,8,8), p = 3 (repeated interior knots, reduced
     continuity: the Alg. 3 stencils of P:468-501 with variable row widths), tensored with itself;
-  * non-uniform open knot spacing (p = 2, 3) and mixed degrees per axis;
+  * non-uniform open knot spacing (p = 2, 3); mixed degrees per axis are rejected (iga.h);
   * periodic C^k with k < p - 1 (Fig. 2 / Alg. 1 for k = 0 and k = p - 2, P:393-399);
   * p = 1 (2D and 3D);
   * Hessians on non-affine rational maps through the assembly kernels ((ddrational) P:237-247,
@@ -107,7 +107,7 @@ def _case(name):
 
 CASES = ["fig3_lap", "fig3_ch", "fig3_lap_nurbs", "fig3_ch_nurbs",
          "nonuni_p2_lap_param", "nonuni_p2_ch_param", "nonuni_p3_ch_param", "nonuni_p2_ch_nurbs",
-         "nonuni_p3_lap_nurbs", "mixed_p23_ch",
+         "nonuni_p3_lap_nurbs",
          "per_p2_k0_lap", "per_p2_k0_ch", "per_p3_k0_ch", "per_p3_k1_ch", "per_p3_k1_lap",
          "p1_lap", "p1_per_lap", "p1_3d_nh",
          "nurbs3d_lap", "nurbs3d_ch", "nurbs3d_nh",
@@ -153,3 +153,20 @@ def test_knot_and_geometry_parity(name, path):
         assert fused in ran, f"{name}/{path}: expected {fused}, ran {sorted(ran)}"
     if path == "split":
         assert not any(k.startswith("k_fused") for k in ran), sorted(ran)
+
+
+def test_mixed_degrees_rejected():
+    """include/iga.h: one degree on every axis in this build -> the form calls return IGA_ERR_PARAM
+    synchronously (the space and its Alg. 3 pattern are still built: checked bit-exact here)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1305_4452_b200 as iga
+    w, _ = _case("mixed_p23_ch")
+    sp = iga.Space.from_workload(w)
+    rp, ci = sp.csr_pattern()
+    orp, oci = oracle.Space.from_workload(w).pattern()
+    assert np.array_equal(rp.cpu().numpy(), orp) and np.array_equal(ci.cpu().numpy(), oci)
+    U = torch.from_numpy(w.U).cuda()
+    with pytest.raises(iga.IgaError) as ei:
+        sp.form_jacobian(iga.make_phys(w.phys, w.params), w.a, w.b, U, U)
+    assert ei.value.code == 1
