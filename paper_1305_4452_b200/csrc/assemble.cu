@@ -315,13 +315,11 @@ static iga_status run_form(iga_space_s *s, const iga_phys *phys, double a, doubl
     if (nb_max > s->nel_local) nb_max = s->nel_local;
     nb_max = std::min<long long>(nb_max, (1LL << 31) / NQ - 1);
     const size_t dsm = (size_t)NQ * ((jac ? L::NE : 0) + L::NR) * sizeof(double);
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[jac]) {
+    {   // per-device attribute: set on the current device before every launch
         cudaError_t ce;
         if (jac) ce = cudaFuncSetAttribute(k_contract<DIM, P, PH, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         else ce = cudaFuncSetAttribute(k_contract<DIM, P, PH, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         if (ce != cudaSuccess) { set_error(cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
-        attr_set[jac] = true;
     }
     double *Dt = s->work;
     for (long long e0 = 0; e0 < s->nel_local; e0 += nb_max) {

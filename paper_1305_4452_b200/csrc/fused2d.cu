@@ -505,12 +505,10 @@ static iga_status launch_k2(iga_space_s *s, const Prm &prm, double a, double b, 
     using TL = Tile2<P>;
     constexpr int NT = 32 * TL::NWARP;
     const size_t smem = fused2d_smem<P, PH, MODE>(JAC);
-    static bool attr = false;
-    if (!attr) {
+    {   // the opt-in is a per-device attribute: set it on the current device before every launch
         cudaError_t ce = cudaFuncSetAttribute(k_fused2d<P, PH, MODE, JAC, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)smem);
         if (ce != cudaSuccess) { set_error(std::string("fused2d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
-        attr = true;
     }
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2d<P, PH, MODE, JAC, UNI>, NT, smem);

@@ -324,12 +324,10 @@ static iga_status run_fused2dm(iga_space_s *s, const iga_phys *phys, double a, d
     Prm prm;
     for (int i = 0; i < 8; i++) prm.p[i] = phys->p[i];
     const bool jac = val != nullptr;
-    static bool attr[2] = {false, false};
-    if (!attr[jac]) {
+    {   // per-device attribute: set on the current device before every launch
         cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused2dm<P, PH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FF::SMEM)
                              : cudaFuncSetAttribute(k_fused2dm<P, PH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FF::SMEM);
         if (ce != cudaSuccess) { set_error(std::string("fused2dm smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
-        attr[jac] = true;
     }
     int occ = 1;
     if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused2dm<P, PH, true>, 32 * FF::WARPS, FF::SMEM);

@@ -645,12 +645,10 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
     const bool jac = val != nullptr;
     const bool jac_ = val != nullptr;
     const size_t smem = jac_ ? FF::SMEM : FF::SMEM_RES;
-    static bool attr[2] = {false, false};
-    if (!attr[jac]) {
+    {   // per-device attribute: set on the current device before every launch
         cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused3d<P, PH, true, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                              : cudaFuncSetAttribute(k_fused3d<P, PH, false, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (ce != cudaSuccess) { set_error(std::string("fused3d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
-        attr[jac] = true;
     }
     int occ = 1;
     if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, true, UNI>, FF::NT, smem);

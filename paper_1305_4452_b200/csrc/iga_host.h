@@ -64,6 +64,9 @@ struct iga_space_s {
     void *gm_buf[3] = {nullptr, nullptr, nullptr};
     int gm_host_ctrl = 0;                // option "gmres_host": host-side Arnoldi control even at rtol = 0
     size_t gm_cap[3] = {0, 0, 0};
+    // distributed-GMRES workspace (gmres_group): the k-th allocation of a solve reuses slot k when
+    // it is large enough, so repeated solves (one per Newton iteration) do not cudaMalloc/Free
+    std::vector<std::pair<void *, size_t>> dr_cache;
     // kernel timing hook (iga_profile_*)
     struct ProfRec { const char *name; cudaEvent_t a, b; };
     bool prof_on = false;

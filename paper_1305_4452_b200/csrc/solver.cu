@@ -527,7 +527,9 @@ __global__ void k_arn_start(ArnLayout Lo, double *base) {
     c->beta = beta;
     c->scale = beta > 0.0 ? 1.0 / beta : 1.0;
     c->res = beta;
-    c->jstop = Lo.m;
+    // beta = 0: the start vector already solves the system; no column is used, so the update
+    // y is 0 (not -0/0) and x stays as it is
+    c->jstop = beta > 0.0 ? Lo.m : 0;
     c->need2 = 1;
 }
 
@@ -596,7 +598,8 @@ __global__ void __launch_bounds__(256) k_arn_solve(ArnLayout Lo, double *base, i
         for (int i = j - 1; i >= 0; i--) {                 // sy = -y
             double t = sy[i];
             for (int k = i + 1; k < j; k++) t += sH[i * j + k] * sy[k];
-            sy[i] = -t / sH[i * j + i];
+            const double d = sH[i * j + i];
+            sy[i] = d != 0.0 ? -t / d : 0.0;                // zero pivot (exact breakdown): drop the direction
         }
     __syncthreads();
     for (int t = threadIdx.x; t < jmax; t += blockDim.x) yn[t] = t < j ? sy[t] : 0.0;
@@ -1126,14 +1129,21 @@ struct DRank {
     uint8_t *Lc = nullptr, *Uc = nullptr;
     int W = 0;
     bool ell = false;
-    std::vector<void *> mem;
+    size_t nalloc = 0;   // allocations of this solve; slot k of s->dr_cache backs the k-th one
     template <class T> T *alloc(size_t count) {
-        void *p = nullptr;
-        if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-        mem.push_back(p);
-        return (T *)p;
+        const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+        auto &c = s->dr_cache;
+        if (c.size() <= nalloc) c.resize(nalloc + 1, {nullptr, 0});
+        auto &slot = c[nalloc++];
+        if (slot.second < bytes) {
+            if (slot.first) cudaFree(slot.first);
+            slot = {nullptr, 0};
+            void *p = nullptr;
+            if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+            slot = {p, bytes};
+        }
+        return (T *)slot.first;
     }
-    ~DRank() { for (void *p : mem) cudaFree(p); }
 };
 
 // host-only: the ghost-exchange messages of the rank at coordinate rc (no GPU; also behind the
@@ -1353,11 +1363,10 @@ iga_status gmres_group(int nr, iga_space_s *const *sp, const int64_t *const *rp,
         cudaMemsetAsync(D.xe, 0, sizeof(double) * (size_t)D.next, st);
     }
     // pointer table for the in-process all-reduce
-    double **dptrs = nullptr;
     std::vector<double *> hptrs(nr);
     for (int r = 0; r < nr; r++) hptrs[r] = R[r].dh;
-    if (cudaMalloc(&dptrs, sizeof(double *) * nr) != cudaSuccess) { cudaGetLastError(); set_error("gmres ptrs"); return IGA_ERR_NOMEM; }
-    R[0].mem.push_back(dptrs);
+    double **dptrs = R[0].alloc<double *>(nr);
+    if (!dptrs) { set_error("gmres ptrs"); return IGA_ERR_NOMEM; }
     cudaMemcpyAsync(dptrs, hptrs.data(), sizeof(double *) * nr, cudaMemcpyHostToDevice, st);
     auto allreduce = [&](int cnt) -> iga_status {
         if (local) {

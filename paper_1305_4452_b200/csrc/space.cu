@@ -276,6 +276,7 @@ static void free_space(iga_space_s *s) {
     for (cudaEvent_t e : s->prof_pool) cudaEventDestroy(e);
     for (void *p : s->allocs) cudaFree(p);
     for (void *p : s->gm_buf) if (p) cudaFree(p);
+    for (auto &c : s->dr_cache) if (c.first) cudaFree(c.first);
     cudaSetDevice(prev);
     delete s;
 }

@@ -96,6 +96,28 @@ def test_zero_rhs_and_bad_args():
         sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(b), restart=0)
 
 
+@pytest.mark.parametrize("restart,maxit", [(30, 30), (5, 12)])
+def test_exact_start_vector_fixed_budget(restart, maxit):
+    """the device-driven fixed-budget GMRES (rtol = 0) with x0 = the exact solution
+    (zero initial residual, beta = 0) must leave x unchanged and finite, not turn it into NaN."""
+    iga = _gpu()
+    w, rp, ci, v, b = _system(3, 8)
+    sp = iga.Space.from_workload(w)
+    rng = np.random.default_rng(12)
+    xs = rng.uniform(-1.0, 1.0, b.size)
+    bb = krylov.csr_matvec(rp, ci, v, xs)                 # x0 = xs solves A x = bb up to rounding
+    x0 = xs
+    x, it, rr = sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(bb), x=_dev(x0), restart=restart, maxit=maxit, rtol=0.0,
+                         precond=2, block_rows=32)
+    xg = x.cpu().numpy()
+    assert np.all(np.isfinite(xg)), "NaN / Inf in x"
+    assert np.max(np.abs(xg - x0)) <= 1e-10 * np.max(np.abs(x0))
+    # an exactly zero right-hand side with x0 = 0 on the same fixed-budget path
+    z, itz, rrz = sp.gmres(_dev(rp), _dev(ci), _dev(v), _dev(np.zeros_like(b)), x=_dev(np.zeros_like(b)),
+                           restart=restart, maxit=maxit, rtol=0.0, precond=2, block_rows=32)
+    assert float(z.abs().max()) == 0.0
+
+
 def test_full_size_newton_step_config3():
     """Config 3 at full size (1024^2 Cahn-Hilliard, 1M rows): the libiga Jacobian and residual,
     then the paper's 30 GMRES iterations; the reported residual is the true one (checked with
