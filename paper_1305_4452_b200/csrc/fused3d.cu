@@ -24,6 +24,10 @@
 #include "iga_host.h"
 #include "pointwise.cuh"
 
+#ifndef IGA_Q1U
+#define IGA_Q1U 1   // experiments: unroll factor of the contraction's q1 loop
+#endif
+
 namespace iga {
 
 template <int P>
@@ -32,6 +36,10 @@ struct UniTab {
     double qw[3][P + 1];
     double hp[3];
 };
+
+// leading doubles of PH::State that the Jacobian coefficients (dcol) read; 0 => the whole state
+template <class PH, class = void> struct PhysJState { static constexpr int value = 0; };
+template <class PH> struct PhysJState<PH, std::void_t<decltype(PH::JSTATE)>> { static constexpr int value = PH::JSTATE; };
 
 template <int P, class PH>
 struct F3 {
@@ -51,26 +59,43 @@ struct F3 {
     static constexpr bool SYMJ = std::is_same<PH, PhysNeoHooke>::value;
     // resident CTAs per SM the register budget is sized for (m = 3: 96 threads -> 3 CTAs; m = 1:
     // one-warp CTAs (27 trial functions), 8 per SM)
-    static constexpr int MINB = M == 1 ? 8 : M == 3 ? 3 : 2;
-    // shared-memory carve-up (in doubles)
-    static constexpr int O_U = 0;                            // [NEN][M]
-    static constexpr int O_UD = O_U + NEN * M;               // [NEN][M]
-    static constexpr int O_TAB = O_UD + NEN * M;             // [3][NQ1][3][NP1]
+#ifndef IGA_VMS_MINB
+#define IGA_VMS_MINB 2
+#endif
+    static constexpr int MINB = M == 1 ? 8 : M == 3 ? 3 : IGA_VMS_MINB;
+    // doubles of the per-point state that the Jacobian coefficients read (the leading members;
+    // VMS keeps its residual coefficients rN, rG after them): only these go to shared memory
+    static constexpr int STJ = PhysJState<PH>::value > 0 ? PhysJState<PH>::value : STD;
+    // shared-memory carve-up (in doubles).  Everything that dies before the coefficient blocks are
+    // built (field kinds Phi, U_e, Udot_e, residual coefficients, node numbers) overlays the D
+    // region: the element's residual F_e is formed before phase 4 for that reason.  VMS fits three
+    // CTAs per SM this way (<= 75 KB each).
+    static constexpr int O_TAB = 0;                          // [3][NQ1][3][NP1]
     static constexpr int O_QW = O_TAB + 3 * NQ1 * 3 * NP1;   // [3][NQ1]
     static constexpr int O_QX = O_QW + 3 * NQ1;              // [3][NQ1]
     static constexpr int O_HP = O_QX + 3 * NQ1;              // [4]
-    static constexpr int O_ST = O_HP + 4;                    // [NQ][STD]
-    static constexpr int O_DV = O_ST + NQ * STD;             // [NQ]
-    static constexpr int O_R = O_DV + NQ;                    // [NR][NQ]
-    static constexpr int O_D = (O_R + NR * NQ + 1) / 2 * 2;  // [NQ][DQS]  (16-byte aligned)
-    static constexpr int O_PHI = O_D;                        // [NQ][M][NKS+1]  overlays D (dead before D)
-    static constexpr int O_RS = O_D + NQ * DQS;              // long long [NEN*M] row starts
-    static constexpr int O_ND = O_RS + NEN * M;              // long long [NEN] nodes
-    static constexpr size_t SMEM = (size_t)(O_ND + NEN) * sizeof(double);
-    // residual only: no coefficient blocks -- row starts (unused) and node numbers right after Phi
-    static constexpr int O_RS_RES = O_PHI + NQ * M * (NKS + 1);
-    static constexpr int O_ND_RES = O_RS_RES + NEN * M;
-    static constexpr size_t SMEM_RES = (size_t)(O_ND_RES + NEN) * sizeof(double);
+    static constexpr int O_ST = O_HP + 4;                    // [NQ][STJ]
+    static constexpr int O_DV = O_ST + NQ * STJ;             // [NQ]
+    static constexpr int O_D = (O_DV + NQ + 1) / 2 * 2;      // [NQ][DQS]  (16-byte aligned)
+    static constexpr int O_PHI = O_D;                        // [NQ][M][NKS+1]     } overlay D
+    static constexpr int O_U = O_PHI + NQ * M * (NKS + 1);   // [NEN][M]            } (dead before
+    static constexpr int O_UD = O_U + NEN * M;               // [NEN][M]            }  phase 4)
+    static constexpr int O_R = O_UD + NEN * M;               // [NR][NQ]            }
+    static constexpr int O_ND = O_R + NR * NQ;               // long long [NEN]     }
+    static constexpr int OVL = O_ND + NEN - O_D;             // overlay extent
+    static constexpr int O_RS = O_D + (NQ * DQS > OVL ? NQ * DQS : OVL);   // long long [NEN*M] row starts
+#ifndef IGA_PBS
+#define IGA_PBS 0
+#endif
+    // trial values P_k(B, q) of every (function, point, trial kind) in shared memory (uniform
+    // tables only: identical for every element, built once per CTA) instead of per column
+    // (A/B: slower at 2 CTAs/SM, and it does not fit three)
+    static constexpr bool PBS = IGA_PBS && M == 4;
+    static constexpr int O_PB = O_RS + NEN * M;              // [NQ][NQK][NEN]
+    static constexpr size_t SMEM = (size_t)(O_PB + (PBS ? NQ * NQK * NEN : 0)) * sizeof(double);
+    // residual only: no coefficient blocks -- row starts (unused) right after the overlay
+    static constexpr int O_RS_RES = O_ND + NEN;
+    static constexpr size_t SMEM_RES = (size_t)(O_RS_RES + NEN * M) * sizeof(double);
     static_assert(NQ * M * (NKS + 1) <= NQ * DQS, "Phi must fit in the D region");
 };
 
@@ -80,7 +105,7 @@ struct F3 {
 template <class F, bool UNI, int P>
 __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double *__restrict__ Dsm, int ij,
                                               int b0, int b1, int b2, const double *__restrict__ tab,
-                                              const UniTab<P> &ut) {
+                                              const UniTab<P> &ut, const double *__restrict__ pbS) {
     using L = typename F::L;
     using KS = typename F::KS;
     constexpr int NP1 = F::NP1, NQ1 = F::NQ1, NEN = F::NEN, NTK = F::NTK, NQK = F::NQK, DB = F::DB;
@@ -121,7 +146,8 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
                 for (int y = 0; y < NP1; y++) Tt[o][x][y] = 0.0;
         // q1 loop rolled: unrolled, VMS spills at 255 registers and Neo-Hooke (168-register cap of
         // 3 CTAs/SM) misses in the instruction cache (A/B: 208 vs 216 ms, 10.1 vs 10.6 ms)
-#pragma unroll 1
+        constexpr int kQ1U = IGA_Q1U;
+#pragma unroll kQ1U
         for (int q1 = 0; q1 < NQ1; q1++) {
             double n1[3];
 #pragma unroll
@@ -143,9 +169,15 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
             for (int q2 = 0; q2 < NQ1; q2++) {
                 const int q = (q0 * NQ1 + q1) * NQ1 + q2;
                 double n2[3];
+                if constexpr (!(UNI && F::PBS)) {
 #pragma unroll
-                for (int k = 0; k < 3; k++) n2[k] = TS(2, q2, k, b2);
+                    for (int k = 0; k < 3; k++) n2[k] = TS(2, q2, k, b2);
+                }
                 double pb[NQK];
+                if constexpr (UNI && F::PBS) {
+#pragma unroll
+                    for (int kq = 0; kq < NQK; kq++) pb[kq] = pbS[(q * NQK + kq) * NEN + (b0 * NP1 + b1) * NP1 + b2];
+                } else {
                 static_for<NQK>([&](auto K) {
                     constexpr int kq = decltype(K)::value;
                     constexpr int c = L::qk(kq);
@@ -156,6 +188,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
                     });
                     pb[kq] = v;
                 });
+                }
                 // H[t] = sum_k D[k][t] pb[k]: block rows (trial kind k) streamed 16 bytes at a time
                 const double2 *Dq2 = reinterpret_cast<const double2 *>(Dsm + q * F::DQS + ij * DB);
                 double H[NTK];
@@ -224,12 +257,12 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     extern __shared__ __align__(16) double sm[];
     double *sU = sm + F::O_U, *sUd = sm + F::O_UD, *sTab = sm + F::O_TAB, *sQW = sm + F::O_QW, *sQX = sm + F::O_QX;
     double *sHP = sm + F::O_HP, *sPhi = sm + F::O_PHI, *sDV = sm + F::O_DV, *sR = sm + F::O_R, *sD = sm + F::O_D;
-    State *sSt = reinterpret_cast<State *>(sm + F::O_ST);
+    double *sStd = sm + F::O_ST;                             // [NQ][STJ] leading state doubles
     // [NEN*M] CSR row (A, i): offset of its first value from `val`, in doubles.  Halo rows live in
     // the halo buffer; their offsets are taken in the flat 64-bit address space (both arrays are
     // 8-byte aligned) so the scatter below addresses everything from the uniform `val` register.
     long long *sRS = reinterpret_cast<long long *>(sm + (JAC ? F::O_RS : F::O_RS_RES));
-    long long *sNode = reinterpret_cast<long long *>(sm + (JAC ? F::O_ND : F::O_ND_RES)); // [NEN] touched-box node
+    long long *sNode = reinterpret_cast<long long *>(sm + F::O_ND); // [NEN] touched-box node (overlays D)
     __shared__ int sG[3 * NP1], sW[3 * NP1], sPosE[3 * NP1 * NP1], sSeg[3 * NP1];
     __shared__ long long sS[3 * NP1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -241,6 +274,30 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     };
 
     const bool uni_knots = s.ax[0].uniform && s.ax[1].uniform && s.ax[2].uniform;
+    if constexpr (JAC && UNI && F::PBS) {
+        // P_k(B, q) = sum over the separable terms of kind k of T0 T1 T2 (the element-independent
+        // uniform tables), once per CTA; read per column in the contraction
+        double *pbS = sm + F::O_PB;
+        for (int i = tid; i < NQ * NQK * NEN; i += F::NT) {
+            const int B = i % NEN, kq = (i / NEN) % NQK, q = i / (NEN * NQK);
+            const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
+            const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
+            double v = 0.0;
+            static_for<NQK>([&](auto K) {
+                constexpr int kk = decltype(K)::value;
+                constexpr int c = L::qk(kk);
+                if (kk == kq) {
+                    static_for<KS::nterms(c)>([&](auto TT) {
+                        constexpr int t = decltype(TT)::value;
+                        v += ut.t[0][q0][KS::ord(c, t, 0)][b0] * ut.t[1][q1][KS::ord(c, t, 1)][b1] *
+                             ut.t[2][q2][KS::ord(c, t, 2)][b2];
+                    });
+                }
+            });
+            pbS[i] = v;
+        }
+        __syncthreads();
+    }
     for (long long el = blockIdx.x; el < nelem; el += gridDim.x) {
         // L2-blocked element order: pencils along axis 2, swept over axis 0 inside blocks of `bw`
         // pencils along axis 1, so the CSR rows an element layer leaves half-accumulated are
@@ -446,7 +503,11 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             const double dV = sQW[q0] * sQW[NQ1 + q1] * sQW[2 * NQ1 + q2];
             State st;
             PH::template prepare<3>(prm.p, Fq, st);
-            sSt[q] = st;
+            {
+                const double *src = reinterpret_cast<const double *>(&st);
+#pragma unroll
+                for (int k = 0; k < F::STJ; k++) sStd[q * F::STJ + k] = src[k];
+            }
             sDV[q] = dV;
             if (Fout) {
                 double r[NKS * M];
@@ -464,12 +525,65 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         }
         __syncthreads();
 
+        // ---- 3b. residual F_e[A, i] (formed before phase 4: R and the node numbers overlay D):
+        //         warp = component i (warp-uniform), lane = A; sum factorised per test kind:
+        //         sum_q0 T0 (sum_q1 T1 (sum_q2 T2 r(q))) ----
+        if (Fout && warp < M && lane < NEN && !(dbg & 32)) {
+            const int A = lane;
+            const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
+            double t0[NQ1][3], t1[NQ1][3], t2[NQ1][3];
+#pragma unroll
+            for (int q = 0; q < NQ1; q++)
+#pragma unroll
+                for (int k = 0; k < 3; k++) {
+                    t0[q][k] = sTab[((0 * NQ1 + q) * 3 + k) * NP1 + a0];
+                    t1[q][k] = sTab[((1 * NQ1 + q) * 3 + k) * NP1 + a1];
+                    t2[q][k] = sTab[((2 * NQ1 + q) * 3 + k) * NP1 + a2];
+                }
+            static_for<M>([&](auto II) {
+                constexpr int I = decltype(II)::value;
+                if (warp == I) {
+                    double acc = 0.0;
+                    static_for<NR>([&](auto RR) {
+                        constexpr int rr = decltype(RR)::value;
+                        constexpr int c = L::R.c[rr];
+                        if constexpr (L::R.i[rr] == I) {
+                            static_for<KS::nterms(c)>([&](auto TT) {
+                                constexpr int t = decltype(TT)::value;
+                                constexpr int o0 = KS::ord(c, t, 0), o1 = KS::ord(c, t, 1), o2 = KS::ord(c, t, 2);
+#pragma unroll
+                                for (int q0 = 0; q0 < NQ1; q0++) {
+                                    double s1 = 0.0;
+#pragma unroll
+                                    for (int q1 = 0; q1 < NQ1; q1++) {
+                                        double s2 = 0.0;
+#pragma unroll
+                                        for (int q2 = 0; q2 < NQ1; q2++)
+                                            s2 += t2[q2][o2] * sR[rr * NQ + (q0 * NQ1 + q1) * NQ1 + q2];
+                                        s1 += t1[q1][o1] * s2;
+                                    }
+                                    acc += t0[q0][o0] * s1;
+                                }
+                            });
+                        }
+                    });
+                    atomicAdd(Fout + sNode[A] * M + I, acc);
+                }
+            });
+        }
+        if constexpr (JAC) __syncthreads();          // F_e read R / sNode: both overlay D
+
         // ---- 4. Jacobian coefficients: warp-uniform trial column (k2 = qk(kq), j), lane = q ----
         if constexpr (JAC) {
             // warp w owns the columns kj = w, w + NWARP, ...: the state stays in registers
             if (lane < NQ && !(dbg & 16)) {
                 const int q = lane;
-                const State st = sSt[q];
+                State st;
+                {
+                    double *dst = reinterpret_cast<double *>(&st);
+#pragma unroll
+                    for (int k = 0; k < F::STJ; k++) dst[k] = sStd[q * F::STJ + k];
+                }
                 const double dV = sDV[q];
                 double chk = 0.0;
                 {
@@ -530,7 +644,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         J = T;
                     }
                     double Kc[NEN];
-                    if (!(dbg & 1)) tsf_column_3d<F, UNI, P>(Kc, sD, I * M + J, b0, b1, b2, sTab, ut);
+                    if (!(dbg & 1)) tsf_column_3d<F, UNI, P>(Kc, sD, I * M + J, b0, b1, b2, sTab, ut, sm + F::O_PB);
                     else {
 #pragma unroll
                         for (int A = 0; A < NEN; A++) Kc[A] = sD[A * 7 + J];
@@ -578,51 +692,6 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     }
                 }
             }
-        }
-        // ---- 6. residual F_e[A, i]: warp = component i (warp-uniform), lane = A; sum
-        //         factorised per test kind: sum_q0 T0 (sum_q1 T1 (sum_q2 T2 r(q))) ----
-        if (Fout && warp < M && lane < NEN && !(dbg & 32)) {
-            const int A = lane;
-            const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
-            double t0[NQ1][3], t1[NQ1][3], t2[NQ1][3];
-#pragma unroll
-            for (int q = 0; q < NQ1; q++)
-#pragma unroll
-                for (int k = 0; k < 3; k++) {
-                    t0[q][k] = sTab[((0 * NQ1 + q) * 3 + k) * NP1 + a0];
-                    t1[q][k] = sTab[((1 * NQ1 + q) * 3 + k) * NP1 + a1];
-                    t2[q][k] = sTab[((2 * NQ1 + q) * 3 + k) * NP1 + a2];
-                }
-            static_for<M>([&](auto II) {
-                constexpr int I = decltype(II)::value;
-                if (warp == I) {
-                    double acc = 0.0;
-                    static_for<NR>([&](auto RR) {
-                        constexpr int rr = decltype(RR)::value;
-                        constexpr int c = L::R.c[rr];
-                        if constexpr (L::R.i[rr] == I) {
-                            static_for<KS::nterms(c)>([&](auto TT) {
-                                constexpr int t = decltype(TT)::value;
-                                constexpr int o0 = KS::ord(c, t, 0), o1 = KS::ord(c, t, 1), o2 = KS::ord(c, t, 2);
-#pragma unroll
-                                for (int q0 = 0; q0 < NQ1; q0++) {
-                                    double s1 = 0.0;
-#pragma unroll
-                                    for (int q1 = 0; q1 < NQ1; q1++) {
-                                        double s2 = 0.0;
-#pragma unroll
-                                        for (int q2 = 0; q2 < NQ1; q2++)
-                                            s2 += t2[q2][o2] * sR[rr * NQ + (q0 * NQ1 + q1) * NQ1 + q2];
-                                        s1 += t1[q1][o1] * s2;
-                                    }
-                                    acc += t0[q0][o0] * s1;
-                                }
-                            });
-                        }
-                    });
-                    atomicAdd(Fout + sNode[A] * M + I, acc);
-                }
-            });
         }
         __syncthreads();
     }

@@ -263,9 +263,10 @@ struct PhysNSVMS {
     static constexpr bool rmask(int k, int i) { return k < 4; }
     template <int DIM>
     struct State {
-        double u[3], gu[3][3], up[3], tauM, tauC, nu;
-        double rN[4], rG[3][4];
+        double u[3], gu[3][3], up[3], tauM, tauC, nu;   // read by dcol (the first JSTATE doubles)
+        double rN[4], rG[3][4];                          // residual coefficients only
     };
+    static constexpr int JSTATE = 18;
     template <int DIM>
     __device__ static inline void prepare(const double *p, const Fields<DIM, 4> &F, State<DIM> &s) {
         static_assert(DIM == 3, "NS_VMS is 3D");
