@@ -21,7 +21,8 @@
  *  - CSR: row_ptr int64 [nrows+1] (config 5 has 4.19e9 nonzeros > 2^31), col_idx int32 [nnz]
  *    global dof indices, ascending within each row; csr_val fp64 [nnz].
  *  - Every call that takes a cudaStream_t (passed as void*) is asynchronous on that stream
- *    and allocates no device memory (iga_gmres excepted, see there).  Buffers must stay alive
+ *    and allocates no device memory (iga_gmres and iga_form_jacobian_host excepted, see
+ *    there).  Buffers must stay alive
  *    until the stream reaches them.
  *  - Errors: every call returns an iga_status; iga_last_error() gives a thread-local message.
  *    Argument / knot / continuity validation is synchronous.  Device-side conditions
@@ -173,7 +174,10 @@ iga_status iga_form_jacobian(iga_space s, const iga_phys *phys, double a, double
 
 /* Host-buffer variant (end-to-end path): copies U/Udot host->device, forms J (and F if
  * F_host != NULL) and copies csr_val / F back, all on `stream`; returns after the stream
- * synchronises.  Host buffers should be pinned for full PCIe bandwidth. */
+ * synchronises.  Host buffers should be pinned for full PCIe bandwidth.
+ * Device memory: the first call allocates the device staging buffers (2 ndof + nnz + nrows
+ * doubles: 34 GB for config 5) and keeps them with the space (freed by iga_space_destroy);
+ * IGA_ERR_NOMEM if that allocation fails.  Single-rank spaces only (IGA_ERR_STATE otherwise). */
 iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, double b,
                                   const double *U_host, const double *Udot_host,
                                   double *csr_val_host, double *F_host, void *stream);

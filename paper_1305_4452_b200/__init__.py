@@ -341,29 +341,7 @@ class Space:
     def __init__(self, dim, degree, knots, periodic, continuity, dof, quad, geometry, ctrl=None, weights=None,
                  device: int = 0, dist=None):
         L = lib()
-        d = _Desc()
-        d.dim = dim
-        self._keep = []
-        for a in range(3):
-            if a < dim:
-                k = np.ascontiguousarray(knots[a], dtype=np.float64)
-                self._keep.append(k)
-                d.degree[a] = int(degree[a])
-                d.n_knots[a] = len(k)
-                d.knots[a] = k.ctypes.data_as(C.POINTER(C.c_double))
-                d.periodic[a] = int(periodic[a])
-                d.periodic_continuity[a] = int(continuity[a])
-                d.quad[a] = int(quad[a]) if quad is not None else 0
-        d.dof = dof
-        d.geometry = geometry
-        if ctrl is not None:
-            c = np.ascontiguousarray(ctrl, dtype=np.float64).reshape(-1)
-            self._keep.append(c)
-            d.ctrl = c.ctypes.data_as(C.POINTER(C.c_double))
-        if weights is not None:
-            w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
-            self._keep.append(w)
-            d.weights = w.ctypes.data_as(C.POINTER(C.c_double))
+        d, self._keep = _make_desc(dim, degree, knots, periodic, continuity, dof, quad, geometry, ctrl, weights)
         dd = _make_dist(dist) if dist is not None else None
         h = C.c_void_p()
         _check(L.iga_space_create(C.byref(d), C.byref(dd) if dd is not None else None, device, C.byref(h)))

@@ -8,11 +8,11 @@
 //              K_e[A,B] = w_A w_B sum_q P(A,q)^T D~(q) P(B,q): H(q) = D~(q) P(B,q), then the
 //              contraction over q1 (per q0) and over q0, using the 1D tables only;
 //   lane A  -> F_e[A].
-// Element blocks are added into a shared-memory copy of the tile's CSR rows (one slot per
-// stencil offset delta in [-p,p]^2) with shared-memory atomics.  At the end of the tile, rows
-// whose whole support lies in the tile are written once with plain coalesced stores; the
-// others (tile boundary) are added with red.global.add.f64 into rows pre-zeroed by
-// k_zero_rows2d.  The CSR position of (row g, delta) comes from the per-axis Alg. 3 tables.
+// Column B of the element block is added straight into the caller's CSR rows with
+// red.global.add.f64 (rows pre-zeroed by k_zero; a shared-memory row image was measured slower:
+// an fp64 shared atomicAdd is a CAS loop on sm_100a).  The CSR position of
+// (row A, column B) is a closed form of the per-node row starts and the per-axis Alg. 3 stencil
+// positions staged once per tile, so no kernel searches col_idx.
 #include <cstdio>
 
 #include "iga_host.h"
