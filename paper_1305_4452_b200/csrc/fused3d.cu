@@ -36,6 +36,12 @@
 #ifndef IGA_HOIST
 #define IGA_HOIST 1  // trial 1D values hoisted out of the contraction loops (see tsf_column_3d)
 #endif
+#ifndef IGA_WS
+#define IGA_WS 1    // VMS: warp-specialised producer/consumer phase 5 (needs IGA_PC)
+#endif
+#ifndef IGA_SMR
+#define IGA_SMR 1   // setmaxnreg rebalancing between producer and consumer warps
+#endif
 #ifndef IGA_BAL
 #define IGA_BAL 1   // column tasks dealt round-robin over all threads (phase 5, non-symmetric forms)
 #endif
@@ -82,12 +88,29 @@ struct F3 {
     // built (field kinds Phi, U_e, Udot_e, residual coefficients, node numbers) overlays the D
     // region: the element's residual F_e is formed before phase 4 for that reason.  VMS fits three
     // CTAs per SM this way (<= 75 KB each).
+    // Producer/consumer contraction (VMS, see pc_produce / pc_consume): the coefficients are
+    // stored compactly -- only the structural nonzeros, [entry (EIJ order)][q] -- and two H buffers
+    // hold H_t(B, q) = sum_k D_tk(q) P_k(B, q) of one (test component I, q0 slab) round for the
+    // four trial components (round r+1 is produced while round r is consumed).  Strides chosen so
+    // that the producer's stores (lane = (b0, q1, q2)) and the consumer's loads (tid = 4 B + J)
+    // are free of bank conflicts.  The point states (phases 3-4) overlay the H buffers.
+    static constexpr bool PC = IGA_PC && M == 4 && !SYMJ;
+    static constexpr int NEC = L::EIJ.n;
+    static constexpr int HS_T = 28, HS_Q2 = 4 * HS_T + 1, HS_Q1 = 3 * HS_Q2, HS_J = 3 * HS_Q1 + 3;
+    static constexpr int HBUF = M * HS_J;                    // one H buffer
+    // warp-specialised Jacobian launch (VMS): 8 warps, two CTAs per SM (16 warps/SM at a 128-register
+    // base); in phase 5 warps 0..3 produce H (setmaxnreg down to PREG), warps 4..7 consume it (up to
+    // CREG): 4 (PREG + CREG) = 8 x 128
+    static constexpr bool WS = IGA_WS && PC;
+    static constexpr int NTJ = WS ? 256 : NT;
+    static constexpr int MINBJ = WS ? 2 : MINB;
+    static constexpr int PREG = 104, CREG = 152;
     static constexpr int O_TAB = 0;                          // [3][NQ1][3][NP1]
     static constexpr int O_QW = O_TAB + 3 * NQ1 * 3 * NP1;   // [3][NQ1]
     static constexpr int O_QX = O_QW + 3 * NQ1;              // [3][NQ1]
     static constexpr int O_HP = O_QX + 3 * NQ1;              // [4]
-    static constexpr int O_ST = O_HP + 4;                    // [NQ][STJ]
-    static constexpr int O_DV = O_ST + NQ * STJ;             // [NQ]
+    static constexpr int O_ST0 = O_HP + 4;                   // [NQ][STJ] (not PC)
+    static constexpr int O_DV = PC ? O_ST0 : O_ST0 + NQ * STJ;   // [NQ]
     static constexpr int O_D = (O_DV + NQ + 1) / 2 * 2;      // [NQ][DQS]  (16-byte aligned)
     static constexpr int O_PHI = O_D;                        // [NQ][M][NKS+1]     } overlay D
     static constexpr int O_U = O_PHI + NQ * M * (NKS + 1);   // [NEN][M]            } (dead before
@@ -95,18 +118,11 @@ struct F3 {
     static constexpr int O_R = O_UD + NEN * M;               // [NR][NQ]            }
     static constexpr int O_ND = O_R + NR * NQ;               // long long [NEN]     }
     static constexpr int OVL = O_ND + NEN - O_D;             // overlay extent
-    // Producer/consumer contraction (VMS, see pc_produce / pc_consume): the coefficients are
-    // stored compactly -- only the structural nonzeros, [entry (EIJ order)][q] -- and an H buffer
-    // holds H_t(B, q) = sum_k D_tk(q) P_k(B, q) of one (test component I, q0 slab) round for the
-    // four trial components.  Strides chosen so that the producer's stores (lane = (b0, q1, q2))
-    // and the consumer's loads (tid = 4 B + J) are free of bank conflicts.
-    static constexpr bool PC = IGA_PC && M == 4 && !SYMJ;
-    static constexpr int NEC = L::EIJ.n;
-    static constexpr int HS_T = 28, HS_Q2 = 4 * HS_T + 1, HS_Q1 = 3 * HS_Q2, HS_J = 3 * HS_Q1 + 3;
-    static constexpr int HSZ = PC ? M * HS_J : 0;
     static constexpr int DREG = PC ? NEC * NQ : NQ * DQS;    // coefficient region
     static constexpr int O_H = O_D + (DREG > OVL ? DREG : OVL);
-    static constexpr int O_RS = O_H + HSZ;                   // long long [NEN*M] row starts
+    static constexpr int HREG = PC ? (2 * HBUF > NQ * STJ ? 2 * HBUF : NQ * STJ) : 0;
+    static constexpr int O_ST = PC ? O_H : O_ST0;
+    static constexpr int O_RS = O_H + HREG;                  // long long [NEN*M] row starts
 #ifndef IGA_PBS
 #define IGA_PBS 0
 #endif
@@ -118,7 +134,8 @@ struct F3 {
     static constexpr size_t SMEM = (size_t)(O_PB + (PBS ? NQ * NQK * NEN : 0)) * sizeof(double);
     // residual only: no coefficient blocks -- row starts (unused) right after the overlay
     static constexpr int O_RS_RES = O_ND + NEN;
-    static constexpr size_t SMEM_RES = (size_t)(O_RS_RES + NEN * M) * sizeof(double);
+    static constexpr int END_RES = O_RS_RES + NEN * M > O_ST + NQ * STJ ? O_RS_RES + NEN * M : O_ST + NQ * STJ;
+    static constexpr size_t SMEM_RES = (size_t)END_RES * sizeof(double);
     static_assert(NQ * M * (NKS + 1) <= NQ * DQS, "Phi must fit in the D region");
     static_assert(!PC || (P == 2 && NTK == 4 && NT == 32 * M), "producer/consumer layout is for p = 2, m = 4");
 };
@@ -467,11 +484,12 @@ __device__ __forceinline__ void pc_consume(double (&Kc)[F::NEN], const double *_
 }
 
 template <int P, class PH, bool JAC, bool UNI>
-__global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3<P, PH>::MINB : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
+__global__ void __launch_bounds__(JAC ? F3<P, PH>::NTJ : F3<P, PH>::NT, JAC ? F3<P, PH>::MINBJ : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
           int dbg, int bw) {
     using F = F3<P, PH>;
+    constexpr int NTH = JAC ? F::NTJ : F::NT, NWP = NTH / 32;   // threads / warps of this launch
     using L = typename F::L;
     using KS = typename F::KS;
     using State = typename F::State;
@@ -501,7 +519,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         // P_k(B, q) = sum over the separable terms of kind k of T0 T1 T2 (the element-independent
         // uniform tables), once per CTA; read per column in the contraction
         double *pbS = sm + F::O_PB;
-        for (int i = tid; i < NQ * NQK * NEN; i += F::NT) {
+        for (int i = tid; i < NQ * NQK * NEN; i += NTH) {
             const int B = i % NEN, kq = (i / NEN) % NQK, q = i / (NEN * NQK);
             const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
             const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
@@ -541,7 +559,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         // ---- 1. stage: tables, per-axis function data, position tables, and (uniform knots:
         //         first[e] = first0 + e, no dependent load) U_e -- one global round trip ----
         const int nU1 = uni_knots ? NEN * M : 0;
-        for (int i = tid; i < 3 * NQ1 * 3 * NP1 + 6 * NQ1 + 3 + 3 * NP1 + 3 * NP1 * NP1 + nU1; i += F::NT) {
+        for (int i = tid; i < 3 * NQ1 * 3 * NP1 + 6 * NQ1 + 3 + 3 * NP1 + 3 * NP1 * NP1 + nU1; i += NTH) {
             int k = i;
             if (k < 3 * NQ1 * 3 * NP1) {
                 const int d = k / (NQ1 * 3 * NP1), r = k % (NQ1 * 3 * NP1);
@@ -599,7 +617,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         }
         __syncthreads();
         {
-            for (int i = tid; i < NEN * M; i += F::NT) {
+            for (int i = tid; i < NEN * M; i += NTH) {
                 {
                     const int k = i, A = k / M, m = k - A * M;
                     const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
@@ -629,7 +647,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
         // ---- 2. field kinds per (q, m), sum factorised over the element's functions:
         //         Phi_k(q) = sum_a0 T0 (sum_a1 T1 (sum_a2 T2 U)) per separable term of kind k ----
-        for (int task = (dbg & 4) ? NQ * M : tid; task < NQ * M; task += F::NT) {
+        for (int task = (dbg & 4) ? NQ * M : tid; task < NQ * M; task += NTH) {
             const int q = task / M, m = task % M;
             const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
             double v0[3][NP1], v1[3][NP1], v2[3][NP1];
@@ -813,7 +831,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     static_for<NQK * M>([&](auto KJ) {
                         constexpr int kq = decltype(KJ)::value / M, j = decltype(KJ)::value % M;
                         constexpr int k2 = L::qk(kq);
-                        if (warp == decltype(KJ)::value % F::NWARP) {
+                        if (warp == decltype(KJ)::value % NWP) {
                             double col[NKS * M];
                             PH::template dcol<3>(st, k2, j, a, b, col);
                             if constexpr (F::PC) {
@@ -864,41 +882,99 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             // lanes write one 32-byte sector of a CSR row) are dealt round-robin over all NT
             // threads -- 432 tasks on 128 threads = 14 warp-passes instead of 4 passes of the
             // 108 (B, J) threads on 4 warps (16 warp-passes, the last warp 12/32 lanes busy).
-            if constexpr (F::PC) {
-                // warp J = trial component: producer and consumer of its own H slice (warp-local,
-                // __syncwarp only); per test component I one transposition through shared memory
-                // so that the scatter keeps 4 consecutive lanes on one 32-byte sector (J fastest)
-                static_assert(F::NWARP == M, "one warp per trial component");
+            if constexpr (F::WS) {
+                // warp specialisation: producers (warp J < M, lane = (b0, q1, q2)) fill H round
+                // r = (I, q0) into buffer r & 1 while consumers (warps M..2M-1, thread (B, J))
+                // contract round r - 1; named barriers 1 + b (full) and 3 + b (empty)
                 double *sH = sm + F::O_H;
-                const int J = warp;
+                constexpr int NRND = M * NQ1;
+                if (warp < M) {
+                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(F::PREG));
 #pragma unroll 1
-                for (int I = 0; I < M; I++) {
-                    double Kc[NEN];
-#pragma unroll
-                    for (int A = 0; A < NEN; A++) Kc[A] = 0.0;
-#pragma unroll 1
-                    for (int q0 = 0; q0 < NQ1; q0++) {
+                    for (int r = 0; r < NRND; r++) {
+                        const int bsel = r & 1;
+                        if (r >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + bsel), "n"(NTH) : "memory");
                         if (lane < NEN) {
+                            const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
+                            double *hb = sH + bsel * F::HBUF;
                             static_for<M * M>([&](auto IJ) {
                                 constexpr int Ic = decltype(IJ)::value / M, Jc = decltype(IJ)::value % M;
-                                if (I == Ic && J == Jc) pc_produce<F, UNI, P, Ic, Jc>(sD, sH, q0, lane, sTab, ut);
+                                if (I == Ic && warp == Jc) pc_produce<F, UNI, P, Ic, Jc>(sD, hb, q0, lane, sTab, ut);
                             });
                         }
-                        __syncwarp();
-                        if (lane < NEN) pc_consume<F, UNI, P>(Kc, sH, q0, lane, J, sTab, ut);
-                        __syncwarp();
+                        asm volatile("bar.arrive %0, %1;" ::"r"(1 + bsel), "n"(NTH) : "memory");
                     }
-                    // Kc of column (B = lane, J) -> T[J][A][B] (inside this warp's own H slice)
-                    if (lane < NEN) {
-                        double *tj = sH + J * F::HS_J + lane;
+                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
+                } else {
+                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(F::CREG));
+                    const int ct = tid - M * 32;
+                    const bool cons = ct < NEN * M;
+                    const int B = ct / M, J = ct - (ct / M) * M;
+                    double Kc[NEN];
+#pragma unroll 1
+                    for (int r = 0; r < NRND; r++) {
+                        const int bsel = r & 1;
+                        const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
+                        asm volatile("bar.sync %0, %1;" ::"r"(1 + bsel), "n"(NTH) : "memory");
+                        if (q0 == 0) {
 #pragma unroll
-                        for (int A = 0; A < NEN; A++) tj[A * NEN] = Kc[A];
+                            for (int A = 0; A < NEN; A++) Kc[A] = 0.0;
+                        }
+                        if (cons) pc_consume<F, UNI, P>(Kc, sH + bsel * F::HBUF, q0, B, J, sTab, ut);
+                        if (r + 2 < NRND) asm volatile("bar.arrive %0, %1;" ::"r"(3 + bsel), "n"(NTH) : "memory");
+                        if (q0 == NQ1 - 1 && cons && !(dbg & 2)) {
+                            const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
+                            int P0[NP1], P1[NP1], P2[NP1], W1[NP1], W2[NP1];
+#pragma unroll
+                            for (int x = 0; x < NP1; x++) {
+                                P0[x] = sPosE[x * NP1 + b0];
+                                P1[x] = sPosE[NP1 * NP1 + x * NP1 + b1];
+                                P2[x] = sPosE[2 * NP1 * NP1 + x * NP1 + b2];
+                                W1[x] = sW[NP1 + x];
+                                W2[x] = sW[2 * NP1 + x];
+                            }
+#pragma unroll
+                            for (int A = 0; A < NEN; A++) {
+                                const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
+                                const int co = (P0[a0] * W1[a1] + P1[a1]) * W2[a2] + P2[a2];
+                                atomicAdd(val + sRS[A * M + I] + (long long)co * M + J, Kc[A]);
+                            }
+                        }
                     }
-                    __syncthreads();
-                    if (tid < NEN * M && !(dbg & 2)) {
-                        const int Bs = tid / M, Js = tid - Bs * M;
-                        const int b0 = Bs / (NP1 * NP1), b1 = (Bs / NP1) % NP1, b2 = Bs % NP1;
-                        const double *tj = sH + Js * F::HS_J + Bs;
+                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 128;");
+                }
+            } else if constexpr (F::PC) {
+                // rounds r = (I, q0): warps produce H of round r+1 into one buffer while the
+                // (B, J) threads consume round r from the other -- one barrier per round
+                static_assert(F::NWARP == M, "one producer warp per trial component");
+                double *sH = sm + F::O_H;
+                const bool cons = tid < NEN * M;
+                const int B = tid / M, J = tid - (tid / M) * M;
+                constexpr int NRND = M * NQ1;
+                auto produce = [&](int r) {
+                    if (lane < NEN) {
+                        const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
+                        double *hb = sH + (r & 1) * F::HBUF;
+                        static_for<M * M>([&](auto IJ) {
+                            constexpr int Ic = decltype(IJ)::value / M, Jc = decltype(IJ)::value % M;
+                            if (I == Ic && warp == Jc) pc_produce<F, UNI, P, Ic, Jc>(sD, hb, q0, lane, sTab, ut);
+                        });
+                    }
+                };
+                double Kc[NEN];
+                produce(0);
+                __syncthreads();
+#pragma unroll 1
+                for (int r = 0; r < NRND; r++) {
+                    const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
+                    if (q0 == 0) {
+#pragma unroll
+                        for (int A = 0; A < NEN; A++) Kc[A] = 0.0;
+                    }
+                    if (cons) pc_consume<F, UNI, P>(Kc, sH + (r & 1) * F::HBUF, q0, B, J, sTab, ut);
+                    if (r + 1 < NRND) produce(r + 1);
+                    if (q0 == NQ1 - 1 && cons && !(dbg & 2)) {
+                        const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
                         int P0[NP1], P1[NP1], P2[NP1], W1[NP1], W2[NP1];
 #pragma unroll
                         for (int x = 0; x < NP1; x++) {
@@ -912,14 +988,14 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         for (int A = 0; A < NEN; A++) {
                             const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
                             const int co = (P0[a0] * W1[a1] + P1[a1]) * W2[a2] + P2[a2];
-                            atomicAdd(val + sRS[A * M + I] + (long long)co * M + Js, tj[A * NEN]);
+                            atomicAdd(val + sRS[A * M + I] + (long long)co * M + J, Kc[A]);
                         }
                     }
                     __syncthreads();
                 }
             } else if constexpr (!F::SYMJ && IGA_BAL) {
 #pragma unroll 1
-                for (int c = tid; c < NEN * M * M; c += F::NT) {
+                for (int c = tid; c < NEN * M * M; c += NTH) {
                     const int I = c / (NEN * M), r = c - I * (NEN * M), B = r / M, J = r - B * M;
                     const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
                     double Kc[NEN];
@@ -1050,7 +1126,7 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
         if (ce != cudaSuccess) { set_error(std::string("fused3d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
     }
     int occ = 1;
-    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, true, UNI>, FF::NT, smem);
+    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, true, UNI>, FF::NTJ, smem);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, false, UNI>, FF::NT, smem);
     occ = std::max(occ, 1);
     const long long nel = s->nel_local;
@@ -1069,7 +1145,7 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
         int bw = (int)(60e6 / (3.0 * (ne2 + P) * row_bytes)) - P;
         if (s->bw_opt > 0) bw = s->bw_opt;
         bw = std::max(1, std::min(bw, ne1));
-        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
+        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NTJ, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
         else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
         launches++;
     }
