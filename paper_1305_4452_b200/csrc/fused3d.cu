@@ -27,20 +27,8 @@
 #ifndef IGA_Q1U
 #define IGA_Q1U 1   // experiments: unroll factor of the contraction's q1 loop
 #endif
-#ifndef IGA_NZ
-#define IGA_NZ 0    // accumulators initialised to -0.0 (see tsf_column_3d)
-#endif
-#ifndef IGA_PC
-#define IGA_PC 0    // VMS: producer/consumer contraction through a shared H buffer (phase 5)
-#endif
 #ifndef IGA_HOIST
 #define IGA_HOIST 1  // trial 1D values hoisted out of the contraction loops (see tsf_column_3d)
-#endif
-#ifndef IGA_WS
-#define IGA_WS 1    // VMS: warp-specialised producer/consumer phase 5 (needs IGA_PC)
-#endif
-#ifndef IGA_SMR
-#define IGA_SMR 1   // setmaxnreg rebalancing between producer and consumer warps
 #endif
 #ifndef IGA_BAL
 #define IGA_BAL 1   // column tasks dealt round-robin over all threads (phase 5, non-symmetric forms)
@@ -88,29 +76,12 @@ struct F3 {
     // built (field kinds Phi, U_e, Udot_e, residual coefficients, node numbers) overlays the D
     // region: the element's residual F_e is formed before phase 4 for that reason.  VMS fits three
     // CTAs per SM this way (<= 75 KB each).
-    // Producer/consumer contraction (VMS, see pc_produce / pc_consume): the coefficients are
-    // stored compactly -- only the structural nonzeros, [entry (EIJ order)][q] -- and two H buffers
-    // hold H_t(B, q) = sum_k D_tk(q) P_k(B, q) of one (test component I, q0 slab) round for the
-    // four trial components (round r+1 is produced while round r is consumed).  Strides chosen so
-    // that the producer's stores (lane = (b0, q1, q2)) and the consumer's loads (tid = 4 B + J)
-    // are free of bank conflicts.  The point states (phases 3-4) overlay the H buffers.
-    static constexpr bool PC = IGA_PC && M == 4 && !SYMJ;
-    static constexpr int NEC = L::EIJ.n;
-    static constexpr int HS_T = 28, HS_Q2 = 4 * HS_T + 1, HS_Q1 = 3 * HS_Q2, HS_J = 3 * HS_Q1 + 3;
-    static constexpr int HBUF = M * HS_J;                    // one H buffer
-    // warp-specialised Jacobian launch (VMS): 8 warps, two CTAs per SM (16 warps/SM at a 128-register
-    // base); in phase 5 warps 0..3 produce H (setmaxnreg down to PREG), warps 4..7 consume it (up to
-    // CREG): 4 (PREG + CREG) = 8 x 128
-    static constexpr bool WS = IGA_WS && PC;
-    static constexpr int NTJ = WS ? 256 : NT;
-    static constexpr int MINBJ = WS ? 2 : MINB;
-    static constexpr int PREG = 104, CREG = 152;
     static constexpr int O_TAB = 0;                          // [3][NQ1][3][NP1]
     static constexpr int O_QW = O_TAB + 3 * NQ1 * 3 * NP1;   // [3][NQ1]
     static constexpr int O_QX = O_QW + 3 * NQ1;              // [3][NQ1]
     static constexpr int O_HP = O_QX + 3 * NQ1;              // [4]
-    static constexpr int O_ST0 = O_HP + 4;                   // [NQ][STJ] (not PC)
-    static constexpr int O_DV = PC ? O_ST0 : O_ST0 + NQ * STJ;   // [NQ]
+    static constexpr int O_ST = O_HP + 4;                    // [NQ][STJ]
+    static constexpr int O_DV = O_ST + NQ * STJ;             // [NQ]
     static constexpr int O_D = (O_DV + NQ + 1) / 2 * 2;      // [NQ][DQS]  (16-byte aligned)
     static constexpr int O_PHI = O_D;                        // [NQ][M][NKS+1]     } overlay D
     static constexpr int O_U = O_PHI + NQ * M * (NKS + 1);   // [NEN][M]            } (dead before
@@ -118,11 +89,7 @@ struct F3 {
     static constexpr int O_R = O_UD + NEN * M;               // [NR][NQ]            }
     static constexpr int O_ND = O_R + NR * NQ;               // long long [NEN]     }
     static constexpr int OVL = O_ND + NEN - O_D;             // overlay extent
-    static constexpr int DREG = PC ? NEC * NQ : NQ * DQS;    // coefficient region
-    static constexpr int O_H = O_D + (DREG > OVL ? DREG : OVL);
-    static constexpr int HREG = PC ? (2 * HBUF > NQ * STJ ? 2 * HBUF : NQ * STJ) : 0;
-    static constexpr int O_ST = PC ? O_H : O_ST0;
-    static constexpr int O_RS = O_H + HREG;                  // long long [NEN*M] row starts
+    static constexpr int O_RS = O_D + (NQ * DQS > OVL ? NQ * DQS : OVL);   // long long [NEN*M] row starts
 #ifndef IGA_PBS
 #define IGA_PBS 0
 #endif
@@ -134,10 +101,8 @@ struct F3 {
     static constexpr size_t SMEM = (size_t)(O_PB + (PBS ? NQ * NQK * NEN : 0)) * sizeof(double);
     // residual only: no coefficient blocks -- row starts (unused) right after the overlay
     static constexpr int O_RS_RES = O_ND + NEN;
-    static constexpr int END_RES = O_RS_RES + NEN * M > O_ST + NQ * STJ ? O_RS_RES + NEN * M : O_ST + NQ * STJ;
-    static constexpr size_t SMEM_RES = (size_t)END_RES * sizeof(double);
+    static constexpr size_t SMEM_RES = (size_t)(O_RS_RES + NEN * M) * sizeof(double);
     static_assert(NQ * M * (NKS + 1) <= NQ * DQS, "Phi must fit in the D region");
-    static_assert(!PC || (P == 2 && NTK == 4 && NT == 32 * M), "producer/consumer layout is for p = 2, m = 4");
 };
 
 // test-side sum factorisation in 3D of one column (trial function B = (b0,b1,b2), pair ij):
@@ -150,9 +115,6 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
     using L = typename F::L;
     using KS = typename F::KS;
     constexpr int NP1 = F::NP1, NQ1 = F::NQ1, NEN = F::NEN, NTK = F::NTK, NQK = F::NQK, DB = F::DB;
-    // accumulators start at -0.0, the identity of fma's addend: fma(x, y, -0) = x*y lets the
-    // compiler drop the zero-initialisation (0.0 is not an identity for x*y = -0)
-    constexpr double kZ = IGA_NZ ? -0.0 : 0.0;
     // Neo-Hooke runs 3 CTAs/SM at the 168-register cap: hoisting spills there (A/B +6 %)
     constexpr int HOIST = F::M == 3 ? 0 : IGA_HOIST;
     auto T = [&](int d, int q, int k, int a) -> double {
@@ -177,7 +139,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
         return false;
     };
 #pragma unroll
-    for (int A = 0; A < NEN; A++) Kc[A] = kZ;
+    for (int A = 0; A < NEN; A++) Kc[A] = 0.0;
     // trial 1D values of this column along axis 1 for every q1, loaded once (HOIST >= 1:
     // the per-iteration loads at the head of the rolled q1 loop were the kernel's largest
     // single stall, ncu r02a) and along axis 2 (HOIST >= 2)
@@ -205,7 +167,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
 #pragma unroll
             for (int x = 0; x < NP1; x++)
 #pragma unroll
-                for (int y = 0; y < NP1; y++) Tt[o][x][y] = kZ;
+                for (int y = 0; y < NP1; y++) Tt[o][x][y] = 0.0;
         // q1 loop rolled: unrolled, VMS spills at 255 registers and Neo-Hooke (168-register cap of
         // 3 CTAs/SM) misses in the instruction cache (A/B: 208 vs 216 ms, 10.1 vs 10.6 ms)
         constexpr int kQ1U = IGA_Q1U;
@@ -232,7 +194,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
 #pragma unroll
                 for (int o2 = 0; o2 < 3; o2++)
 #pragma unroll
-                    for (int x = 0; x < NP1; x++) S[o][o2][x] = kZ;
+                    for (int x = 0; x < NP1; x++) S[o][o2][x] = 0.0;
 #pragma unroll
             for (int q2 = 0; q2 < NQ1; q2++) {
                 const int q = (q0 * NQ1 + q1) * NQ1 + q2;
@@ -264,7 +226,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
                 const double2 *Dq2 = reinterpret_cast<const double2 *>(Dsm + q * F::DQS + ij * DB);
                 double H[NTK];
 #pragma unroll
-                for (int t = 0; t < NTK; t++) H[t] = kZ;
+                for (int t = 0; t < NTK; t++) H[t] = 0.0;
 #pragma unroll
                 for (int x = 0; x < DB / 2; x++) {
                     const double2 v2 = Dq2[x];
@@ -314,182 +276,13 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
     }
 }
 
-// ---- producer/consumer contraction (VMS): phase 5 in rounds (test component I, q0 slab) ----
-// Producer (warp J = trial component, lane = (b0, q1, q2), 27 lanes): for the block (I, J) --
-// compile-time, so only its structural nonzeros are multiplied -- the lane keeps the block's
-// coefficients at its point q = (q0, q1, q2) in registers and forms, for the 9 trial functions
-// B = (b0, b1, b2) of its b0 slab,
-//     H_t(B, q) = sum_k D_(I,J)[t][k](q) P_k(B, q),
-// P_k a product of the 1D tables (Cox-de Boor values, tensor product P:196-203).  H goes to the
-// shared buffer.  Compared with every (B, J) thread reading the dense D block at every point
-// (broadcast loads: 27 B x 20 doubles per point), the buffer carries 4 doubles per (B, q):
-// the shared-memory data pipe was the co-bottleneck of the column-per-thread design.
-template <class F, bool UNI, int P, int I, int J>
-__device__ __forceinline__ void pc_produce(const double *__restrict__ sDc, double *__restrict__ sH, int q0, int lane,
-                                           const double *__restrict__ tab, const UniTab<P> &ut) {
-    using L = typename F::L;
-    using KS = typename F::KS;
-    constexpr int NP1 = F::NP1, NQ1 = F::NQ1, NQ = F::NQ, NTK = F::NTK, NQK = F::NQK;
-    constexpr int e0 = L::eij_start(I, J), ne = L::eij_count(I, J);
-    auto T = [&](int d, int q, int k, int a) -> double {
-        if constexpr (UNI) return ut.t[d][q][k][a];
-        else return tab[((d * NQ1 + q) * 3 + k) * NP1 + a];
-    };
-    const int b0 = lane / (NQ1 * NQ1), q1 = (lane / NQ1) % NQ1, q2 = lane % NQ1;
-    const int q = (q0 * NQ1 + q1) * NQ1 + q2;
-    double Dv[ne > 0 ? ne : 1];
-    static_for<ne>([&](auto EE) {
-        constexpr int e = decltype(EE)::value;
-        Dv[e] = sDc[(e0 + e) * NQ + q];
-    });
-    double n0[3], n2[3][NP1];
-#pragma unroll
-    for (int o = 0; o < 3; o++) {
-        n0[o] = T(0, q0, o, b0);
-#pragma unroll
-        for (int x = 0; x < NP1; x++) n2[o][x] = T(2, q2, o, x);
-    }
-    double *dst = sH + J * F::HS_J + q1 * F::HS_Q1 + q2 * F::HS_Q2 + b0 * NP1 * NP1;
-#pragma unroll 1
-    for (int b1 = 0; b1 < NP1; b1++) {
-        double n01[3][3];
-        {
-            double n1[3];
-#pragma unroll
-            for (int o = 0; o < 3; o++) n1[o] = T(1, q1, o, b1);
-#pragma unroll
-            for (int o0 = 0; o0 < 3; o0++)
-#pragma unroll
-                for (int o1 = 0; o1 < 3; o1++) n01[o0][o1] = n0[o0] * n1[o1];   // unused pairs: dead code
-        }
-#pragma unroll
-        for (int b2 = 0; b2 < NP1; b2++) {
-            double pb[NQK];
-            static_for<NQK>([&](auto K) {
-                constexpr int kq = decltype(K)::value;
-                constexpr int c = L::qk(kq);
-                double v = 0.0;
-                static_for<KS::nterms(c)>([&](auto TT) {
-                    constexpr int tt = decltype(TT)::value;
-                    v += n01[KS::ord(c, tt, 0)][KS::ord(c, tt, 1)] * n2[KS::ord(c, tt, 2)][b2];
-                });
-                pb[kq] = v;
-            });
-            double H[NTK];
-#pragma unroll
-            for (int t = 0; t < NTK; t++) H[t] = 0.0;
-            static_for<ne>([&](auto EE) {
-                constexpr int e = decltype(EE)::value;
-                constexpr int t = L::tk_of(L::EIJ.c[e0 + e]), kq = L::qk_of(L::EIJ.c2[e0 + e]);
-                H[t] += Dv[e] * pb[kq];
-            });
-#pragma unroll
-            for (int t = 0; t < NTK; t++) dst[t * F::HS_T + b1 * NP1 + b2] = H[t];
-        }
-    }
-}
-
-// Consumer (thread = trial function B, trial component J; the round's test component I): the
-// test-side sum factorisation of column (B, J) over the q0 slab -- q2 and q1 contracted with the
-// 1D test tables, the slab folded into the column Kc[A] (kept in registers across the slabs).
-template <class F, bool UNI, int P>
-__device__ __forceinline__ void pc_consume(double (&Kc)[F::NEN], const double *__restrict__ sH, int q0, int B, int J,
-                                           const double *__restrict__ tab, const UniTab<P> &ut) {
-    using L = typename F::L;
-    using KS = typename F::KS;
-    constexpr int NP1 = F::NP1, NQ1 = F::NQ1, NTK = F::NTK;
-    auto T = [&](int d, int q, int k, int a) -> double {
-        if constexpr (UNI) return ut.t[d][q][k][a];
-        else return tab[((d * NQ1 + q) * 3 + k) * NP1 + a];
-    };
-    constexpr auto used01 = [](int o0, int o1) {
-        for (int t = 0; t < NTK; t++) {
-            const int c = L::tk(t);
-            for (int s = 0; s < KS::nterms(c); s++)
-                if (KS::ord(c, s, 0) == o0 && KS::ord(c, s, 1) == o1) return true;
-        }
-        return false;
-    };
-    constexpr auto used0 = [](int o0) {
-        for (int t = 0; t < NTK; t++) {
-            const int c = L::tk(t);
-            for (int s = 0; s < KS::nterms(c); s++)
-                if (KS::ord(c, s, 0) == o0) return true;
-        }
-        return false;
-    };
-    const double *src = sH + J * F::HS_J + B;
-    double Tt[3][NP1][NP1];
-#pragma unroll
-    for (int o = 0; o < 3; o++)
-#pragma unroll
-        for (int x = 0; x < NP1; x++)
-#pragma unroll
-            for (int y = 0; y < NP1; y++) Tt[o][x][y] = 0.0;
-#pragma unroll 1
-    for (int q1 = 0; q1 < NQ1; q1++) {
-        double h[NQ1][NTK];
-#pragma unroll
-        for (int q2 = 0; q2 < NQ1; q2++)
-#pragma unroll
-            for (int t = 0; t < NTK; t++) h[q2][t] = src[q1 * F::HS_Q1 + q2 * F::HS_Q2 + t * F::HS_T];
-        double S[3][3][NP1];
-#pragma unroll
-        for (int o = 0; o < 3; o++)
-#pragma unroll
-            for (int o2 = 0; o2 < 3; o2++)
-#pragma unroll
-                for (int x = 0; x < NP1; x++) S[o][o2][x] = 0.0;
-#pragma unroll
-        for (int q2 = 0; q2 < NQ1; q2++) {
-            static_for<NTK>([&](auto TK) {
-                constexpr int t = decltype(TK)::value;
-                constexpr int c = L::tk(t);
-                static_for<KS::nterms(c)>([&](auto TT) {
-                    constexpr int s = decltype(TT)::value;
-                    constexpr int o0 = KS::ord(c, s, 0), o1 = KS::ord(c, s, 1), o2 = KS::ord(c, s, 2);
-#pragma unroll
-                    for (int a2 = 0; a2 < NP1; a2++) S[o0][o1][a2] += h[q2][t] * T(2, q2, o2, a2);
-                });
-            });
-        }
-        static_for<3>([&](auto O0) {
-            constexpr int o0 = decltype(O0)::value;
-            static_for<3>([&](auto O1) {
-                constexpr int o1 = decltype(O1)::value;
-                if constexpr (used01(o0, o1)) {
-#pragma unroll
-                    for (int a1 = 0; a1 < NP1; a1++) {
-                        const double t1 = T(1, q1, o1, a1);
-#pragma unroll
-                        for (int a2 = 0; a2 < NP1; a2++) Tt[o0][a1][a2] += t1 * S[o0][o1][a2];
-                    }
-                }
-            });
-        });
-    }
-    static_for<3>([&](auto O0) {
-        constexpr int o0 = decltype(O0)::value;
-        if constexpr (used0(o0)) {
-#pragma unroll
-            for (int a0 = 0; a0 < NP1; a0++) {
-                const double t0 = T(0, q0, o0, a0);
-#pragma unroll
-                for (int a1 = 0; a1 < NP1; a1++)
-#pragma unroll
-                    for (int a2 = 0; a2 < NP1; a2++) Kc[(a0 * NP1 + a1) * NP1 + a2] += t0 * Tt[o0][a1][a2];
-            }
-        }
-    });
-}
-
 template <int P, class PH, bool JAC, bool UNI>
-__global__ void __launch_bounds__(JAC ? F3<P, PH>::NTJ : F3<P, PH>::NT, JAC ? F3<P, PH>::MINBJ : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
+__global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3<P, PH>::MINB : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
           int dbg, int bw) {
     using F = F3<P, PH>;
-    constexpr int NTH = JAC ? F::NTJ : F::NT, NWP = NTH / 32;   // threads / warps of this launch
+    constexpr int NTH = F::NT, NWP = F::NWARP;
     using L = typename F::L;
     using KS = typename F::KS;
     using State = typename F::State;
@@ -834,21 +627,6 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         if (warp == decltype(KJ)::value % NWP) {
                             double col[NKS * M];
                             PH::template dcol<3>(st, k2, j, a, b, col);
-                            if constexpr (F::PC) {
-                                // compact: structural nonzeros only, [entry][q] (lane = q: conflict-free)
-                                static_for<M>([&](auto II) {
-                                    constexpr int i = decltype(II)::value;
-                                    static_for<NTK>([&](auto TK) {
-                                        constexpr int t = decltype(TK)::value;
-                                        constexpr int e = L::eij_find(i, j, L::tk(t), k2);
-                                        if constexpr (e >= 0) {
-                                            const double v = col[L::tk(t) * M + i] * dV;
-                                            chk += v;
-                                            sD[e * NQ + q] = v;
-                                        }
-                                    });
-                                });
-                            } else {
 #pragma unroll
                             for (int i = 0; i < M; i++) {
                                 // block layout [trial kind k][test kind t]: this column's NTK entries
@@ -869,7 +647,6 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                                     for (int t = 0; t < NTK; t++) dst[t] = v[t];
                                 }
                             }
-                            }
                         }
                     });
                     if (!isfinite(chk)) errbits |= 2;
@@ -882,118 +659,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             // lanes write one 32-byte sector of a CSR row) are dealt round-robin over all NT
             // threads -- 432 tasks on 128 threads = 14 warp-passes instead of 4 passes of the
             // 108 (B, J) threads on 4 warps (16 warp-passes, the last warp 12/32 lanes busy).
-            if constexpr (F::WS) {
-                // warp specialisation: producers (warp J < M, lane = (b0, q1, q2)) fill H round
-                // r = (I, q0) into buffer r & 1 while consumers (warps M..2M-1, thread (B, J))
-                // contract round r - 1; named barriers 1 + b (full) and 3 + b (empty)
-                double *sH = sm + F::O_H;
-                constexpr int NRND = M * NQ1;
-                if (warp < M) {
-                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(F::PREG));
-#pragma unroll 1
-                    for (int r = 0; r < NRND; r++) {
-                        const int bsel = r & 1;
-                        if (r >= 2) asm volatile("bar.sync %0, %1;" ::"r"(3 + bsel), "n"(NTH) : "memory");
-                        if (lane < NEN) {
-                            const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
-                            double *hb = sH + bsel * F::HBUF;
-                            static_for<M * M>([&](auto IJ) {
-                                constexpr int Ic = decltype(IJ)::value / M, Jc = decltype(IJ)::value % M;
-                                if (I == Ic && warp == Jc) pc_produce<F, UNI, P, Ic, Jc>(sD, hb, q0, lane, sTab, ut);
-                            });
-                        }
-                        asm volatile("bar.arrive %0, %1;" ::"r"(1 + bsel), "n"(NTH) : "memory");
-                    }
-                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 128;");
-                } else {
-                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(F::CREG));
-                    const int ct = tid - M * 32;
-                    const bool cons = ct < NEN * M;
-                    const int B = ct / M, J = ct - (ct / M) * M;
-                    double Kc[NEN];
-#pragma unroll 1
-                    for (int r = 0; r < NRND; r++) {
-                        const int bsel = r & 1;
-                        const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
-                        asm volatile("bar.sync %0, %1;" ::"r"(1 + bsel), "n"(NTH) : "memory");
-                        if (q0 == 0) {
-#pragma unroll
-                            for (int A = 0; A < NEN; A++) Kc[A] = 0.0;
-                        }
-                        if (cons) pc_consume<F, UNI, P>(Kc, sH + bsel * F::HBUF, q0, B, J, sTab, ut);
-                        if (r + 2 < NRND) asm volatile("bar.arrive %0, %1;" ::"r"(3 + bsel), "n"(NTH) : "memory");
-                        if (q0 == NQ1 - 1 && cons && !(dbg & 2)) {
-                            const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
-                            int P0[NP1], P1[NP1], P2[NP1], W1[NP1], W2[NP1];
-#pragma unroll
-                            for (int x = 0; x < NP1; x++) {
-                                P0[x] = sPosE[x * NP1 + b0];
-                                P1[x] = sPosE[NP1 * NP1 + x * NP1 + b1];
-                                P2[x] = sPosE[2 * NP1 * NP1 + x * NP1 + b2];
-                                W1[x] = sW[NP1 + x];
-                                W2[x] = sW[2 * NP1 + x];
-                            }
-#pragma unroll
-                            for (int A = 0; A < NEN; A++) {
-                                const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
-                                const int co = (P0[a0] * W1[a1] + P1[a1]) * W2[a2] + P2[a2];
-                                atomicAdd(val + sRS[A * M + I] + (long long)co * M + J, Kc[A]);
-                            }
-                        }
-                    }
-                    if constexpr (IGA_SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 128;");
-                }
-            } else if constexpr (F::PC) {
-                // rounds r = (I, q0): warps produce H of round r+1 into one buffer while the
-                // (B, J) threads consume round r from the other -- one barrier per round
-                static_assert(F::NWARP == M, "one producer warp per trial component");
-                double *sH = sm + F::O_H;
-                const bool cons = tid < NEN * M;
-                const int B = tid / M, J = tid - (tid / M) * M;
-                constexpr int NRND = M * NQ1;
-                auto produce = [&](int r) {
-                    if (lane < NEN) {
-                        const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
-                        double *hb = sH + (r & 1) * F::HBUF;
-                        static_for<M * M>([&](auto IJ) {
-                            constexpr int Ic = decltype(IJ)::value / M, Jc = decltype(IJ)::value % M;
-                            if (I == Ic && warp == Jc) pc_produce<F, UNI, P, Ic, Jc>(sD, hb, q0, lane, sTab, ut);
-                        });
-                    }
-                };
-                double Kc[NEN];
-                produce(0);
-                __syncthreads();
-#pragma unroll 1
-                for (int r = 0; r < NRND; r++) {
-                    const int I = r / NQ1, q0 = r - (r / NQ1) * NQ1;
-                    if (q0 == 0) {
-#pragma unroll
-                        for (int A = 0; A < NEN; A++) Kc[A] = 0.0;
-                    }
-                    if (cons) pc_consume<F, UNI, P>(Kc, sH + (r & 1) * F::HBUF, q0, B, J, sTab, ut);
-                    if (r + 1 < NRND) produce(r + 1);
-                    if (q0 == NQ1 - 1 && cons && !(dbg & 2)) {
-                        const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
-                        int P0[NP1], P1[NP1], P2[NP1], W1[NP1], W2[NP1];
-#pragma unroll
-                        for (int x = 0; x < NP1; x++) {
-                            P0[x] = sPosE[x * NP1 + b0];
-                            P1[x] = sPosE[NP1 * NP1 + x * NP1 + b1];
-                            P2[x] = sPosE[2 * NP1 * NP1 + x * NP1 + b2];
-                            W1[x] = sW[NP1 + x];
-                            W2[x] = sW[2 * NP1 + x];
-                        }
-#pragma unroll
-                        for (int A = 0; A < NEN; A++) {
-                            const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
-                            const int co = (P0[a0] * W1[a1] + P1[a1]) * W2[a2] + P2[a2];
-                            atomicAdd(val + sRS[A * M + I] + (long long)co * M + J, Kc[A]);
-                        }
-                    }
-                    __syncthreads();
-                }
-            } else if constexpr (!F::SYMJ && IGA_BAL) {
+            if constexpr (!F::SYMJ && IGA_BAL) {
 #pragma unroll 1
                 for (int c = tid; c < NEN * M * M; c += NTH) {
                     const int I = c / (NEN * M), r = c - I * (NEN * M), B = r / M, J = r - B * M;
@@ -1126,7 +792,7 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
         if (ce != cudaSuccess) { set_error(std::string("fused3d smem: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
     }
     int occ = 1;
-    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, true, UNI>, FF::NTJ, smem);
+    if (jac) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, true, UNI>, FF::NT, smem);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused3d<P, PH, false, UNI>, FF::NT, smem);
     occ = std::max(occ, 1);
     const long long nel = s->nel_local;
@@ -1145,7 +811,7 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
         int bw = (int)(60e6 / (3.0 * (ne2 + P) * row_bytes)) - P;
         if (s->bw_opt > 0) bw = s->bw_opt;
         bw = std::max(1, std::min(bw, ne1));
-        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NTJ, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
+        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
         else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
         launches++;
     }

@@ -139,12 +139,6 @@ struct Lists {
             if (EIJ.i[e] == i && EIJ.j[e] == j) n++;
         return n;
     }
-    // position of the entry (i, j, c, c2) within EIJ; -1 if structurally zero
-    static constexpr int eij_find(int i, int j, int c, int c2) {
-        for (int e = 0; e < EIJ.n; e++)
-            if (EIJ.i[e] == i && EIJ.j[e] == j && EIJ.c[e] == c && EIJ.c2[e] == c2) return e;
-        return -1;
-    }
     // position of entry ee (in E order) within EIJ
     static constexpr int eij_of(int ee) {
         for (int e = 0; e < EIJ.n; e++)
