@@ -26,7 +26,13 @@ template <int P> struct Tile2 {
     // width te1 <= TE1 so that the tile count fills the SMs in whole rounds (wave quantisation)
     static constexpr int TE1 = P == 2 ? 36 : 32;
     // 12 warps (168 registers, no spills with the direct scatter; measured best for p = 2 and 3)
-    static constexpr int NWARP = 12;
+#ifndef IGA_NW2
+#define IGA_NW2 12
+#endif
+#ifndef IGA_NW3
+#define IGA_NW3 12
+#endif
+    static constexpr int NWARP = P == 2 ? IGA_NW2 : IGA_NW3;
     static constexpr int NB0 = TE0 + P, NB1 = TE1 + P;      // touched node box (uniform knots)
     static constexpr int NSL = (2 * P + 1) * (2 * P + 1);   // stencil slots per row
 };

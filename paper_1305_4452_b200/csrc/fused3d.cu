@@ -30,6 +30,12 @@
 #ifndef IGA_HOIST
 #define IGA_HOIST 1  // trial 1D values hoisted out of the contraction loops (see tsf_column_3d)
 #endif
+#ifndef IGA_TAIL
+#define IGA_TAIL 1   // split the partial last pass of column tasks over q0 sub-ranges
+#endif
+#ifndef IGA_DYN
+#define IGA_DYN 1    // dynamic element order through a global counter (see the element loop)
+#endif
 #ifndef IGA_BAL
 #define IGA_BAL 1   // column tasks dealt round-robin over all threads (phase 5, non-symmetric forms)
 #endif
@@ -111,7 +117,8 @@ struct F3 {
 template <class F, bool UNI, int P>
 __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double *__restrict__ Dsm, int ij,
                                               int b0, int b1, int b2, const double *__restrict__ tab,
-                                              const UniTab<P> &ut, const double *__restrict__ pbS) {
+                                              const UniTab<P> &ut, const double *__restrict__ pbS,
+                                              int q0lo = 0, int q0hi = F::NQ1) {
     using L = typename F::L;
     using KS = typename F::KS;
     constexpr int NP1 = F::NP1, NQ1 = F::NQ1, NEN = F::NEN, NTK = F::NTK, NQK = F::NQK, DB = F::DB;
@@ -157,7 +164,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
             for (int k = 0; k < 3; k++) n2all[q][k] = TS(2, q, k, b2);
     }
 #pragma unroll 1
-    for (int q0 = 0; q0 < NQ1; q0++) {
+    for (int q0 = q0lo; q0 < q0hi; q0++) {   // a q0 sub-range: partial column (tail split)
         double n0[3];
 #pragma unroll
         for (int k = 0; k < 3; k++) n0[k] = TS(0, q0, k, b0);
@@ -332,7 +339,13 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         }
         __syncthreads();
     }
-    for (long long el = blockIdx.x; el < nelem; el += gridDim.x) {
+    // Dynamic element order (IGA_DYN): after its first element a CTA takes the next unprocessed one
+    // from a global counter, so all CTAs stay on consecutive elements of the L2-blocked order and
+    // the CSR rows they add into stay L2-resident (a static stride lets the 296 CTAs drift apart by
+    // hundreds of pencils over ~7000 elements each: DRAM traffic was independent of bw, 5.8-6.8x
+    // the algorithmic bytes).
+    __shared__ long long sEl;
+    for (long long el = blockIdx.x; el < nelem;) {
         // L2-blocked element order: pencils along axis 2, swept over axis 0 inside blocks of `bw`
         // pencils along axis 1, so the CSR rows an element layer leaves half-accumulated are
         // still in L2 when the next layer adds to them (the red.add scatter then reads each
@@ -660,12 +673,25 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             // threads -- 432 tasks on 128 threads = 14 warp-passes instead of 4 passes of the
             // 108 (B, J) threads on 4 warps (16 warp-passes, the last warp 12/32 lanes busy).
             if constexpr (!F::SYMJ && IGA_BAL) {
+                // The last NCOL mod NT columns (a partial pass: 48 of 432 for VMS) are split in two
+                // q0 sub-ranges on two threads each (partial columns, both added with red.add): the
+                // tail takes 2/3 of a column time instead of a whole one while the rest of the
+                // CTA waits at the barrier (IGA_TAIL=0: whole tail columns).
+                constexpr int NCOL = NEN * M * M, NFULL = NCOL / NTH * NTH, NTAIL = NCOL - NFULL;
+                constexpr bool SPLIT = IGA_TAIL && NTAIL > 0 && 2 * NTAIL <= NTH && NQ1 >= 2;
 #pragma unroll 1
-                for (int c = tid; c < NEN * M * M; c += NTH) {
+                for (int cc = tid; cc < (SPLIT ? NFULL + 2 * NTAIL : NCOL); cc += NTH) {
+                    int c = cc, q0lo = 0, q0hi = NQ1;
+                    if (SPLIT && cc >= NFULL) {
+                        const int h = (cc - NFULL) / NTAIL;                 // 0: q0 < NQ1-1, 1: last slab
+                        c = NFULL + (cc - NFULL) - h * NTAIL;
+                        q0lo = h ? NQ1 - 1 : 0;
+                        q0hi = h ? NQ1 : NQ1 - 1;
+                    }
                     const int I = c / (NEN * M), r = c - I * (NEN * M), B = r / M, J = r - B * M;
                     const int b0 = B / (NP1 * NP1), b1 = (B / NP1) % NP1, b2 = B % NP1;
                     double Kc[NEN];
-                    if (!(dbg & 1)) tsf_column_3d<F, UNI, P>(Kc, sD, I * M + J, b0, b1, b2, sTab, ut, sm + F::O_PB);
+                    if (!(dbg & 1)) tsf_column_3d<F, UNI, P>(Kc, sD, I * M + J, b0, b1, b2, sTab, ut, sm + F::O_PB, q0lo, q0hi);
                     else {
 #pragma unroll
                         for (int A = 0; A < NEN; A++) Kc[A] = sD[A * 7 + J];
@@ -765,7 +791,14 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 }
             }
         }
-        __syncthreads();
+        if constexpr (IGA_DYN) {
+            if (tid == 0) sEl = (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
+            __syncthreads();
+            el = sEl;
+        } else {
+            __syncthreads();
+            el += gridDim.x;
+        }
     }
     if (errbits) atomicOr(s.errflag, errbits);
 }
@@ -811,6 +844,10 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
         int bw = (int)(60e6 / (3.0 * (ne2 + P) * row_bytes)) - P;
         if (s->bw_opt > 0) bw = s->bw_opt;
         bw = std::max(1, std::min(bw, ne1));
+        if (IGA_DYN) {
+            cudaError_t me = cudaMemsetAsync(s->dev.wq, 0, sizeof(unsigned long long), st);
+            if (me != cudaSuccess) { set_error(std::string("fused3d counter: ") + cudaGetErrorString(me)); return IGA_ERR_CUDA; }
+        }
         if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
         else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
         launches++;

@@ -58,6 +58,7 @@ struct SpaceDev {
     const double *wts;        // [nnodes]        (or nullptr)
     long long nnodes;
     int *errflag;             // device error flag (bit 0: detJ<=0, bit 1: non-finite)
+    unsigned long long *wq;   // element work counter of the persistent 3D kernel (zeroed per launch)
     // multi-rank: CSR rows of halo functions (sub-box id s != 0, bit d-1-a set = halo on axis a)
     // accumulate into the library's halo buffer at hbase[s]; owned rows (s = 0) into csr_val
     double *halo;

@@ -705,6 +705,7 @@ static iga_status create(const iga_space_desc *d, const iga_dist *dist, int devi
         if ((st = dalloc(s, &s->errflag, 1)) != IGA_OK) goto fail;
         CUDA_TRY(cudaMemset(s->errflag, 0, sizeof(int)));
         s->dev.errflag = s->errflag;
+        if ((st = dalloc(s, &s->dev.wq, 1)) != IGA_OK) goto fail;
         if (s->nranks > 1 && (st = dist_setup(s, dist)) != IGA_OK) goto fail;
         // quadrature-point coefficient workspace: <= 4 GiB, sized to the local element count
         size_t want = (size_t)s->nqp_local * 512 * sizeof(double);
