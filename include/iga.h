@@ -175,6 +175,10 @@ iga_status iga_form_jacobian(iga_space s, const iga_phys *phys, double a, double
 /* Host-buffer variant (end-to-end path): copies U/Udot host->device, forms J (and F if
  * F_host != NULL) and copies csr_val / F back, all on `stream`; returns after the stream
  * synchronises.  Host buffers should be pinned for full PCIe bandwidth.
+ * On 3D spaces with uniform knots along axis 0 the elements are assembled in slabs along axis 0
+ * (option "hb_slabs", default 32; 0 = one launch) and each node layer's CSR rows are copied back
+ * on a second stream as soon as the last element touching the layer is assembled, so the copy
+ * of the values overlaps the assembly.
  * Device memory: the first call allocates the device staging buffers (2 ndof + nnz + nrows
  * doubles: 34 GB for config 5) and keeps them with the space (freed by iga_space_destroy);
  * IGA_ERR_NOMEM if that allocation fails.  Single-rank spaces only (IGA_ERR_STATE otherwise). */

@@ -40,6 +40,10 @@ struct iga_space_s {
     // SpaceDev, whose size the fused kernels' register allocation turned out to be sensitive to)
     const double *dknots[3] = {nullptr, nullptr, nullptr};
     double *hb_U = nullptr, *hb_Ud = nullptr, *hb_val = nullptr, *hb_F = nullptr;   // host-buffer path staging
+    int hb_slabs = 32;                   // host path: element slabs along axis 0 whose finished rows are
+                                         // copied back while later slabs assemble (option "hb_slabs", 0 = off)
+    cudaStream_t hb_copy = nullptr;      // host path: device-to-host copy stream
+    std::vector<cudaEvent_t> hb_ev;      // host path: one event per slab
     int el_lo[3] = {0, 0, 0}, el_hi[3] = {1, 1, 1};
     long long ndof_global = 0, nrows_owned = 0, nnz_owned = 0, nqp_local = 0, nel_local = 0;
     // device allocations owned by the space

@@ -274,6 +274,8 @@ static void free_space(iga_space_s *s) {
     prof_collect(s);
     dist_destroy(s);
     for (cudaEvent_t e : s->prof_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : s->hb_ev) cudaEventDestroy(e);
+    if (s->hb_copy) cudaStreamDestroy(s->hb_copy);
     for (void *p : s->allocs) cudaFree(p);
     for (void *p : s->gm_buf) if (p) cudaFree(p);
     for (auto &c : s->dr_cache) if (c.first) cudaFree(c.first);
@@ -838,6 +840,84 @@ iga_status iga_form_jacobian(iga_space s, const iga_phys *phys, double a, double
     return st;
 }
 
+// Host-buffer path, pipelined (3D, uniform axis 0): the outputs are zeroed once, the elements
+// are assembled in slabs along axis 0, and the CSR rows of every node layer go back to the host
+// on a second stream as soon as the last element touching that layer has been assembled (its
+// slab's event), so the device-to-host copy of the values -- 33.6 GB for config 5, longer than
+// the assembly itself -- runs under the assembly of the later slabs.  A layer g0's rows are one
+// contiguous range of the CSR values: offset m^2 S0(g0) T1 T2, length m^2 W0(g0) T1 T2 (the
+// closed-form row start, single rank).  Layer completion comes from the Alg. 1
+// element -> function map (uniform: element e touches first0 + e + k, k = 0..p, mod nu), so on a
+// periodic axis the first p layers (also touched by the last elements) go last.
+static iga_status form_host_pipelined(iga_space_s *s, const iga_phys *phys, double a, double b, const double *dU,
+                                      const double *dUd, double *dV, double *dF, double *val_h, double *F_h,
+                                      cudaStream_t cs) {
+    const int lo0 = s->el_lo[0], ne0 = s->el_hi[0] - lo0, nu0 = s->nu[0], p0 = s->p[0], m = s->dof;
+    const int nsl = std::min(s->hb_slabs, ne0);
+    const AxisDev &ax0 = s->dev.ax[0];
+    std::vector<int> done(nu0, -1);                       // slab after which layer g is complete
+    std::vector<int> bnd(nsl + 1);                        // slab j = elements [bnd[j], bnd[j+1])
+    for (int j = 0; j <= nsl; j++) bnd[j] = (int)((long long)j * ne0 / nsl);
+    for (int e = 0, sl = 0; e < ne0; e++) {
+        while (e >= bnd[sl + 1]) sl++;
+        for (int k = 0; k <= p0; k++) {
+            int g = ax0.first0 + lo0 + e + k;
+            g %= nu0;
+            done[g] = std::max(done[g], sl);
+        }
+    }
+    for (int g = 0; g < nu0; g++) if (done[g] < 0) done[g] = nsl - 1;   // (every function has support)
+    long long T1 = 0, T2 = 0;
+    for (int w : s->rowW[1]) T1 += w;
+    for (int w : s->rowW[2]) T2 += w;
+    const long long per = (long long)m * m * T1 * T2;     // values per unit of axis-0 width
+    std::vector<long long> S0(nu0 + 1, 0);
+    for (int g = 0; g < nu0; g++) S0[g + 1] = S0[g] + (long long)s->rowW[0][g] * per;
+    cudaError_t ce = cudaSuccess;
+    if (!s->hb_copy) ce = cudaStreamCreateWithFlags(&s->hb_copy, cudaStreamNonBlocking);
+    while (ce == cudaSuccess && (int)s->hb_ev.size() < nsl + 1) {
+        cudaEvent_t ev;
+        ce = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (ce == cudaSuccess) s->hb_ev.push_back(ev);
+    }
+    if (ce != cudaSuccess) { set_error(std::string("host pipeline: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, s->device);
+    k_zero_pair(dV, s->nnz_owned, dF, dF ? s->nrows_owned : 0, cs, nsm);
+    int launches = 1;
+    iga_status st = IGA_OK;
+    for (int j = 0; j < nsl && st == IGA_OK; j++) {
+        int lo[3], hi[3];
+        for (int d = 0; d < 3; d++) { lo[d] = s->el_lo[d]; hi[d] = s->el_hi[d]; }
+        lo[0] = lo0 + bnd[j];
+        hi[0] = lo0 + bnd[j + 1];
+        st = launch_form_box(s, phys, a, b, dU, dUd, dV, dF, cs, lo, hi);
+        launches += s->last_launches;
+        if (st != IGA_OK) break;
+        ce = cudaEventRecord(s->hb_ev[j], cs);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s->hb_copy, s->hb_ev[j], 0);
+        for (int g = 0; g < nu0 && ce == cudaSuccess;) {     // contiguous runs of layers done after slab j
+            if (done[g] != j) { g++; continue; }
+            int h = g;
+            while (h < nu0 && done[h] == j) h++;
+            ce = cudaMemcpyAsync(val_h + S0[g], dV + S0[g], (size_t)(S0[h] - S0[g]) * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s->hb_copy);
+            g = h;
+        }
+        if (ce != cudaSuccess) break;
+    }
+    if (st == IGA_OK && ce == cudaSuccess && F_h) {
+        ce = cudaEventRecord(s->hb_ev[nsl], cs);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s->hb_copy, s->hb_ev[nsl], 0);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(F_h, dF, (size_t)s->nrows_owned * sizeof(double), cudaMemcpyDeviceToHost, s->hb_copy);
+    }
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s->hb_copy);
+    s->last_launches = launches;
+    if (ce != cudaSuccess) { set_error(std::string("host pipeline: ") + cudaGetErrorString(ce)); return IGA_ERR_CUDA; }
+    return st;
+}
+
 iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, double b, const double *U_host,
                                   const double *Udot_host, double *csr_val_host, double *F_host, void *stream) {
     iga_status st = check_phys(s, phys);
@@ -864,7 +944,11 @@ iga_status iga_form_jacobian_host(iga_space s, const iga_phys *phys, double a, d
     double *dU = s->hb_U, *dUd = Udot_host ? s->hb_Ud : nullptr, *dV = s->hb_val, *dF = F_host ? s->hb_F : nullptr;
     ce = cudaMemcpyAsync(dU, U_host, nU * sizeof(double), cudaMemcpyHostToDevice, cs);
     if (ce == cudaSuccess && Udot_host) ce = cudaMemcpyAsync(dUd, Udot_host, nU * sizeof(double), cudaMemcpyHostToDevice, cs);
-    if (ce == cudaSuccess) {
+    const int ne0 = s->el_hi[0] - s->el_lo[0];
+    const bool pipe = s->hb_slabs > 1 && s->dim == 3 && s->dev.ax[0].uniform && ne0 >= 2 * s->hb_slabs && !s->force_split;
+    if (ce == cudaSuccess && pipe) {
+        st = form_host_pipelined(s, phys, a, b, dU, dUd, dV, dF, csr_val_host, F_host, cs);
+    } else if (ce == cudaSuccess) {
         st = launch_form(s, phys, a, b, dU, dUd, dV, dF, cs);
         const int nl = s->last_launches;
         if (st == IGA_OK) ce = cudaMemcpyAsync(csr_val_host, dV, nz * sizeof(double), cudaMemcpyDeviceToHost, cs);
@@ -1047,6 +1131,7 @@ iga_status iga_space_set_option(iga_space s, const char *key, long long value) {
     if (std::strcmp(key, "general") == 0) { s->force_general = value != 0; return IGA_OK; }
     if (std::strcmp(key, "dbg") == 0) { s->dbg = (int)value; return IGA_OK; }
     if (std::strcmp(key, "bw") == 0) { s->bw_opt = (int)value; return IGA_OK; }
+    if (std::strcmp(key, "hb_slabs") == 0) { s->hb_slabs = (int)std::max<long long>(0, value); return IGA_OK; }
     if (std::strcmp(key, "gmres_host") == 0) { s->gm_host_ctrl = value != 0; return IGA_OK; }
     set_error(std::string("unknown option ") + key);
     return IGA_ERR_PARAM;
