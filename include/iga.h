@@ -320,7 +320,9 @@ int iga_profile_read(iga_space s, int max, char *names /* [max][32] */, int *lau
 /* Diagnostics (K8): measured ceilings on this device.  which: 0 DFMA flop/s, 1 DMMA
  * (mma.sync m8n8k4 f64) flop/s, 2 DFMA+DMMA mixed flop/s, 3/4/5 fp64 red.add per second with
  * 32/4/1 lanes per contiguous group into a `param`-double (default 26 MB) array, 6 store
- * bytes/s, 7 shared-memory fp64 atomics/s.  Returns < 0 on error. */
+ * bytes/s, 7 shared-memory fp64 atomics/s, 8/10 bulk reductions (96/384 B) per second, 9 fp64
+ * red.add/s in the config-5 lane pattern, 11/12 warp-level 128-bit broadcast loads per second
+ * (4 distinct addresses per warp, shared memory / L1-resident global).  Returns < 0 on error. */
 double iga_microbench(int device, int which, long long param);
 
 const char *iga_last_error(void);

@@ -172,7 +172,7 @@ def make_phys(kind: int, params) -> _Phys:
 MICROBENCH = {0: "dfma_flops", 1: "dmma_flops", 2: "dfma_dmma_mixed_flops", 3: "red_f64_warp_contig_per_s",
               4: "red_f64_sector_per_s", 5: "red_f64_scattered_per_s", 6: "store_bytes_per_s",
               7: "smem_atomic_f64_per_s", 8: "bulkred_96B_ops_per_s", 9: "red_f64_c5pattern_per_s",
-              10: "bulkred_384B_ops_per_s"}
+              10: "bulkred_384B_ops_per_s", 11: "lds128_bcast_warp_loads_per_s", 12: "ldg128_bcast_warp_loads_per_s"}
 
 
 def microbench(device: int = 0, which=None, param: int = 0) -> dict:

@@ -144,6 +144,37 @@ __global__ void k_smem_atomic(double *out, int reps) {
     if (threadIdx.x == 0 && buf[0] == -1.0) out[0] = buf[1];
 }
 
+// Broadcast 128-bit loads, the 3D contraction's coefficient pattern: lanes (B, J) = (lane / 4,
+// lane % 4) read block J's double2 (4 distinct conflict-free 16-byte addresses per warp
+// instruction), 10 loads feeding 20 independent DFMAs per iteration.  V = 0: shared memory,
+// 1: global (L1-resident).  Shows that a warp-uniform 128-bit load costs 4 data-pipe wavefronts
+// from either memory.
+template <int V>
+__global__ void __launch_bounds__(128, 4) k_bcast(const double2 *g, double *out, int iters) {
+    __shared__ double2 sm[4 * 42 * 12];
+    const int tid = threadIdx.x, J = tid & 3;
+    const double2 *gb = g + (size_t)blockIdx.x * 4 * 42 * 12;
+    for (int i = tid; i < 4 * 42 * 12; i += blockDim.x) sm[i] = gb[i];
+    __syncthreads();
+    double acc[20];
+#pragma unroll
+    for (int i = 0; i < 20; i++) acc[i] = 0.0;
+    const double pb[5] = {1.0 + tid, 2.0, 3.0, 4.0, 5.0};
+    for (int it = 0; it < iters; it++) {
+        const int base = ((it % 12) * 4 + J) * 42;   // 42 double2 per block: J offsets in distinct banks
+#pragma unroll
+        for (int x = 0; x < 10; x++) {
+            const double2 v = V == 0 ? sm[base + x] : gb[base + x];
+            acc[2 * x] += v.x * pb[(2 * x) % 5];
+            acc[2 * x + 1] += v.y * pb[(2 * x + 1) % 5];
+        }
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int i = 0; i < 20; i++) t += acc[i];
+    out[blockIdx.x * blockDim.x + tid] = t;
+}
+
 }  // namespace
 
 extern "C" double iga_microbench(int device, int which, long long param) {
@@ -200,6 +231,15 @@ extern "C" double iga_microbench(int device, int which, long long param) {
             k_red_c5<<<blocks * 4, thr>>>(buf, n, 64);
             work = (double)blocks * 4 * (thr / 32) * 27 * 64;
             break;
+        case 11: case 12: {   // broadcast 128-bit loads (shared / L1-resident global): warp-loads/s
+            const int grid = nsm * 4, iters = 1 << 14;
+            const size_t need = (size_t)grid * 4 * 42 * 12 * 2;   // doubles
+            if ((size_t)n < need) { work = 0.0; break; }
+            if (which == 11) k_bcast<0><<<grid, 128>>>((const double2 *)buf, buf + need, iters);
+            else k_bcast<1><<<grid, 128>>>((const double2 *)buf, buf + need, iters);
+            work = (double)grid * 4 * iters * 10;
+            break;
+        }
         case 10:  // bulk reductions of 384 B per op
             k_bulkred<<<blocks, thr>>>(buf, n, 384, 64);
             work = (double)blocks * (thr / 32) * 64;
