@@ -53,8 +53,117 @@ struct UniTab {
 template <class PH, class = void> struct PhysJState { static constexpr int value = 0; };
 template <class PH> struct PhysJState<PH, std::void_t<decltype(PH::JSTATE)>> { static constexpr int value = PH::JSTATE; };
 
-template <int P, class PH>
+// ---- fully sum-factorised contraction (FS): compile-time tables ----
+// K_IJ[A, B] = sum_q sum_(t,k) P_t(A,q) D_IJ,tk(q) P_k(B,q) with every kind a sum of separable
+// terms prod_d T_d[q_d][o_d][a_d] is contracted one axis at a time for test AND trial functions:
+//   stage 1 (axis 2):  X1_G[q0 q1][a2 b2] = sum_(tau,kap in G) sum_q2 T2[q2][o2 tau][a2] T2[q2][o2 kap][b2] D_IJ,t(tau)k(kap)(q)
+//   stage 2+3 (axes 1, 0):  K_IJ[A, B] = sum_G sum_q0 TT0_G[q0][a0 b0] sum_q1 T1[q1][o1 ta][a1] T1[q1][o1 ka][b1] X1_G[q0 q1][a2 b2]
+// where a group G = (test class ta, trial class ka) collects the terms by their (axis-0, axis-1)
+// derivative orders.  Every loaded coefficient then feeds 3-9 FMAs held in registers (the
+// test-side column form reads the whole D block once per column and point: 1 FMA per load).
+template <class L>
+struct FsMeta {
+    using KS = typename L::KS;
+    static constexpr int M = L::M;
+    struct Term { int k, o0, o1, o2; };           // kind index (t or kq) and derivative orders
+    struct Terms { int n; Term t[16]; };
+    static constexpr Terms make_terms(bool test) {
+        Terms T{};
+        const int nk = test ? L::NTK : L::NQK;
+        for (int k = 0; k < nk; k++) {
+            const int c = test ? L::tk(k) : L::qk(k);
+            for (int s = 0; s < KS::nterms(c); s++) {
+                T.t[T.n].k = k;
+                T.t[T.n].o0 = KS::ord(c, s, 0);
+                T.t[T.n].o1 = KS::ord(c, s, 1);
+                T.t[T.n].o2 = KS::ord(c, s, 2);
+                T.n++;
+            }
+        }
+        return T;
+    }
+    static constexpr Terms TT = make_terms(true), QT = make_terms(false);
+    struct Cls { int n; int o0[16], o1[16]; };
+    static constexpr Cls make_cls(const Terms &T) {
+        Cls C{};
+        for (int i = 0; i < T.n; i++) {
+            bool seen = false;
+            for (int c = 0; c < C.n; c++) seen = seen || (C.o0[c] == T.t[i].o0 && C.o1[c] == T.t[i].o1);
+            if (!seen) { C.o0[C.n] = T.t[i].o0; C.o1[C.n] = T.t[i].o1; C.n++; }
+        }
+        return C;
+    }
+    static constexpr Cls TA = make_cls(TT), KA = make_cls(QT);
+    static constexpr int NTA = TA.n, NKA = KA.n, NG = NTA * NKA;
+    static constexpr int cls(const Cls &C, int o0, int o1) {
+        for (int c = 0; c < C.n; c++) if (C.o0[c] == o0 && C.o1[c] == o1) return c;
+        return -1;
+    }
+    // combos (test term, trial term) of group g = ta * NKA + ka
+    static constexpr int ncombo(int g) {
+        int n = 0;
+        for (int a = 0; a < TT.n; a++)
+            for (int b = 0; b < QT.n; b++)
+                if (cls(TA, TT.t[a].o0, TT.t[a].o1) == g / NKA && cls(KA, QT.t[b].o0, QT.t[b].o1) == g % NKA) n++;
+        return n;
+    }
+    static constexpr int combo(int g, int c, bool test) {
+        int n = 0;
+        for (int a = 0; a < TT.n; a++)
+            for (int b = 0; b < QT.n; b++)
+                if (cls(TA, TT.t[a].o0, TT.t[a].o1) == g / NKA && cls(KA, QT.t[b].o0, QT.t[b].o1) == g % NKA) {
+                    if (n == c) return test ? a : b;
+                    n++;
+                }
+        return -1;
+    }
+    static constexpr int MAXC = [] { int m = 1; for (int g = 0; g < NG; g++) m = ncombo(g) > m ? ncombo(g) : m; return m; }();
+    static constexpr int cbase(int g) { int n = 0; for (int x = 0; x < g; x++) n += ncombo(x); return n; }
+    static constexpr int NCMB = cbase(NG);              // all (test term, trial term) combos
+    // axis-0 order pairs (o0 test, o0 trial): stage 3 sums the groups of one pair first
+    struct O0P { int n; int a[16], b[16]; };
+    static constexpr O0P make_o0p() {
+        O0P P{};
+        for (int g = 0; g < NG; g++) {
+            const int a = TA.o0[g / NKA], b = KA.o0[g % NKA];
+            bool seen = false;
+            for (int p = 0; p < P.n; p++) seen = seen || (P.a[p] == a && P.b[p] == b);
+            if (!seen) { P.a[P.n] = a; P.b[P.n] = b; P.n++; }
+        }
+        return P;
+    }
+    static constexpr O0P PO = make_o0p();
+    static constexpr int NO0P = PO.n;
+    static constexpr bool in_o0p(int g, int p) { return TA.o0[g / NKA] == PO.a[p] && KA.o0[g % NKA] == PO.b[p]; }
+    // compact coefficient index of (i, j, contraction kind c, c2) in the (i, j, c, c2)-ordered list
+    static constexpr int eij(int i, int j, int c, int c2) {
+        for (int e = 0; e < L::EIJ.n; e++)
+            if (L::EIJ.i[e] == i && L::EIJ.j[e] == j && L::EIJ.c[e] == c && L::EIJ.c2[e] == c2) return e;
+        return -1;
+    }
+};
+
+// FS stage-1 coefficient offsets per (I, J) and combo (__grid_constant__); a structurally zero
+// coefficient points at a zero slot of every point's row, so one copy of the stage-1 code serves
+// all 16 blocks with the same work per warp
+template <int NIJ, int NCMB>
+struct alignas(4) FsTab { unsigned char off[NIJ][(NCMB + 3) / 4 * 4]; };   // rows padded to whole words
+
+// FS is used for the uniform-table kernels whose CTA has one warp per trial component (VMS: m = 4,
+// 128 threads; Neo-Hooke: m = 3, 96 threads; Cahn-Hilliard: m = 1, 32 threads)
+#ifndef IGA_FS_NH
+#define IGA_FS_NH 1
+#endif
+#ifndef IGA_FS_CH
+#define IGA_FS_CH 1
+#endif
+template <class PH> struct FsOk {
+    static constexpr bool value = PH::M == 4 || (PH::M == 3 && IGA_FS_NH) || (PH::M == 1 && IGA_FS_CH);
+};
+
+template <int P, class PH, bool FS = false>
 struct F3 {
+    static constexpr bool FSC = FS && P == 2;                  // FS contraction + compact D
     static constexpr int M = PH::M;
     static constexpr int NP1 = P + 1, NQ1 = P + 1, NQ = NQ1 * NQ1 * NQ1, NEN = NP1 * NP1 * NP1;
     static constexpr int NCOMBO = M * M;
@@ -64,7 +173,10 @@ struct F3 {
     using KS = typename L::KS;
     static constexpr int NKS = KS::NKS, NC = KS::NC, NR = L::NR, NTK = L::NTK, NQK = L::NQK;
     static constexpr int DB = (NTK * NQK + 1) / 2 * 2;        // dense block per (i, j), padded even
-    static constexpr int DQS = NCOMBO * DB + 2;               // q stride (+2: spread smem banks)
+    // q stride: dense blocks (+2: spread smem banks); FS: the compact (i, j, c, c2) list, odd
+    // stride so that the 9 (q0, q1) rows a stage-1 warp reads fall in distinct bank pairs
+    static constexpr int DQS = FSC ? ((L::EIJ.n + 1) | 1) : NCOMBO * DB + 2;
+    static constexpr int ZSLOT = L::EIJ.n;                   // FS: zero coefficient slot per point
     using State = typename PH::template State<3>;
     static constexpr int STD = (sizeof(State) + 7) / 8;      // doubles per state
     // symmetric element Jacobian (hyperelastic tangent, major symmetry): contract blocks I <= J
@@ -104,7 +216,23 @@ struct F3 {
     // (A/B: slower at 2 CTAs/SM, and it does not fit three)
     static constexpr bool PBS = IGA_PBS && M == 4;
     static constexpr int O_PB = O_RS + NEN * M;              // [NQ][NQK][NEN]
-    static constexpr size_t SMEM = (size_t)(O_PB + (PBS ? NQ * NQK * NEN : 0)) * sizeof(double);
+    // FS stage-1 output X1[J][G][q0 q1][a2 b2] of one test component I; J stride = 4 mod 16
+    // doubles so that a stage-2 warp (lanes J fastest, then a2 b2) reads distinct bank pairs
+    static constexpr int X1G = NQ1 * NQ1 * NP1 * NP1;
+    static constexpr int xjs() {
+        if constexpr (FSC) {
+            const int n = FsMeta<L>::NG * X1G;
+            return n + ((4 - n) % 16 + 16) % 16;
+        } else return 0;
+    }
+    static constexpr int XJS = xjs();
+    static constexpr int O_X1 = O_PB + (PBS ? NQ * NQK * NEN : 0);
+    static constexpr int ncmb() {
+        if constexpr (FSC) return FsMeta<L>::NCMB;
+        else return 1;
+    }
+    using FT = FsTab<FSC ? M * M : 1, ncmb()>;
+    static constexpr size_t SMEM = (size_t)(O_X1 + M * XJS) * sizeof(double);
     // residual only: no coefficient blocks -- row starts (unused) right after the overlay
     static constexpr int O_RS_RES = O_ND + NEN;
     static constexpr size_t SMEM_RES = (size_t)(O_RS_RES + NEN * M) * sizeof(double);
@@ -283,12 +411,156 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
     }
 }
 
+// FS stage 1 (axis 2) for test component I and trial component J = warp: lane = (q0 q1, a2),
+// 3 accumulators (b2) per group G; the coefficient of combo c of block (I, J) sits at offset
+// ft.off[I M + J][c] of every point's compact row (the zero slot if it is structurally zero).
+//   X1[J][G][q0 q1][a2 b2] = sum_(tau, kap in G) sum_q2 T2[q2][o2 tau][a2] T2[q2][o2 kap][b2] D_IJ(q)
+// Every loaded coefficient feeds one DMUL and three DFMAs.
+template <class F, int P>
+__device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict__ sD, const double *__restrict__ sTab,
+                                          double *__restrict__ sX1, const UniTab<P> &ut, const typename F::FT &ft,
+                                          int lane) {
+    using FM = FsMeta<typename F::L>;
+    constexpr int NQ1 = F::NQ1, NP1 = F::NP1, NQQ = NQ1 * NQ1, NAB = NP1 * NP1;
+    if (lane >= NQQ * NP1) return;
+    const int q01 = lane / NP1, a2 = lane - q01 * NP1;
+    double t2a[NQ1][3];                                  // test values on axis 2 (unused orders are dead)
+#pragma unroll
+    for (int q2 = 0; q2 < NQ1; q2++)
+#pragma unroll
+        for (int o = 0; o < 3; o++) t2a[q2][o] = sTab[((2 * NQ1 + q2) * 3 + o) * NP1 + a2];
+    const double *Dq = sD + q01 * NQ1 * F::DQS;
+    const unsigned char *off = ft.off[I * F::M + J];
+    double *dst = sX1 + J * F::XJS + q01 * NAB + a2 * NP1;
+    static_for<FM::NG>([&](auto GG) {
+        constexpr int g = decltype(GG)::value;
+        double acc[NP1];
+#pragma unroll
+        for (int b2 = 0; b2 < NP1; b2++) acc[b2] = 0.0;
+        static_for<FM::ncombo(g)>([&](auto CC) {
+            constexpr int c = decltype(CC)::value;
+            constexpr int ta = FM::combo(g, c, true), kb = FM::combo(g, c, false);
+            constexpr int ot = FM::TT.t[ta].o2, ok = FM::QT.t[kb].o2;
+            const int e = off[FM::cbase(g) + c];
+#pragma unroll
+            for (int q2 = 0; q2 < NQ1; q2++) {
+                const double x = Dq[q2 * F::DQS + e] * t2a[q2][ot];
+#pragma unroll
+                for (int b2 = 0; b2 < NP1; b2++) acc[b2] += x * ut.t[2][q2][ok][b2];
+            }
+        });
+#pragma unroll
+        for (int b2 = 0; b2 < NP1; b2++) dst[g * NQQ * NAB + b2] = acc[b2];
+    });
+}
+
+// FS stages 2 + 3 (axes 1 and 0) for test component I: task (J, a2 b2, a1), J fastest (4
+// consecutive lanes fill one 32-byte sector of a CSR row), K[a0][b0][b1] in registers:
+//   z_p[b1]    = sum_(G in p) sum_q1 T1[q1][o1 ta][a1] T1[q1][o1 ka][b1] X1_G[q0 q1][a2 b2]
+//   y_oa[b0 b1] = sum_(p: test o0 = oa) T0[q0][o0 trial p][b0] z_p[b1]
+//   K[a0 b0 b1] += T0[q0][oa][a0] y_oa[b0 b1]          (per q0)
+// then each value is added into its CSR position with red.global.add.f64.
+template <class F, int P>
+__device__ __forceinline__ void fs_stage23(int I, int tid, const double *__restrict__ sX1, const double *__restrict__ sTab,
+                                           const int *sPosE, const int *sW, const long long *sRS, double *__restrict__ val,
+                                           const UniTab<P> &ut, int dbg) {
+    using FM = FsMeta<typename F::L>;
+    constexpr int M = F::M, NQ1 = F::NQ1, NP1 = F::NP1, NQQ = NQ1 * NQ1, NAB = NP1 * NP1, NKA = FM::NKA;
+#pragma unroll 1
+    for (int task = tid; task < M * NAB * NP1; task += F::NT) {
+        const int J = task % M, r = task / M, ab2 = r % NAB, a1 = r / NAB;
+        const int a2 = ab2 / NP1, b2 = ab2 - a2 * NP1;
+        double t1a[NQ1][3];                              // test values on axis 1 (unused orders are dead)
+#pragma unroll
+        for (int q1 = 0; q1 < NQ1; q1++)
+#pragma unroll
+            for (int o = 0; o < 3; o++) t1a[q1][o] = sTab[((1 * NQ1 + q1) * 3 + o) * NP1 + a1];
+        double K[NP1][NP1][NP1];
+#pragma unroll
+        for (int x = 0; x < NP1 * NP1 * NP1; x++) (&K[0][0][0])[x] = 0.0;
+        const double *X = sX1 + J * F::XJS + ab2;
+        static_for<NQ1>([&](auto Q0) {
+            constexpr int q0 = decltype(Q0)::value;
+            static_for<3>([&](auto OA) {                   // test derivative order on axis 0
+                constexpr int oa = decltype(OA)::value;
+                constexpr bool used = [] { for (int p = 0; p < FM::NO0P; p++) if (FM::PO.a[p] == oa) return true; return false; }();
+                if constexpr (used) {
+                    double y[NP1][NP1];
+#pragma unroll
+                    for (int x = 0; x < NP1 * NP1; x++) (&y[0][0])[x] = 0.0;
+                    static_for<FM::NO0P>([&](auto PP) {
+                        constexpr int pp = decltype(PP)::value;
+                        if constexpr (FM::PO.a[pp] == oa) {
+                            double z[NP1];
+#pragma unroll
+                            for (int b1 = 0; b1 < NP1; b1++) z[b1] = 0.0;
+                            static_for<FM::NG>([&](auto GG) {
+                                constexpr int g = decltype(GG)::value;
+                                if constexpr (FM::in_o0p(g, pp)) {
+                                    constexpr int oa1 = FM::TA.o1[g / NKA], ob1 = FM::KA.o1[g % NKA];
+#pragma unroll
+                                    for (int q1 = 0; q1 < NQ1; q1++) {
+                                        const double x = X[(g * NQQ + q0 * NQ1 + q1) * NAB] * t1a[q1][oa1];
+#pragma unroll
+                                        for (int b1 = 0; b1 < NP1; b1++) z[b1] += x * ut.t[1][q1][ob1][b1];
+                                    }
+                                }
+                            });
+                            constexpr int ob0 = FM::PO.b[pp];
+#pragma unroll
+                            for (int b0 = 0; b0 < NP1; b0++)
+#pragma unroll
+                                for (int b1 = 0; b1 < NP1; b1++) y[b0][b1] += ut.t[0][q0][ob0][b0] * z[b1];
+                        }
+                    });
+#pragma unroll
+                    for (int a0 = 0; a0 < NP1; a0++)
+#pragma unroll
+                        for (int x = 0; x < NP1 * NP1; x++) (&K[a0][0][0])[x] += ut.t[0][q0][oa][a0] * (&y[0][0])[x];
+                }
+            });
+        });
+        if (!(dbg & 2)) {
+            // CSR position of (A, B) in row (A, I): ((pos0 W1 + pos1) W2 + pos2) nodes
+            const int W1a = sW[NP1 + a1], W2a = sW[2 * NP1 + a2];
+            const int P2ab = sPosE[2 * NP1 * NP1 + a2 * NP1 + b2];
+            int P1b[NP1];
+#pragma unroll
+            for (int b1 = 0; b1 < NP1; b1++) P1b[b1] = sPosE[NP1 * NP1 + a1 * NP1 + b1];
+#pragma unroll
+            for (int a0 = 0; a0 < NP1; a0++) {
+                const long long rs = sRS[((a0 * NP1 + a1) * NP1 + a2) * M + I] + J;
+#pragma unroll
+                for (int b0 = 0; b0 < NP1; b0++) {
+                    const int p0 = sPosE[a0 * NP1 + b0];
+#pragma unroll
+                    for (int b1 = 0; b1 < NP1; b1++) {
+                        const int co = (p0 * W1a + P1b[b1]) * W2a + P2ab;
+                        atomicAdd(val + rs + (long long)co * M, K[a0][b0][b1]);
+                    }
+                }
+            }
+        } else {
+            double sum = 0.0;
+#pragma unroll
+            for (int x = 0; x < NP1 * NP1 * NP1; x++) sum += (&K[0][0][0])[x];
+            if (sum == 1.2345e300) val[0] = sum;
+        }
+    }
+}
+
+#ifndef IGA_FS
+#define IGA_FS 1    // fully sum-factorised contraction for the uniform-table VMS Jacobian (0: column form)
+#endif
+template <int P, class PH, bool JAC, bool UNI>
+using F3K = F3<P, PH, JAC && UNI && FsOk<PH>::value && IGA_FS>;
+
 template <int P, class PH, bool JAC, bool UNI>
 __global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3<P, PH>::MINB : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
-          int dbg, int bw) {
-    using F = F3<P, PH>;
+          const __grid_constant__ typename F3K<P, PH, JAC, UNI>::FT ft, int dbg, int bw) {
+    using F = F3K<P, PH, JAC, UNI>;
     constexpr int NTH = F::NT, NWP = F::NWARP;
     using L = typename F::L;
     using KS = typename F::KS;
@@ -622,6 +894,9 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 
         // ---- 4. Jacobian coefficients: warp-uniform trial column (k2 = qk(kq), j), lane = q ----
         if constexpr (JAC) {
+            if constexpr (F::FSC) {
+                if (tid < NQ) sD[tid * F::DQS + F::ZSLOT] = 0.0;   // FS zero slot (the region overlays phase 2-3 data)
+            }
             // warp w owns the columns kj = w, w + NWARP, ...: the state stays in registers
             if (lane < NQ && !(dbg & 16)) {
                 const int q = lane;
@@ -640,6 +915,21 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                         if (warp == decltype(KJ)::value % NWP) {
                             double col[NKS * M];
                             PH::template dcol<3>(st, k2, j, a, b, col);
+                            if constexpr (F::FSC) {
+                                // compact list: only the structurally nonzero (i, j, t, k) entries
+                                static_for<M>([&](auto II) {
+                                    constexpr int i = decltype(II)::value;
+                                    static_for<NTK>([&](auto TK) {
+                                        constexpr int t = decltype(TK)::value;
+                                        constexpr int e = FsMeta<L>::eij(i, j, L::tk(t), k2);
+                                        if constexpr (e >= 0) {
+                                            const double v = col[L::tk(t) * M + i] * dV;
+                                            chk += v;
+                                            sD[q * F::DQS + e] = v;
+                                        }
+                                    });
+                                });
+                            } else {
 #pragma unroll
                             for (int i = 0; i < M; i++) {
                                 // block layout [trial kind k][test kind t]: this column's NTK entries
@@ -660,6 +950,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                                     for (int t = 0; t < NTK; t++) dst[t] = v[t];
                                 }
                             }
+                            }
                         }
                     });
                     if (!isfinite(chk)) errbits |= 2;
@@ -667,6 +958,20 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             }
             __syncthreads();
 
+            if constexpr (F::FSC) {
+                // ---- 5 (FS). fully sum-factorised contraction, one test component I at a time:
+                //      stage 1 per (I, J = warp) compiled with its exact coefficient structure ----
+                static_assert(F::NWARP == M, "FS stage 1 maps warp = trial component J");
+                using FM = FsMeta<L>;
+                double *sX1 = sm + F::O_X1;
+#pragma unroll 1
+                for (int I = 0; I < M; I++) {
+                    fs_stage1<F, P>(I, warp, sD, sTab, sX1, ut, ft, lane);
+                    __syncthreads();
+                    fs_stage23<F, P>(I, tid, sX1, sTab, sPosE, sW, sRS, val, ut, dbg);
+                    __syncthreads();
+                }
+            } else
             // ---- 5. test-side sum factorisation + coalesced emission ----
             // Non-symmetric forms: the NEN*M*M column tasks (I, B, J) (J fastest: 4 consecutive
             // lanes write one 32-byte sector of a CSR row) are dealt round-robin over all NT
@@ -806,7 +1111,8 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
 template <int P, class PH, bool UNI>
 static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, double b, const double *U,
                               const double *Ud, double *val, double *F, cudaStream_t st, int nsm) {
-    using FF = F3<P, PH>;
+    using FF = F3K<P, PH, true, UNI>;
+    using FR = F3K<P, PH, false, UNI>;
     Prm prm;
     for (int i = 0; i < 8; i++) prm.p[i] = phys->p[i];
     UniTab<P> ut{};
@@ -816,9 +1122,24 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
             for (int q = 0; q <= P; q++) ut.qw[d][q] = s->qw0[d][q];
             ut.hp[d] = s->hp0[d];
         }
+    typename FF::FT ft{};
+    typename FR::FT ftr{};
+    if constexpr (FF::FSC) {
+        using L = typename FF::L;
+        using FM = FsMeta<L>;
+        static_assert(FF::DQS <= 255, "compact offsets must fit a byte");
+        for (int I = 0; I < FF::M; I++)
+            for (int J = 0; J < FF::M; J++)
+                for (int g = 0; g < FM::NG; g++)
+                    for (int c = 0; c < FM::ncombo(g); c++) {
+                        const int e = FM::eij(I, J, L::tk(FM::TT.t[FM::combo(g, c, true)].k),
+                                              L::qk(FM::QT.t[FM::combo(g, c, false)].k));
+                        ft.off[I * FF::M + J][FM::cbase(g) + c] = (unsigned char)(e < 0 ? FF::ZSLOT : e);
+                    }
+    }
     const bool jac = val != nullptr;
     const bool jac_ = val != nullptr;
-    const size_t smem = jac_ ? FF::SMEM : FF::SMEM_RES;
+    const size_t smem = jac_ ? FF::SMEM : FR::SMEM_RES;
     {   // per-device attribute: set on the current device before every launch
         cudaError_t ce = jac ? cudaFuncSetAttribute(k_fused3d<P, PH, true, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
                              : cudaFuncSetAttribute(k_fused3d<P, PH, false, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -848,8 +1169,8 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
             cudaError_t me = cudaMemsetAsync(s->dev.wq, 0, sizeof(unsigned long long), st);
             if (me != cudaSuccess) { set_error(std::string("fused3d counter: ") + cudaGetErrorString(me)); return IGA_ERR_CUDA; }
         }
-        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
-        else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, s->dbg, bw);
+        if (jac) k_fused3d<P, PH, true, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, ft, s->dbg, bw);
+        else k_fused3d<P, PH, false, UNI><<<grid, FF::NT, smem, st>>>(s->dev, prm, a, b, U, Ud, val, F, nel, ut, ftr, s->dbg, bw);
         launches++;
     }
     s->last_launches = launches;
