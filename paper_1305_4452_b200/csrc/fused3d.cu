@@ -149,13 +149,15 @@ struct FsMeta {
 template <int NIJ, int NCMB>
 struct alignas(4) FsTab { unsigned char off[NIJ][(NCMB + 3) / 4 * 4]; };   // rows padded to whole words
 
-// FS is used for the uniform-table kernels whose CTA has one warp per trial component (VMS: m = 4,
-// 128 threads; Neo-Hooke: m = 3, 96 threads; Cahn-Hilliard: m = 1, 32 threads)
+// FS is used for the uniform-table kernels whose CTA has one warp per trial component.  On for
+// VMS (m = 4, 128 threads).  Neo-Hooke (m = 3) has uniform tables only on periodic meshes (config
+// 4 is open: never reached, untested); 3D Cahn-Hilliard (m = 1): A/B config 8 149.9 vs 140.8 ms,
+// the column form is kept.
 #ifndef IGA_FS_NH
-#define IGA_FS_NH 1
+#define IGA_FS_NH 0
 #endif
 #ifndef IGA_FS_CH
-#define IGA_FS_CH 1
+#define IGA_FS_CH 0
 #endif
 template <class PH> struct FsOk {
     static constexpr bool value = PH::M == 4 || (PH::M == 3 && IGA_FS_NH) || (PH::M == 1 && IGA_FS_CH);
