@@ -61,12 +61,6 @@ template <class PH> struct PhysJState<PH, std::void_t<decltype(PH::JSTATE)>> { s
 // where a group G = (test class ta, trial class ka) collects the terms by their (axis-0, axis-1)
 // derivative orders.  Every loaded coefficient then feeds 3-9 FMAs held in registers (the
 // test-side column form reads the whole D block once per column and point: 1 FMA per load).
-#ifndef IGA_FS_PASS
-#define IGA_FS_PASS 0   // FS stage buffer split into passes by the test axis-0 order (fits 3 CTAs/SM; A/B 174.2 ms at 3 CTAs, 170.7 at 2 vs 160.9 single pass: K live across stage 1 spills at 168 registers)
-#endif
-#ifndef IGA_FS_MINB
-#define IGA_FS_MINB (IGA_FS_PASS ? 3 : 2)
-#endif
 template <class L>
 struct FsMeta {
     using KS = typename L::KS;
@@ -125,26 +119,6 @@ struct FsMeta {
     }
     static constexpr int MAXC = [] { int m = 1; for (int g = 0; g < NG; g++) m = ncombo(g) > m ? ncombo(g) : m; return m; }();
     static constexpr int cbase(int g) { int n = 0; for (int x = 0; x < g; x++) n += ncombo(x); return n; }
-    // stage-1 group sets (IGA_FS_S1): set w = groups of warp w for every trial component J,
-    // greedy by combo count (largest first onto the lightest set)
-    struct GSet { int of[64]; };
-    static constexpr GSet make_gset(int NS) {
-        GSet S{};
-        int load[8] = {};
-        bool done[64] = {};
-        for (int k = 0; k < NG; k++) {
-            int best = -1;
-            for (int g = 0; g < NG; g++)
-                if (!done[g] && (best < 0 || ncombo(g) > ncombo(best))) best = g;
-            int w = 0;
-            for (int x = 1; x < NS; x++) if (load[x] < load[w]) w = x;
-            S.of[best] = w;
-            load[w] += ncombo(best);
-            done[best] = true;
-        }
-        return S;
-    }
-    static constexpr int gset_of(int g, int ns) { return make_gset(ns).of[g]; }
     static constexpr int NCMB = cbase(NG);              // all (test term, trial term) combos
     // axis-0 order pairs (o0 test, o0 trial): stage 3 sums the groups of one pair first
     struct O0P { int n; int a[16], b[16]; };
@@ -159,31 +133,6 @@ struct FsMeta {
         return P;
     }
     static constexpr O0P PO = make_o0p();
-    // passes: X1 holds the groups of one test axis-0 derivative order at a time (IGA_FS_PASS),
-    // which shrinks the stage buffer so that three CTAs fit per SM
-    struct Pass { int n; int oa[4]; };
-    static constexpr Pass make_pass() {
-        Pass P{};
-        for (int t = 0; t < NTA; t++) {
-            bool seen = false;
-            for (int p = 0; p < P.n; p++) seen = seen || P.oa[p] == TA.o0[t];
-            if (!seen) P.oa[P.n++] = TA.o0[t];
-        }
-        return P;
-    }
-    static constexpr Pass PS_ = make_pass();
-    static constexpr int NPASS = IGA_FS_PASS ? PS_.n : 1;
-    static constexpr int pass_of(int g) {
-        if (!IGA_FS_PASS) return 0;
-        for (int p = 0; p < PS_.n; p++) if (PS_.oa[p] == TA.o0[g / NKA]) return p;
-        return -1;
-    }
-    static constexpr int slot(int g) { int n = 0; for (int x = 0; x < g; x++) n += pass_of(x) == pass_of(g); return n; }
-    static constexpr int NGP = [] {
-        int m = 0;
-        for (int p = 0; p < NPASS; p++) { int n = 0; for (int g = 0; g < NG; g++) n += pass_of(g) == p; m = n > m ? n : m; }
-        return m;
-    }();
     static constexpr int NO0P = PO.n;
     static constexpr bool in_o0p(int g, int p) { return TA.o0[g / NKA] == PO.a[p] && KA.o0[g % NKA] == PO.b[p]; }
     // compact coefficient index of (i, j, contraction kind c, c2) in the (i, j, c, c2)-ordered list
@@ -203,7 +152,8 @@ struct alignas(4) FsTab { unsigned char off[NIJ][(NCMB + 3) / 4 * 4]; };   // ro
 // FS is used for the uniform-table kernels whose CTA has one warp per trial component.  On for
 // VMS (m = 4, 128 threads).  Neo-Hooke (m = 3) has uniform tables only on periodic meshes (config
 // 4 is open: never reached, untested); 3D Cahn-Hilliard (m = 1): A/B config 8 149.9 vs 140.8 ms,
-// the column form is kept.
+// the column form is kept.  Also tried: X1 in two passes for three CTAs per SM, and
+// stage 1 over balanced group sets with the structural zeros skipped -- both slower.
 #ifndef IGA_FS_NH
 #define IGA_FS_NH 0
 #endif
@@ -239,7 +189,7 @@ struct F3 {
 #ifndef IGA_VMS_MINB
 #define IGA_VMS_MINB 2
 #endif
-    static constexpr int MINB = FSC ? IGA_FS_MINB : M == 1 ? 8 : M == 3 ? 3 : IGA_VMS_MINB;
+    static constexpr int MINB = M == 1 ? 8 : M == 3 ? 3 : IGA_VMS_MINB;
     // doubles of the per-point state that the Jacobian coefficients read (the leading members;
     // VMS keeps its residual coefficients rN, rG after them): only these go to shared memory
     static constexpr int STJ = PhysJState<PH>::value > 0 ? PhysJState<PH>::value : STD;
@@ -274,7 +224,7 @@ struct F3 {
     static constexpr int X1G = NQ1 * NQ1 * NP1 * NP1;
     static constexpr int xjs() {
         if constexpr (FSC) {
-            const int n = FsMeta<L>::NGP * X1G;
+            const int n = FsMeta<L>::NG * X1G;
             return n + ((4 - n) % 16 + 16) % 16;
         } else return 0;
     }
@@ -464,13 +414,12 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
     }
 }
 
-// FS stage 1 (axis 2), pass PS, for test component I and trial component J = warp: lane =
-// (q0 q1, a2), 3 accumulators (b2) per group G of the pass; the coefficient of combo c of block
-// (I, J) sits at offset ft.off[I M + J][c] of every point's compact row (the zero slot if it is
-// structurally zero).
-//   X1[J][slot G][q0 q1][a2 b2] = sum_(tau, kap in G) sum_q2 T2[q2][o2 tau][a2] T2[q2][o2 kap][b2] D_IJ(q)
+// FS stage 1 (axis 2) for test component I and trial component J = warp: lane = (q0 q1, a2),
+// 3 accumulators (b2) per group G; the coefficient of combo c of block (I, J) sits at offset
+// ft.off[I M + J][c] of every point's compact row (the zero slot if it is structurally zero).
+//   X1[J][G][q0 q1][a2 b2] = sum_(tau, kap in G) sum_q2 T2[q2][o2 tau][a2] T2[q2][o2 kap][b2] D_IJ(q)
 // Every loaded coefficient feeds one DMUL and three DFMAs.
-template <class F, int P, int PS>
+template <class F, int P>
 __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict__ sD, const double *__restrict__ sTab,
                                           double *__restrict__ sX1, const UniTab<P> &ut, const typename F::FT &ft,
                                           int lane) {
@@ -488,179 +437,118 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
     double *dst = sX1 + J * F::XJS + q01 * NAB + a2 * NP1;
     static_for<FM::NG>([&](auto GG) {
         constexpr int g = decltype(GG)::value;
-        if constexpr (FM::pass_of(g) == PS) {
-            double acc[NP1];
+        double acc[NP1];
 #pragma unroll
-            for (int b2 = 0; b2 < NP1; b2++) acc[b2] = 0.0;
-            static_for<FM::ncombo(g)>([&](auto CC) {
-                constexpr int c = decltype(CC)::value;
-                constexpr int ta = FM::combo(g, c, true), kb = FM::combo(g, c, false);
-                constexpr int ot = FM::TT.t[ta].o2, ok = FM::QT.t[kb].o2;
-                const int e = off[FM::cbase(g) + c];
+        for (int b2 = 0; b2 < NP1; b2++) acc[b2] = 0.0;
+        static_for<FM::ncombo(g)>([&](auto CC) {
+            constexpr int c = decltype(CC)::value;
+            constexpr int ta = FM::combo(g, c, true), kb = FM::combo(g, c, false);
+            constexpr int ot = FM::TT.t[ta].o2, ok = FM::QT.t[kb].o2;
+            const int e = off[FM::cbase(g) + c];
 #pragma unroll
-                for (int q2 = 0; q2 < NQ1; q2++) {
-                    const double x = Dq[q2 * F::DQS + e] * t2a[q2][ot];
+            for (int q2 = 0; q2 < NQ1; q2++) {
+                const double x = Dq[q2 * F::DQS + e] * t2a[q2][ot];
 #pragma unroll
-                    for (int b2 = 0; b2 < NP1; b2++) acc[b2] += x * ut.t[2][q2][ok][b2];
-                }
-            });
+                for (int b2 = 0; b2 < NP1; b2++) acc[b2] += x * ut.t[2][q2][ok][b2];
+            }
+        });
 #pragma unroll
-            for (int b2 = 0; b2 < NP1; b2++) dst[FM::slot(g) * NQQ * NAB + b2] = acc[b2];
-        }
+        for (int b2 = 0; b2 < NP1; b2++) dst[g * NQQ * NAB + b2] = acc[b2];
     });
 }
 
-#ifndef IGA_FS_S1
-#define IGA_FS_S1 1   // stage 1: warp = balanced group set for all J, structural zeros skipped (0: warp = J, dense)
-#endif
-// stage 1, IGA_FS_S1 = 1: warp W takes the groups of set W for every J; a structurally zero
-// combo of block (I, J) is skipped (warp-uniform branch), so the work per warp is the sparse
-// count of its groups, balanced across the warps
-template <class F, int P, int PS, int W>
-__device__ __forceinline__ void fs_stage1_sets(int I, const double *__restrict__ sD, const double *__restrict__ sTab,
-                                               double *__restrict__ sX1, const UniTab<P> &ut, const typename F::FT &ft,
-                                               int lane) {
-    using FM = FsMeta<typename F::L>;
-    constexpr int NQ1 = F::NQ1, NP1 = F::NP1, NQQ = NQ1 * NQ1, NAB = NP1 * NP1;
-    if (lane >= NQQ * NP1) return;
-    const int q01 = lane / NP1, a2 = lane - q01 * NP1;
-    double t2a[NQ1][3];
-#pragma unroll
-    for (int q2 = 0; q2 < NQ1; q2++)
-#pragma unroll
-        for (int o = 0; o < 3; o++) t2a[q2][o] = sTab[((2 * NQ1 + q2) * 3 + o) * NP1 + a2];
-    const double *Dq = sD + q01 * NQ1 * F::DQS;
-#pragma unroll 1
-    for (int J = 0; J < F::M; J++) {
-        const unsigned char *off = ft.off[I * F::M + J];
-        double *dst = sX1 + J * F::XJS + q01 * NAB + a2 * NP1;
-        static_for<FM::NG>([&](auto GG) {
-            constexpr int g = decltype(GG)::value;
-            if constexpr (FM::pass_of(g) == PS && FM::gset_of(g, F::NWARP) == W) {
-                double acc[NP1];
-#pragma unroll
-                for (int b2 = 0; b2 < NP1; b2++) acc[b2] = 0.0;
-                static_for<FM::ncombo(g)>([&](auto CC) {
-                    constexpr int c = decltype(CC)::value;
-                    constexpr int ta = FM::combo(g, c, true), kb = FM::combo(g, c, false);
-                    constexpr int ot = FM::TT.t[ta].o2, ok = FM::QT.t[kb].o2;
-                    const int e = off[FM::cbase(g) + c];
-                    if (e != F::ZSLOT) {
-#pragma unroll
-                        for (int q2 = 0; q2 < NQ1; q2++) {
-                            const double x = Dq[q2 * F::DQS + e] * t2a[q2][ot];
-#pragma unroll
-                            for (int b2 = 0; b2 < NP1; b2++) acc[b2] += x * ut.t[2][q2][ok][b2];
-                        }
-                    }
-                });
-#pragma unroll
-                for (int b2 = 0; b2 < NP1; b2++) dst[FM::slot(g) * NQQ * NAB + b2] = acc[b2];
-            }
-        });
-    }
-}
-
-// FS stages 2 + 3 (axes 1 and 0), pass PS, for test component I: task (J, a2 b2, a1), J fastest
-// (4 consecutive lanes fill one 32-byte sector of a CSR row), K[a0][b0][b1] in registers across
-// the passes:
+// FS stages 2 + 3 (axes 1 and 0) for test component I: task (J, a2 b2, a1), J fastest (4
+// consecutive lanes fill one 32-byte sector of a CSR row), K[a0][b0][b1] in registers:
 //   z_p[b1]    = sum_(G in p) sum_q1 T1[q1][o1 ta][a1] T1[q1][o1 ka][b1] X1_G[q0 q1][a2 b2]
 //   y_oa[b0 b1] = sum_(p: test o0 = oa) T0[q0][o0 trial p][b0] z_p[b1]
 //   K[a0 b0 b1] += T0[q0][oa][a0] y_oa[b0 b1]          (per q0)
-template <class F, int P, int PS>
-__device__ __forceinline__ void fs_stage23(double (&K)[F::NP1][F::NP1][F::NP1], int J, int ab2, int a1,
-                                           const double *__restrict__ sX1, const double *__restrict__ sTab,
-                                           const UniTab<P> &ut) {
+// then each value is added into its CSR position with red.global.add.f64.
+template <class F, int P>
+__device__ __forceinline__ void fs_stage23(int I, int tid, const double *__restrict__ sX1, const double *__restrict__ sTab,
+                                           const int *sPosE, const int *sW, const long long *sRS, double *__restrict__ val,
+                                           const UniTab<P> &ut, int dbg) {
     using FM = FsMeta<typename F::L>;
-    constexpr int NQ1 = F::NQ1, NP1 = F::NP1, NQQ = NQ1 * NQ1, NAB = NP1 * NP1, NKA = FM::NKA;
-    double t1a[NQ1][3];                                  // test values on axis 1 (unused orders are dead)
+    constexpr int M = F::M, NQ1 = F::NQ1, NP1 = F::NP1, NQQ = NQ1 * NQ1, NAB = NP1 * NP1, NKA = FM::NKA;
+#pragma unroll 1
+    for (int task = tid; task < M * NAB * NP1; task += F::NT) {
+        const int J = task % M, r = task / M, ab2 = r % NAB, a1 = r / NAB;
+        const int a2 = ab2 / NP1, b2 = ab2 - a2 * NP1;
+        double t1a[NQ1][3];                              // test values on axis 1 (unused orders are dead)
 #pragma unroll
-    for (int q1 = 0; q1 < NQ1; q1++)
+        for (int q1 = 0; q1 < NQ1; q1++)
 #pragma unroll
-        for (int o = 0; o < 3; o++) t1a[q1][o] = sTab[((1 * NQ1 + q1) * 3 + o) * NP1 + a1];
-    const double *X = sX1 + J * F::XJS + ab2;
-    static_for<NQ1>([&](auto Q0) {
-        constexpr int q0 = decltype(Q0)::value;
-        static_for<3>([&](auto OA) {                       // test derivative order on axis 0
-            constexpr int oa = decltype(OA)::value;
-            constexpr bool used = [] {
-                for (int p = 0; p < FM::NO0P; p++)
-                    if (FM::PO.a[p] == oa) {
-                        for (int g = 0; g < FM::NG; g++) if (FM::in_o0p(g, p) && FM::pass_of(g) == PS) return true;
-                    }
-                return false;
-            }();
-            if constexpr (used) {
-                double y[NP1][NP1];
+            for (int o = 0; o < 3; o++) t1a[q1][o] = sTab[((1 * NQ1 + q1) * 3 + o) * NP1 + a1];
+        double K[NP1][NP1][NP1];
 #pragma unroll
-                for (int x = 0; x < NP1 * NP1; x++) (&y[0][0])[x] = 0.0;
-                static_for<FM::NO0P>([&](auto PP) {
-                    constexpr int pp = decltype(PP)::value;
-                    if constexpr (FM::PO.a[pp] == oa) {
-                        double z[NP1];
+        for (int x = 0; x < NP1 * NP1 * NP1; x++) (&K[0][0][0])[x] = 0.0;
+        const double *X = sX1 + J * F::XJS + ab2;
+        static_for<NQ1>([&](auto Q0) {
+            constexpr int q0 = decltype(Q0)::value;
+            static_for<3>([&](auto OA) {                   // test derivative order on axis 0
+                constexpr int oa = decltype(OA)::value;
+                constexpr bool used = [] { for (int p = 0; p < FM::NO0P; p++) if (FM::PO.a[p] == oa) return true; return false; }();
+                if constexpr (used) {
+                    double y[NP1][NP1];
 #pragma unroll
-                        for (int b1 = 0; b1 < NP1; b1++) z[b1] = 0.0;
-                        static_for<FM::NG>([&](auto GG) {
-                            constexpr int g = decltype(GG)::value;
-                            if constexpr (FM::in_o0p(g, pp) && FM::pass_of(g) == PS) {
-                                constexpr int oa1 = FM::TA.o1[g / NKA], ob1 = FM::KA.o1[g % NKA];
+                    for (int x = 0; x < NP1 * NP1; x++) (&y[0][0])[x] = 0.0;
+                    static_for<FM::NO0P>([&](auto PP) {
+                        constexpr int pp = decltype(PP)::value;
+                        if constexpr (FM::PO.a[pp] == oa) {
+                            double z[NP1];
 #pragma unroll
-                                for (int q1 = 0; q1 < NQ1; q1++) {
-                                    const double x = X[(FM::slot(g) * NQQ + q0 * NQ1 + q1) * NAB] * t1a[q1][oa1];
+                            for (int b1 = 0; b1 < NP1; b1++) z[b1] = 0.0;
+                            static_for<FM::NG>([&](auto GG) {
+                                constexpr int g = decltype(GG)::value;
+                                if constexpr (FM::in_o0p(g, pp)) {
+                                    constexpr int oa1 = FM::TA.o1[g / NKA], ob1 = FM::KA.o1[g % NKA];
 #pragma unroll
-                                    for (int b1 = 0; b1 < NP1; b1++) z[b1] += x * ut.t[1][q1][ob1][b1];
+                                    for (int q1 = 0; q1 < NQ1; q1++) {
+                                        const double x = X[(g * NQQ + q0 * NQ1 + q1) * NAB] * t1a[q1][oa1];
+#pragma unroll
+                                        for (int b1 = 0; b1 < NP1; b1++) z[b1] += x * ut.t[1][q1][ob1][b1];
+                                    }
                                 }
-                            }
-                        });
-                        constexpr int ob0 = FM::PO.b[pp];
+                            });
+                            constexpr int ob0 = FM::PO.b[pp];
 #pragma unroll
-                        for (int b0 = 0; b0 < NP1; b0++)
+                            for (int b0 = 0; b0 < NP1; b0++)
 #pragma unroll
-                            for (int b1 = 0; b1 < NP1; b1++) y[b0][b1] += ut.t[0][q0][ob0][b0] * z[b1];
-                    }
-                });
+                                for (int b1 = 0; b1 < NP1; b1++) y[b0][b1] += ut.t[0][q0][ob0][b0] * z[b1];
+                        }
+                    });
 #pragma unroll
-                for (int a0 = 0; a0 < NP1; a0++)
+                    for (int a0 = 0; a0 < NP1; a0++)
 #pragma unroll
-                    for (int x = 0; x < NP1 * NP1; x++) (&K[a0][0][0])[x] += ut.t[0][q0][oa][a0] * (&y[0][0])[x];
-            }
+                        for (int x = 0; x < NP1 * NP1; x++) (&K[a0][0][0])[x] += ut.t[0][q0][oa][a0] * (&y[0][0])[x];
+                }
+            });
         });
-    });
-}
-
-// FS scatter of task (J, a2 b2, a1) of test component I: each K value is added into its CSR
-// position with red.global.add.f64 (row (A, I), column node B, component J)
-template <class F>
-__device__ __forceinline__ void fs_scatter(const double (&K)[F::NP1][F::NP1][F::NP1], int I, int J, int ab2, int a1,
-                                           const int *sPosE, const int *sW, const long long *sRS,
-                                           double *__restrict__ val, int dbg) {
-    constexpr int M = F::M, NP1 = F::NP1;
-    const int a2 = ab2 / NP1, b2 = ab2 - a2 * NP1;
-    if (!(dbg & 2)) {
-        // CSR position of (A, B) in row (A, I): ((pos0 W1 + pos1) W2 + pos2) nodes
-        const int W1a = sW[NP1 + a1], W2a = sW[2 * NP1 + a2];
-        const int P2ab = sPosE[2 * NP1 * NP1 + a2 * NP1 + b2];
-        int P1b[NP1];
+        if (!(dbg & 2)) {
+            // CSR position of (A, B) in row (A, I): ((pos0 W1 + pos1) W2 + pos2) nodes
+            const int W1a = sW[NP1 + a1], W2a = sW[2 * NP1 + a2];
+            const int P2ab = sPosE[2 * NP1 * NP1 + a2 * NP1 + b2];
+            int P1b[NP1];
 #pragma unroll
-        for (int b1 = 0; b1 < NP1; b1++) P1b[b1] = sPosE[NP1 * NP1 + a1 * NP1 + b1];
+            for (int b1 = 0; b1 < NP1; b1++) P1b[b1] = sPosE[NP1 * NP1 + a1 * NP1 + b1];
 #pragma unroll
-        for (int a0 = 0; a0 < NP1; a0++) {
-            const long long rs = sRS[((a0 * NP1 + a1) * NP1 + a2) * M + I] + J;
+            for (int a0 = 0; a0 < NP1; a0++) {
+                const long long rs = sRS[((a0 * NP1 + a1) * NP1 + a2) * M + I] + J;
 #pragma unroll
-            for (int b0 = 0; b0 < NP1; b0++) {
-                const int p0 = sPosE[a0 * NP1 + b0];
+                for (int b0 = 0; b0 < NP1; b0++) {
+                    const int p0 = sPosE[a0 * NP1 + b0];
 #pragma unroll
-                for (int b1 = 0; b1 < NP1; b1++) {
-                    const int co = (p0 * W1a + P1b[b1]) * W2a + P2ab;
-                    atomicAdd(val + rs + (long long)co * M, K[a0][b0][b1]);
+                    for (int b1 = 0; b1 < NP1; b1++) {
+                        const int co = (p0 * W1a + P1b[b1]) * W2a + P2ab;
+                        atomicAdd(val + rs + (long long)co * M, K[a0][b0][b1]);
+                    }
                 }
             }
-        }
-    } else {
-        double sum = 0.0;
+        } else {
+            double sum = 0.0;
 #pragma unroll
-        for (int x = 0; x < NP1 * NP1 * NP1; x++) sum += (&K[0][0][0])[x];
-        if (sum == 1.2345e300) val[0] = sum;
+            for (int x = 0; x < NP1 * NP1 * NP1; x++) sum += (&K[0][0][0])[x];
+            if (sum == 1.2345e300) val[0] = sum;
+        }
     }
 }
 
@@ -671,7 +559,7 @@ template <int P, class PH, bool JAC, bool UNI>
 using F3K = F3<P, PH, JAC && UNI && FsOk<PH>::value && IGA_FS>;
 
 template <int P, class PH, bool JAC, bool UNI>
-__global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3K<P, PH, JAC, UNI>::MINB : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
+__global__ void __launch_bounds__(F3<P, PH>::NT, JAC ? F3<P, PH>::MINB : (F3<P, PH>::M == 1 ? 16 : 8))   // residual-only: A/B 4 -> 8 = -15 % / -12 % (configs 4 / 5); m = 1: 16 (-10 %)
 k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U, const double *__restrict__ Ud,
           double *__restrict__ val, double *__restrict__ Fout, long long nelem, const __grid_constant__ UniTab<P> ut,
           const __grid_constant__ typename F3K<P, PH, JAC, UNI>::FT ft, int dbg, int bw) {
@@ -1079,29 +967,12 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 static_assert(F::NWARP == M, "FS stage 1 maps warp = trial component J");
                 using FM = FsMeta<L>;
                 double *sX1 = sm + F::O_X1;
-                constexpr int NT23 = M * NP1 * NP1 * NP1;                 // stage 2+3 tasks (J, a2 b2, a1)
-                static_assert(NT23 <= NTH, "one stage 2+3 task per thread");
-                const bool act = tid < NT23;
-                const int tJ = tid % M, tab2 = (tid / M) % (NP1 * NP1), ta1 = tid / (M * NP1 * NP1);
 #pragma unroll 1
                 for (int I = 0; I < M; I++) {
-                    double K[NP1][NP1][NP1];
-#pragma unroll
-                    for (int x = 0; x < NP1 * NP1 * NP1; x++) (&K[0][0][0])[x] = 0.0;
-                    static_for<FsMeta<L>::NPASS>([&](auto PSS) {
-                        constexpr int PS = decltype(PSS)::value;
-                        if constexpr (IGA_FS_S1) {
-                            static_for<NWP>([&](auto WW) {
-                                if (warp == decltype(WW)::value) fs_stage1_sets<F, P, PS, decltype(WW)::value>(I, sD, sTab, sX1, ut, ft, lane);
-                            });
-                        } else {
-                            fs_stage1<F, P, PS>(I, warp, sD, sTab, sX1, ut, ft, lane);
-                        }
-                        __syncthreads();
-                        if (act) fs_stage23<F, P, PS>(K, tJ, tab2, ta1, sX1, sTab, ut);
-                        __syncthreads();
-                    });
-                    if (act) fs_scatter<F>(K, I, tJ, tab2, ta1, sPosE, sW, sRS, val, dbg);
+                    fs_stage1<F, P>(I, warp, sD, sTab, sX1, ut, ft, lane);
+                    __syncthreads();
+                    fs_stage23<F, P>(I, tid, sX1, sTab, sPosE, sW, sRS, val, ut, dbg);
+                    __syncthreads();
                 }
             } else
             // ---- 5. test-side sum factorisation + coalesced emission ----
