@@ -148,6 +148,10 @@ struct FsMeta {
 // all 16 blocks with the same work per warp
 template <int NIJ, int NCMB>
 struct alignas(4) FsTab { unsigned char off[NIJ][(NCMB + 3) / 4 * 4]; };   // rows padded to whole words
+#ifndef IGA_FS_TK
+#define IGA_FS_TK 1   // stage-1 offsets indexed by (test kind, trial kind): the Laplacian's three trial
+                      // terms share one coefficient, loaded once
+#endif
 
 // FS is used for the uniform-table kernels whose CTA has one warp per trial component.  On for
 // VMS (m = 4, 128 threads).  Neo-Hooke (m = 3) has uniform tables only on periodic meshes (config
@@ -231,7 +235,7 @@ struct F3 {
     static constexpr int XJS = xjs();
     static constexpr int O_X1 = O_PB + (PBS ? NQ * NQK * NEN : 0);
     static constexpr int ncmb() {
-        if constexpr (FSC) return FsMeta<L>::NCMB;
+        if constexpr (FSC) return IGA_FS_TK ? NTK * NQK : FsMeta<L>::NCMB;
         else return 1;
     }
     using FT = FsTab<FSC ? M * M : 1, ncmb()>;
@@ -435,6 +439,45 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
     const double *Dq = sD + q01 * NQ1 * F::DQS;
     const unsigned char *off = ft.off[I * F::M + J];
     double *dst = sX1 + J * F::XJS + q01 * NAB + a2 * NP1;
+#if IGA_FS_TK
+    // per test class: each (test term, trial kind) coefficient at the three q2 loaded once into
+    // registers (the Laplacian's three trial terms share it), then the class's groups
+    static_for<FM::NTA>([&](auto TAC) {
+        constexpr int ta = decltype(TAC)::value;
+        double dv[FM::TT.n][F::NQK][NQ1];
+        static_for<FM::TT.n>([&](auto TU) {
+            constexpr int tu = decltype(TU)::value;
+            if constexpr (FM::cls(FM::TA, FM::TT.t[tu].o0, FM::TT.t[tu].o1) == ta) {
+                static_for<F::NQK>([&](auto KQ) {
+                    constexpr int kq = decltype(KQ)::value;
+                    const int e = off[FM::TT.t[tu].k * F::NQK + kq];
+#pragma unroll
+                    for (int q2 = 0; q2 < NQ1; q2++) dv[tu][kq][q2] = Dq[q2 * F::DQS + e];
+                });
+            }
+        });
+        static_for<FM::NKA>([&](auto KAC) {
+            constexpr int g = ta * FM::NKA + decltype(KAC)::value;
+            double acc[NP1];
+#pragma unroll
+            for (int b2 = 0; b2 < NP1; b2++) acc[b2] = 0.0;
+            static_for<FM::ncombo(g)>([&](auto CC) {
+                constexpr int c = decltype(CC)::value;
+                constexpr int tu = FM::combo(g, c, true), kb = FM::combo(g, c, false);
+                constexpr int ot = FM::TT.t[tu].o2, ok = FM::QT.t[kb].o2, kq = FM::QT.t[kb].k;
+#pragma unroll
+                for (int q2 = 0; q2 < NQ1; q2++) {
+                    const double x = dv[tu][kq][q2] * t2a[q2][ot];
+#pragma unroll
+                    for (int b2 = 0; b2 < NP1; b2++) acc[b2] += x * ut.t[2][q2][ok][b2];
+                }
+            });
+#pragma unroll
+            for (int b2 = 0; b2 < NP1; b2++) dst[g * NQQ * NAB + b2] = acc[b2];
+        });
+    });
+    (void)FM::NCMB;
+#else
     static_for<FM::NG>([&](auto GG) {
         constexpr int g = decltype(GG)::value;
         double acc[NP1];
@@ -444,7 +487,7 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
             constexpr int c = decltype(CC)::value;
             constexpr int ta = FM::combo(g, c, true), kb = FM::combo(g, c, false);
             constexpr int ot = FM::TT.t[ta].o2, ok = FM::QT.t[kb].o2;
-            const int e = off[FM::cbase(g) + c];
+            const int e = off[IGA_FS_TK ? FM::TT.t[ta].k * F::NQK + FM::QT.t[kb].k : FM::cbase(g) + c];
 #pragma unroll
             for (int q2 = 0; q2 < NQ1; q2++) {
                 const double x = Dq[q2 * F::DQS + e] * t2a[q2][ot];
@@ -455,6 +498,7 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
 #pragma unroll
         for (int b2 = 0; b2 < NP1; b2++) dst[g * NQQ * NAB + b2] = acc[b2];
     });
+#endif
 }
 
 // FS stages 2 + 3 (axes 1 and 0) for test component I: task (J, a2 b2, a1), J fastest (4
@@ -1135,9 +1179,9 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
             for (int J = 0; J < FF::M; J++)
                 for (int g = 0; g < FM::NG; g++)
                     for (int c = 0; c < FM::ncombo(g); c++) {
-                        const int e = FM::eij(I, J, L::tk(FM::TT.t[FM::combo(g, c, true)].k),
-                                              L::qk(FM::QT.t[FM::combo(g, c, false)].k));
-                        ft.off[I * FF::M + J][FM::cbase(g) + c] = (unsigned char)(e < 0 ? FF::ZSLOT : e);
+                        const int t = FM::TT.t[FM::combo(g, c, true)].k, kq = FM::QT.t[FM::combo(g, c, false)].k;
+                        const int e = FM::eij(I, J, L::tk(t), L::qk(kq));
+                        ft.off[I * FF::M + J][IGA_FS_TK ? t * FF::NQK + kq : FM::cbase(g) + c] = (unsigned char)(e < 0 ? FF::ZSLOT : e);
                     }
     }
     const bool jac = val != nullptr;
