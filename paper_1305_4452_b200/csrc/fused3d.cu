@@ -461,15 +461,23 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
             double acc[NP1];
 #pragma unroll
             for (int b2 = 0; b2 < NP1; b2++) acc[b2] = 0.0;
-            static_for<FM::ncombo(g)>([&](auto CC) {
-                constexpr int c = decltype(CC)::value;
-                constexpr int tu = FM::combo(g, c, true), kb = FM::combo(g, c, false);
-                constexpr int ot = FM::TT.t[tu].o2, ok = FM::QT.t[kb].o2, kq = FM::QT.t[kb].k;
+            // every (test term, trial term) pair of the class pair is a combo (structural zeros
+            // read the zero slot): per trial term, sum over the test terms first
+            static_for<FM::QT.n>([&](auto KB) {
+                constexpr int kb = decltype(KB)::value;
+                if constexpr (FM::cls(FM::KA, FM::QT.t[kb].o0, FM::QT.t[kb].o1) == decltype(KAC)::value) {
+                    constexpr int ok = FM::QT.t[kb].o2, kq = FM::QT.t[kb].k;
 #pragma unroll
-                for (int q2 = 0; q2 < NQ1; q2++) {
-                    const double x = dv[tu][kq][q2] * t2a[q2][ot];
+                    for (int q2 = 0; q2 < NQ1; q2++) {
+                        double y = 0.0;
+                        static_for<FM::TT.n>([&](auto TU) {
+                            constexpr int tu = decltype(TU)::value;
+                            if constexpr (FM::cls(FM::TA, FM::TT.t[tu].o0, FM::TT.t[tu].o1) == ta)
+                                y += dv[tu][kq][q2] * t2a[q2][FM::TT.t[tu].o2];
+                        });
 #pragma unroll
-                    for (int b2 = 0; b2 < NP1; b2++) acc[b2] += x * ut.t[2][q2][ok][b2];
+                        for (int b2 = 0; b2 < NP1; b2++) acc[b2] += y * ut.t[2][q2][ok][b2];
+                    }
                 }
             });
 #pragma unroll
