@@ -549,13 +549,22 @@ __device__ __forceinline__ void fs_stage23(int I, int tid, const double *__restr
                             double z[NP1];
 #pragma unroll
                             for (int b1 = 0; b1 < NP1; b1++) z[b1] = 0.0;
-                            static_for<FM::NG>([&](auto GG) {
-                                constexpr int g = decltype(GG)::value;
-                                if constexpr (FM::in_o0p(g, pp)) {
-                                    constexpr int oa1 = FM::TA.o1[g / NKA], ob1 = FM::KA.o1[g % NKA];
+                            // per trial class of this pair and q1: the test classes (with their
+                            // axis-1 test value) summed before the trial table
+                            static_for<NKA>([&](auto KAC) {
+                                constexpr int ka = decltype(KAC)::value;
+                                if constexpr (FM::KA.o0[ka] == FM::PO.b[pp]) {
+                                    constexpr int ob1 = FM::KA.o1[ka];
 #pragma unroll
                                     for (int q1 = 0; q1 < NQ1; q1++) {
-                                        const double x = X[(g * NQQ + q0 * NQ1 + q1) * NAB] * t1a[q1][oa1];
+                                        double x = 0.0;
+                                        static_for<FM::NTA>([&](auto TAC) {
+                                            constexpr int ta = decltype(TAC)::value;
+                                            if constexpr (FM::TA.o0[ta] == oa) {
+                                                constexpr int g = ta * NKA + ka, oa1 = FM::TA.o1[ta];
+                                                x += X[(g * NQQ + q0 * NQ1 + q1) * NAB] * t1a[q1][oa1];
+                                            }
+                                        });
 #pragma unroll
                                         for (int b1 = 0; b1 < NP1; b1++) z[b1] += x * ut.t[1][q1][ob1][b1];
                                     }
