@@ -146,8 +146,14 @@ struct FsMeta {
 // FS stage-1 coefficient offsets per (I, J) and combo (__grid_constant__); a structurally zero
 // coefficient points at a zero slot of every point's row, so one copy of the stage-1 code serves
 // all 16 blocks with the same work per warp
-template <int NIJ, int NCMB>
-struct alignas(4) FsTab { unsigned char off[NIJ][(NCMB + 3) / 4 * 4]; };   // rows padded to whole words
+template <int NIJ, int NCMB, int NOFF4 = 1>
+struct alignas(4) FsTab {
+    unsigned char off[NIJ][(NCMB + 3) / 4 * 4];   // stage 1: rows padded to whole words
+    unsigned char off4[NOFF4];                     // phase 4: [kq][j][i][t] compact index or 255
+};
+#ifndef IGA_FS_P4
+#define IGA_FS_P4 1   // FS phase 4: one code copy per trial kind, component j = warp at run time
+#endif
 #ifndef IGA_FS_TK
 #define IGA_FS_TK 1   // stage-1 offsets indexed by (test kind, trial kind): the Laplacian's three trial
                       // terms share one coefficient, loaded once
@@ -238,7 +244,7 @@ struct F3 {
         if constexpr (FSC) return IGA_FS_TK ? NTK * NQK : FsMeta<L>::NCMB;
         else return 1;
     }
-    using FT = FsTab<FSC ? M * M : 1, ncmb()>;
+    using FT = FsTab<FSC ? M * M : 1, ncmb(), FSC ? NQK * M * M * NTK : 1>;
     static constexpr size_t SMEM = (size_t)(O_X1 + M * XJS) * sizeof(double);
     // residual only: no coefficient blocks -- row starts (unused) right after the overlay
     static constexpr int O_RS_RES = O_ND + NEN;
@@ -972,7 +978,29 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 }
                 const double dV = sDV[q];
                 double chk = 0.0;
-                {
+                if constexpr (F::FSC && IGA_FS_P4) {
+                    // warp w computes the columns (kq, j = w) of every trial kind kq (M == NWARP)
+                    const int j = warp;
+                    static_for<NQK>([&](auto KQ) {
+                        constexpr int kq = decltype(KQ)::value;
+                        double col[NKS * M];
+                        PH::template dcol_j<3, L::qk(kq)>(st, j, a, b, col);
+                        const unsigned char *o4 = ft.off4 + (kq * M + j) * M * NTK;
+                        static_for<M>([&](auto II) {
+                            constexpr int i = decltype(II)::value;
+                            static_for<NTK>([&](auto TK) {
+                                constexpr int t = decltype(TK)::value;
+                                const int e = o4[i * NTK + t];
+                                if (e != 255) {
+                                    const double v = col[L::tk(t) * M + i] * dV;
+                                    chk += v;
+                                    sD[q * F::DQS + e] = v;
+                                }
+                            });
+                        });
+                    });
+                    if (!isfinite(chk)) errbits |= 2;
+                } else {
                     static_for<NQK * M>([&](auto KJ) {
                         constexpr int kq = decltype(KJ)::value / M, j = decltype(KJ)::value % M;
                         constexpr int k2 = L::qk(kq);
@@ -1199,6 +1227,13 @@ static iga_status run_fused3d(iga_space_s *s, const iga_phys *phys, double a, do
                         const int t = FM::TT.t[FM::combo(g, c, true)].k, kq = FM::QT.t[FM::combo(g, c, false)].k;
                         const int e = FM::eij(I, J, L::tk(t), L::qk(kq));
                         ft.off[I * FF::M + J][IGA_FS_TK ? t * FF::NQK + kq : FM::cbase(g) + c] = (unsigned char)(e < 0 ? FF::ZSLOT : e);
+                    }
+        for (int kq = 0; kq < FF::NQK; kq++)
+            for (int j = 0; j < FF::M; j++)
+                for (int i = 0; i < FF::M; i++)
+                    for (int t = 0; t < FF::NTK; t++) {
+                        const int e = FM::eij(i, j, L::tk(t), L::qk(kq));
+                        ft.off4[((kq * FF::M + j) * FF::M + i) * FF::NTK + t] = (unsigned char)(e < 0 ? 255 : e);
                     }
     }
     const bool jac = val != nullptr;

@@ -349,6 +349,30 @@ struct PhysNSVMS {
             if (k2 == 0) dp = b;
             else if (k2 <= 3) dgp[k2 - 1] = b;
         }
+        dcol_dir<DIM>(s, dut, du, dgu, dlu, dp, dgp, col);
+    }
+    // the same column for a compile-time trial kind K2 and a run-time (warp-uniform) component j:
+    // the direction is built with selects (no dynamically indexed register arrays), so one code copy
+    // serves the four components (the FS kernel's phase 4, fused3d.cu)
+    template <int DIM, int K2>
+    __device__ static inline void dcol_j(const State<DIM> &s, int j, double a, double b, double *col) {
+        double dut[3], du[3], dgu[3][3], dlu[3], dgp[3];
+#pragma unroll
+        for (int x = 0; x < 3; x++) {
+            dut[x] = (K2 == 0 && j == x) ? a : 0.0;
+            du[x] = (K2 == 0 && j == x) ? b : 0.0;
+            dlu[x] = (K2 == 4 && j == x) ? b : 0.0;
+            dgp[x] = (K2 == 1 + x && j == 3) ? b : 0.0;
+#pragma unroll
+            for (int y = 0; y < 3; y++) dgu[x][y] = (K2 == 1 + y && j == x) ? b : 0.0;
+        }
+        const double dp = (K2 == 0 && j == 3) ? b : 0.0;
+        dcol_dir<DIM>(s, dut, du, dgu, dlu, dp, dgp, col);
+    }
+    template <int DIM>
+    __device__ static inline void dcol_dir(const State<DIM> &s, const double (&dut)[3], const double (&du)[3],
+                                           const double (&dgu)[3][3], const double (&dlu)[3], double dp,
+                                           const double (&dgp)[3], double *col) {
         double drM[3];
 #pragma unroll
         for (int i = 0; i < 3; i++)
