@@ -929,6 +929,49 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     t1[q][k] = sTab[((1 * NQ1 + q) * 3 + k) * NP1 + a1];
                     t2[q][k] = sTab[((2 * NQ1 + q) * 3 + k) * NP1 + a2];
                 }
+            // residual kinds common to all components (r~ entry rr = rbase(c) + i): one code copy
+            // with I = warp at run time (IGA_FS_P4), else one copy per component
+            constexpr bool RUNI = [] {
+                for (int c = 0; c < KS::NC; c++) {
+                    int n = 0;
+                    for (int i = 0; i < M; i++) n += L::crmask(c, i);
+                    if (n != 0 && n != M) return false;
+                }
+                for (int r = 0; r < NR; r++) {
+                    int base = 0;
+                    for (int c = 0; c < L::R.c[r]; c++) base += L::crmask(c, 0) ? M : 0;
+                    if (r != base + L::R.i[r]) return false;
+                }
+                return true;
+            }();
+            if constexpr (RUNI && IGA_FS_P4 && F::FSC) {
+                const int I = warp;
+                double acc = 0.0;
+                static_for<KS::NC>([&](auto CC) {
+                    constexpr int c = decltype(CC)::value;
+                    if constexpr (L::crmask(c, 0)) {
+                        constexpr int rb = [] { int b = 0; for (int x = 0; x < c; x++) b += L::crmask(x, 0) ? M : 0; return b; }();
+                        const double *Rr = sR + (rb + I) * NQ;
+                        static_for<KS::nterms(c)>([&](auto TT) {
+                            constexpr int t = decltype(TT)::value;
+                            constexpr int o0 = KS::ord(c, t, 0), o1 = KS::ord(c, t, 1), o2 = KS::ord(c, t, 2);
+#pragma unroll
+                            for (int q0 = 0; q0 < NQ1; q0++) {
+                                double s1 = 0.0;
+#pragma unroll
+                                for (int q1 = 0; q1 < NQ1; q1++) {
+                                    double s2 = 0.0;
+#pragma unroll
+                                    for (int q2 = 0; q2 < NQ1; q2++) s2 += t2[q2][o2] * Rr[(q0 * NQ1 + q1) * NQ1 + q2];
+                                    s1 += t1[q1][o1] * s2;
+                                }
+                                acc += t0[q0][o0] * s1;
+                            }
+                        });
+                    }
+                });
+                atomicAdd(Fout + sNode[A] * M + I, acc);
+            } else
             static_for<M>([&](auto II) {
                 constexpr int I = decltype(II)::value;
                 if (warp == I) {
