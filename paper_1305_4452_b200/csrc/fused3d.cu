@@ -151,6 +151,9 @@ struct alignas(4) FsTab {
     unsigned char off[NIJ][(NCMB + 3) / 4 * 4];   // stage 1: rows padded to whole words
     unsigned char off4[NOFF4];                     // phase 4: [kq][j][i][t] compact index or 255
 };
+#ifndef IGA_FS_ALL
+#define IGA_FS_ALL 1   // FS stage 1: all coefficient loads of a block issued before the classes
+#endif
 #ifndef IGA_FS_P4
 #define IGA_FS_P4 1   // FS phase 4: one code copy per trial kind, component j = warp at run time
 #endif
@@ -448,8 +451,22 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
 #if IGA_FS_TK
     // per test class: each (test term, trial kind) coefficient at the three q2 loaded once into
     // registers (the Laplacian's three trial terms share it), then the class's groups
+#if IGA_FS_ALL
+    // all of the block's coefficients issued up front (60 loads for VMS), then the classes
+    double dv[FM::TT.n][F::NQK][NQ1];
+    static_for<FM::TT.n>([&](auto TU) {
+        constexpr int tu = decltype(TU)::value;
+        static_for<F::NQK>([&](auto KQ) {
+            constexpr int kq = decltype(KQ)::value;
+            const int e = off[FM::TT.t[tu].k * F::NQK + kq];
+#pragma unroll
+            for (int q2 = 0; q2 < NQ1; q2++) dv[tu][kq][q2] = Dq[q2 * F::DQS + e];
+        });
+    });
+#endif
     static_for<FM::NTA>([&](auto TAC) {
         constexpr int ta = decltype(TAC)::value;
+#if !IGA_FS_ALL
         double dv[FM::TT.n][F::NQK][NQ1];
         static_for<FM::TT.n>([&](auto TU) {
             constexpr int tu = decltype(TU)::value;
@@ -462,6 +479,7 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
                 });
             }
         });
+#endif
         static_for<FM::NKA>([&](auto KAC) {
             constexpr int g = ta * FM::NKA + decltype(KAC)::value;
             double acc[NP1];
