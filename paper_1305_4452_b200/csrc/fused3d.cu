@@ -36,6 +36,9 @@
 #ifndef IGA_DYN
 #define IGA_DYN 1    // dynamic element order through a global counter (see the element loop)
 #endif
+#ifndef IGA_PREF
+#define IGA_PREF 1   // next element claimed at the start of the current one (counter latency hidden)
+#endif
 #ifndef IGA_BAL
 #define IGA_BAL 1   // column tasks dealt round-robin over all threads (phase 5, non-symmetric forms)
 #endif
@@ -220,9 +223,15 @@ struct F3 {
     static constexpr int O_PHI = O_D;                        // [NQ][M][NKS+1]     } overlay D
     static constexpr int O_U = O_PHI + NQ * M * (NKS + 1);   // [NEN][M]            } (dead before
     static constexpr int O_UD = O_U + NEN * M;               // [NEN][M]            }  phase 4)
-    static constexpr int O_R = O_UD + NEN * M;               // [NR][NQ]            }
-    static constexpr int O_ND = O_R + NR * NQ;               // long long [NEN]     }
-    static constexpr int OVL = O_ND + NEN - O_D;             // overlay extent
+    static constexpr int O_RA = O_UD + NEN * M;              // [NR][NQ]            }
+    static constexpr int O_NDA = O_RA + NR * NQ;             // long long [NEN]     }
+    // FS (IGA_NB3): R and the node numbers overlay the stage-1 output X1 instead of D (X1 is
+    // first written after phase 4), so phase 4 needs no barrier after the residual F_e
+#ifndef IGA_NB3
+#define IGA_NB3 1
+#endif
+    static constexpr bool RX1 = FSC && IGA_NB3;
+    static constexpr int OVL = (RX1 ? O_RA : O_NDA + NEN) - O_D;   // overlay extent
     static constexpr int O_RS = O_D + (NQ * DQS > OVL ? NQ * DQS : OVL);   // long long [NEN*M] row starts
 #ifndef IGA_PBS
 #define IGA_PBS 0
@@ -243,6 +252,8 @@ struct F3 {
     }
     static constexpr int XJS = xjs();
     static constexpr int O_X1 = O_PB + (PBS ? NQ * NQK * NEN : 0);
+    static constexpr int O_R = RX1 ? O_X1 : O_RA;
+    static constexpr int O_ND = RX1 ? O_X1 + NR * NQ : O_NDA;
     static constexpr int ncmb() {
         if constexpr (FSC) return IGA_FS_TK ? NTK * NQK : FsMeta<L>::NCMB;
         else return 1;
@@ -253,6 +264,7 @@ struct F3 {
     static constexpr int O_RS_RES = O_ND + NEN;
     static constexpr size_t SMEM_RES = (size_t)(O_RS_RES + NEN * M) * sizeof(double);
     static_assert(NQ * M * (NKS + 1) <= NQ * DQS, "Phi must fit in the D region");
+    static_assert(!RX1 || NR * NQ + NEN <= M * XJS, "R and the node numbers must fit the X1 region");
 };
 
 // test-side sum factorisation in 3D of one column (trial function B = (b0,b1,b2), pair ij):
@@ -705,7 +717,10 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     // hundreds of pencils over ~7000 elements each: DRAM traffic was independent of bw, 5.8-6.8x
     // the algorithmic bytes).
     __shared__ long long sEl;
+    long long nxt = 0;
     for (long long el = blockIdx.x; el < nelem;) {
+        // IGA_PREF: claim the next element now; the counter's round trip overlaps this element
+        if (IGA_DYN && IGA_PREF && tid == 0) nxt = (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
         // L2-blocked element order: pencils along axis 2, swept over axis 0 inside blocks of `bw`
         // pencils along axis 1, so the CSR rows an element layer leaves half-accumulated are
         // still in L2 when the next layer adds to them (the red.add scatter then reads each
@@ -1021,7 +1036,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 }
             });
         }
-        if constexpr (JAC) __syncthreads();          // F_e read R / sNode: both overlay D
+        if constexpr (JAC && !F::RX1) __syncthreads();   // F_e read R / sNode: both overlay D
 
         // ---- 4. Jacobian coefficients: warp-uniform trial column (k2 = qk(kq), j), lane = q ----
         if constexpr (JAC) {
@@ -1122,7 +1137,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     fs_stage1<F, P>(I, warp, sD, sTab, sX1, ut, ft, lane);
                     __syncthreads();
                     fs_stage23<F, P>(I, tid, sX1, sTab, sPosE, sW, sRS, val, ut, dbg);
-                    __syncthreads();
+                    if (I + 1 < M || !IGA_PREF) __syncthreads();   // the last one: the end-of-element barrier
                 }
             } else
             // ---- 5. test-side sum factorisation + coalesced emission ----
@@ -1250,7 +1265,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             }
         }
         if constexpr (IGA_DYN) {
-            if (tid == 0) sEl = (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
+            if (tid == 0) sEl = IGA_PREF ? nxt : (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
             __syncthreads();
             el = sEl;
         } else {
