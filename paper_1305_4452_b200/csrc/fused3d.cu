@@ -717,10 +717,12 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
     // hundreds of pencils over ~7000 elements each: DRAM traffic was independent of bw, 5.8-6.8x
     // the algorithmic bytes).
     __shared__ long long sEl;
+    // IGA_PREF on the FS kernel only (3D Cahn-Hilliard: A/B 147.0 vs 140.8 ms with it)
+    constexpr bool PREF = IGA_PREF && F::FSC;
     long long nxt = 0;
     for (long long el = blockIdx.x; el < nelem;) {
         // IGA_PREF: claim the next element now; the counter's round trip overlaps this element
-        if (IGA_DYN && IGA_PREF && tid == 0) nxt = (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
+        if (IGA_DYN && PREF && tid == 0) nxt = (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
         // L2-blocked element order: pencils along axis 2, swept over axis 0 inside blocks of `bw`
         // pencils along axis 1, so the CSR rows an element layer leaves half-accumulated are
         // still in L2 when the next layer adds to them (the red.add scatter then reads each
@@ -1137,7 +1139,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     fs_stage1<F, P>(I, warp, sD, sTab, sX1, ut, ft, lane);
                     __syncthreads();
                     fs_stage23<F, P>(I, tid, sX1, sTab, sPosE, sW, sRS, val, ut, dbg);
-                    if (I + 1 < M || !IGA_PREF) __syncthreads();   // the last one: the end-of-element barrier
+                    if (I + 1 < M || !PREF) __syncthreads();   // the last one: the end-of-element barrier
                 }
             } else
             // ---- 5. test-side sum factorisation + coalesced emission ----
@@ -1265,7 +1267,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             }
         }
         if constexpr (IGA_DYN) {
-            if (tid == 0) sEl = IGA_PREF ? nxt : (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
+            if (tid == 0) sEl = PREF ? nxt : (long long)gridDim.x + (long long)atomicAdd(s.wq, 1ULL);
             __syncthreads();
             el = sEl;
         } else {

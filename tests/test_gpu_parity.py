@@ -289,3 +289,27 @@ def test_rerun_spread_bounded(cid, n):
     for vals, F in runs[1:]:
         assert rowmax_rel_err(rpn, v0, vals.cpu().numpy()) <= 1e-14
         assert vec_rel_err(runs[0][1].cpu().numpy(), F.cpu().numpy()) <= 1e-14
+
+
+@pytest.mark.parametrize("cid,n,offset", [(5, 7, 1), (5, 7, 2), (8, 6, 1)])
+def test_unaligned_values_buffer(cid, n, offset):
+    """The caller's CSR value buffer may start at any 8-byte boundary (iga.h: plain double
+    pointer): a view `offset` doubles into a larger allocation gives the same values as the
+    oracle.  On the uniform VMS path the element rows are added by 96-byte bulk reductions that
+    need 16-byte alignment; an unaligned buffer takes the scalar red.add fallback."""
+    iga = _gpu()
+    w = workloads.make(cid, n=n)
+    sp = iga.Space.from_workload(w)
+    dev = torch.device("cuda", 0)
+    ph = iga.make_phys(w.phys, w.params)
+    big = torch.full((sp.nnz + 4,), float("nan"), dtype=torch.float64, device=dev)
+    view = big[offset:offset + sp.nnz]
+    assert view.data_ptr() % 16 == (8 if offset % 2 else 0)
+    sp.form_jacobian(ph, w.a, w.b, torch.from_numpy(w.U).to(dev), torch.from_numpy(w.Udot).to(dev), vals=view)
+    sp.check()
+    torch.cuda.synchronize()
+    osp = oracle.Space.from_workload(w)
+    K, T, _ = osp.assemble_dense(w.phys, w.params, w.a, w.b, w.U, w.Udot)
+    orp, _, ovals = oracle.dense_to_csr(K, T)
+    assert rowmax_rel_err(orp, ovals, view.cpu().numpy()) <= ROW_TOL
+    assert torch.isnan(big[:offset]).all() and torch.isnan(big[offset + sp.nnz:]).all()   # nothing outside
