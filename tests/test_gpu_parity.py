@@ -295,8 +295,8 @@ def test_rerun_spread_bounded(cid, n):
 def test_unaligned_values_buffer(cid, n, offset):
     """The caller's CSR value buffer may start at any 8-byte boundary (iga.h: plain double
     pointer): a view `offset` doubles into a larger allocation gives the same values as the
-    oracle.  On the uniform VMS path the element rows are added by 96-byte bulk reductions that
-    need 16-byte alignment; an unaligned buffer takes the scalar red.add fallback."""
+    oracle, and nothing outside the view is written (the scatter's red.add needs only 8-byte
+    alignment; a 16-byte bulk-reduction scatter was tried and would need a fallback here)."""
     iga = _gpu()
     w = workloads.make(cid, n=n)
     sp = iga.Space.from_workload(w)
