@@ -199,13 +199,22 @@ struct F3 {
     using State = typename PH::template State<3>;
     static constexpr int STD = (sizeof(State) + 7) / 8;      // doubles per state
     // symmetric element Jacobian (hyperelastic tangent, major symmetry): contract blocks I <= J
-    static constexpr bool SYMJ = std::is_same<PH, PhysNeoHooke>::value;
+#ifndef IGA_NH_SYM
+#define IGA_NH_SYM 1
+#endif
+    static constexpr bool SYMJ = std::is_same<PH, PhysNeoHooke>::value && IGA_NH_SYM;
     // resident CTAs per SM the register budget is sized for (m = 3: 96 threads -> 3 CTAs; m = 1:
     // one-warp CTAs (27 trial functions), 8 per SM)
 #ifndef IGA_VMS_MINB
 #define IGA_VMS_MINB 2
 #endif
-    static constexpr int MINB = M == 1 ? 8 : M == 3 ? 3 : IGA_VMS_MINB;
+#ifndef IGA_NH_MINB
+#define IGA_NH_MINB 3
+#endif
+#ifndef IGA_NH_HOIST
+#define IGA_NH_HOIST 0
+#endif
+    static constexpr int MINB = M == 1 ? 8 : M == 3 ? IGA_NH_MINB : IGA_VMS_MINB;
     // doubles of the per-point state that the Jacobian coefficients read (the leading members;
     // VMS keeps its residual coefficients rN, rG after them): only these go to shared memory
     static constexpr int STJ = PhysJState<PH>::value > 0 ? PhysJState<PH>::value : STD;
@@ -279,7 +288,7 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
     using KS = typename F::KS;
     constexpr int NP1 = F::NP1, NQ1 = F::NQ1, NEN = F::NEN, NTK = F::NTK, NQK = F::NQK, DB = F::DB;
     // Neo-Hooke runs 3 CTAs/SM at the 168-register cap: hoisting spills there (A/B +6 %)
-    constexpr int HOIST = F::M == 3 ? 0 : IGA_HOIST;
+    constexpr int HOIST = F::M == 3 ? IGA_NH_HOIST : IGA_HOIST;
     auto T = [&](int d, int q, int k, int a) -> double {
         if constexpr (UNI) return ut.t[d][q][k][a];
         else return tab[((d * NQ1 + q) * 3 + k) * NP1 + a];
