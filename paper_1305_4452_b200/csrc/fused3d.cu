@@ -39,6 +39,9 @@
 #ifndef IGA_PREF
 #define IGA_PREF 1   // next element claimed at the start of the current one (counter latency hidden)
 #endif
+#ifndef IGA_RS3
+#define IGA_RS3 1    // row starts computed by warps 1.. during phase 3 (uniform knots; one barrier per element fewer)
+#endif
 #ifndef IGA_BAL
 #define IGA_BAL 1   // column tasks dealt round-robin over all threads (phase 5, non-symmetric forms)
 #endif
@@ -154,6 +157,13 @@ struct alignas(4) FsTab {
     unsigned char off[NIJ][(NCMB + 3) / 4 * 4];   // stage 1: rows padded to whole words
     unsigned char off4[NOFF4];                     // phase 4: [kq][j][i][t] compact index or 255
 };
+#ifndef IGA_FS_BS1
+#define IGA_FS_BS1 5   // FS loop: the barrier protecting X1 sits inside stage 1, after the arithmetic of its
+                       // first IGA_FS_BS1 groups (held in registers; 5 = the first test class) and before
+                       // their stores: the coefficient loads and a third of the stage overlap the wait for
+                       // the slowest stage-2+3 warp.  Config 5 A/B: 0: 136.45, 1: 134.95, 3: 135.3,
+                       // 5: 134.6, 8: 136.6 ms
+#endif
 #ifndef IGA_FS_ALL
 #define IGA_FS_ALL 1   // FS stage 1: all coefficient loads of a block issued before the classes
 #endif
@@ -165,6 +175,9 @@ struct alignas(4) FsTab {
                       // terms share one coefficient, loaded once
 #endif
 
+#if IGA_FS_BS1 && !IGA_FS_TK
+#error "IGA_FS_BS1 needs the IGA_FS_TK form of stage 1"
+#endif
 // FS is used for the uniform-table kernels whose CTA has one warp per trial component.  On for
 // VMS (m = 4, 128 threads).  Neo-Hooke (m = 3) has uniform tables only on periodic meshes (config
 // 4 is open: never reached, untested); 3D Cahn-Hilliard (m = 1): A/B config 8 149.9 vs 140.8 ms,
@@ -456,10 +469,19 @@ __device__ __forceinline__ void tsf_column_3d(double (&Kc)[F::NEN], const double
 template <class F, int P>
 __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict__ sD, const double *__restrict__ sTab,
                                           double *__restrict__ sX1, const UniTab<P> &ut, const typename F::FT &ft,
-                                          int lane) {
+                                          int lane_, bool bar = false) {
     using FM = FsMeta<typename F::L>;
     constexpr int NQ1 = F::NQ1, NP1 = F::NP1, NQQ = NQ1 * NQ1, NAB = NP1 * NP1;
+#if IGA_FS_BS1
+    // every lane runs the stage (idle lanes on lane 0's operands, stores predicated) so that the
+    // CTA barrier protecting X1 can sit between the first group's arithmetic and its stores
+    const bool act = lane_ < NQQ * NP1;
+    const int lane = act ? lane_ : 0;
+#else
+    const int lane = lane_;
+    constexpr bool act = true;
     if (lane >= NQQ * NP1) return;
+#endif
     const int q01 = lane / NP1, a2 = lane - q01 * NP1;
     double t2a[NQ1][3];                                  // test values on axis 2 (unused orders are dead)
 #pragma unroll
@@ -484,6 +506,10 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
             for (int q2 = 0; q2 < NQ1; q2++) dv[tu][kq][q2] = Dq[q2 * F::DQS + e];
         });
     });
+#endif
+#if IGA_FS_BS1
+    static_assert(IGA_FS_BS1 <= FM::NG, "IGA_FS_BS1: groups held before the barrier");
+    double hold[IGA_FS_BS1][NP1];
 #endif
     static_for<FM::NTA>([&](auto TAC) {
         constexpr int ta = decltype(TAC)::value;
@@ -525,8 +551,26 @@ __device__ __forceinline__ void fs_stage1(int I, int J, const double *__restrict
                     }
                 }
             });
+#if IGA_FS_BS1
+            // the first IGA_FS_BS1 groups are held in registers until the barrier
+            if constexpr (g < IGA_FS_BS1) {
 #pragma unroll
-            for (int b2 = 0; b2 < NP1; b2++) dst[g * NQQ * NAB + b2] = acc[b2];
+                for (int b2 = 0; b2 < NP1; b2++) hold[g][b2] = acc[b2];
+                if constexpr (g == IGA_FS_BS1 - 1) {
+                    if (bar) __syncthreads();            // all stage-2+3 reads of the previous X1 are done
+                    if (act) {
+#pragma unroll
+                        for (int h = 0; h < IGA_FS_BS1; h++)
+#pragma unroll
+                            for (int b2 = 0; b2 < NP1; b2++) dst[h * NQQ * NAB + b2] = hold[h][b2];
+                    }
+                }
+            } else
+#endif
+            if (act) {
+#pragma unroll
+                for (int b2 = 0; b2 < NP1; b2++) dst[g * NQQ * NAB + b2] = acc[b2];
+            }
         });
     });
     (void)FM::NCMB;
@@ -808,8 +852,12 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
             }
         }
         __syncthreads();
-        {
-            for (int i = tid; i < NEN * M; i += NTH) {
+        // node numbers and closed-form row starts (and U_e on non-uniform knots).  IGA_RS3 with
+        // uniform knots: nothing before phase 3b reads them, so warps 1.. compute them during
+        // phase 3 (whose 27 points occupy warp 0 only) and the barrier after this pass is dropped
+        constexpr bool RS3 = IGA_RS3 && NTH > 32;
+        auto row_starts = [&](int i0, int stride) {
+            for (int i = i0; i < NEN * M; i += stride) {
                 {
                     const int k = i, A = k / M, m = k - A * M;
                     const int a0 = A / (NP1 * NP1), a1 = (A / NP1) % NP1, a2 = A % NP1;
@@ -834,8 +882,11 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                     }
                 }
             }
+        };
+        if (!(RS3 && uni_knots)) {
+            row_starts(tid, NTH);
+            __syncthreads();
         }
-        __syncthreads();
 
         // ---- 2. field kinds per (q, m), sum factorised over the element's functions:
         //         Phi_k(q) = sum_a0 T0 (sum_a1 T1 (sum_a2 T2 U)) per separable term of kind k ----
@@ -912,6 +963,7 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         __syncthreads();
 
         // ---- 3. per-point state + residual coefficients ----
+        if (RS3 && uni_knots && tid >= 32) row_starts(tid - 32, NTH - 32);
         if (tid < NQ && !(dbg & 8)) {
             const int q = tid;
             const int q0 = q / (NQ1 * NQ1), q1 = (q / NQ1) % NQ1, q2 = q % NQ1;
@@ -1145,10 +1197,17 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 double *sX1 = sm + F::O_X1;
 #pragma unroll 1
                 for (int I = 0; I < M; I++) {
+#if IGA_FS_BS1
+                    fs_stage1<F, P>(I, warp, sD, sTab, sX1, ut, ft, lane, I > 0);
+                    __syncthreads();
+                    fs_stage23<F, P>(I, tid, sX1, sTab, sPosE, sW, sRS, val, ut, dbg);
+                    if (I + 1 == M && !PREF) __syncthreads();  // the last one: the end-of-element barrier
+#else
                     fs_stage1<F, P>(I, warp, sD, sTab, sX1, ut, ft, lane);
                     __syncthreads();
                     fs_stage23<F, P>(I, tid, sX1, sTab, sPosE, sW, sRS, val, ut, dbg);
                     if (I + 1 < M || !PREF) __syncthreads();   // the last one: the end-of-element barrier
+#endif
                 }
             } else
             // ---- 5. test-side sum factorisation + coalesced emission ----
