@@ -39,6 +39,9 @@
 #ifndef IGA_PREF
 #define IGA_PREF 1   // next element claimed at the start of the current one (counter latency hidden)
 #endif
+#ifndef IGA_UFIRST
+#define IGA_UFIRST 1  // staging: U_e / Udot_e loads issued before the table / position items (config 8 140.9 -> 138.0 ms, config 5 132.85 -> 132.2 ms)
+#endif
 #ifndef IGA_RS3
 #define IGA_RS3 1    // row starts computed by warps 1.. during phase 3 (uniform knots; one barrier per element fewer)
 #endif
@@ -794,7 +797,30 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
         auto EL = [&](int d) { return d == 0 ? e[0] : (d == 1 ? e[1] : e[2]); };   // no local-memory indexing
         // ---- 1. stage: tables, per-axis function data, position tables, and (uniform knots:
         //         first[e] = first0 + e, no dependent load) U_e -- one global round trip ----
+#if IGA_UFIRST
+        // the U_e / Udot_e loads are issued first, into registers, and stored after the loop: the
+        // loop's own global loads (positions, row widths, segment prefixes) share their round trip
+        // instead of preceding it
+        static_assert(NEN * M <= NTH, "one U_e entry per thread");
+        const int nU1 = 0;
+        const bool uld = uni_knots && tid < NEN * M;
+        double pu = 0.0, pud = 0.0;
+        if (uld) {
+            const int A = tid / M, m = tid - A * M;
+            int g[3];
+#pragma unroll
+            for (int d = 0; d < 3; d++) {
+                const int aa = d == 0 ? A / (NP1 * NP1) : d == 1 ? (A / NP1) % NP1 : A % NP1;
+                g[d] = s.ax[d].first0 + EL(d) + aa;
+                if (g[d] >= s.ax[d].nu) g[d] -= s.ax[d].nu;
+            }
+            const long long node = local_node(s, g[0], g[1], g[2]);
+            pu = U[node * M + m];
+            pud = Ud ? Ud[node * M + m] : 0.0;
+        }
+#else
         const int nU1 = uni_knots ? NEN * M : 0;
+#endif
         for (int i = tid; i < 3 * NQ1 * 3 * NP1 + 6 * NQ1 + 3 + 3 * NP1 + 3 * NP1 * NP1 + nU1; i += NTH) {
             int k = i;
             if (k < 3 * NQ1 * 3 * NP1) {
@@ -851,6 +877,12 @@ k_fused3d(SpaceDev s, Prm prm, double a, double b, const double *__restrict__ U,
                 sSeg[k] = l >= s.ax[d].n_own;
             }
         }
+#if IGA_UFIRST
+        if (uld) {
+            sU[tid] = pu;
+            sUd[tid] = pud;
+        }
+#endif
         __syncthreads();
         // node numbers and closed-form row starts (and U_e on non-uniform knots).  IGA_RS3 with
         // uniform knots: nothing before phase 3b reads them, so warps 1.. compute them during
